@@ -1,0 +1,170 @@
+/*
+ * bfla.h — C ABI of the B200 (sm_100a) BFLA hot path.  ABI version 1.
+ *
+ * Block-Filtered Long-Context Attention (arXiv 2605.12193).  Citations "P:n" are lines of the
+ * paper's text; "Eq. k" its equations; R1..R21 the readings listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA tensors) unless stated.
+ *    The caller owns every buffer; the library never allocates, frees, or keeps a pointer past
+ *    the work it enqueues.  Parameter structs are read before the call returns.
+ *  - All work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy stream).
+ *    No entry point synchronises the device.
+ *  - Validation is synchronous and happens before any launch: on a non-OK status nothing has
+ *    been enqueued and outputs are untouched.  Faults inside kernels surface at the caller's
+ *    next synchronisation as a CUDA error.
+ *  - Identical inputs give identical output bits (masks, lists, O, LSE): no atomics decide any
+ *    value (atomics only accumulate integer statistics).
+ *  - Calls are reentrant; there is no global mutable state except the thread-local detail
+ *    string of bfla_last_error().
+ *  - Element strides are in ELEMENTS (bf16 = 2 bytes); the head_dim axis must be contiguous.
+ */
+#ifndef BFLA_H_
+#define BFLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BFLA_ABI_VERSION 1
+
+typedef enum {
+    BFLA_OK = 0,
+    BFLA_ERR_INVALID_ARGUMENT = 1, /* a paper invariant is violated: Hq % Hkv != 0 (Eq. 3), Nq > Nkv or
+                                      Nq < 1 (Eq. 11, N_c >= 0), b/g/T not powers of two, g does not divide b
+                                      (Eq. 6), T does not divide b (Eq. 19), gamma not in (0,1] (Eq. 17),
+                                      keep_ratio not in (0,1], rho not in [0,1] (Eq. 25), eta < 0, n_local < 0,
+                                      n_sink < 0, NULL required pointer                                       */
+    BFLA_ERR_UNSUPPORTED = 2,      /* valid but not built: head_dim not in {128, 256}, T != 64, G = b/g > 8,
+                                      FLATTEN with non-contiguous tokens, page_size not in {16, 32, 64}     */
+    BFLA_ERR_MISALIGNED = 3,       /* TMA rules: base address % 16 B, strides % 16 B                         */
+    BFLA_ERR_WORKSPACE = 4,        /* ws_bytes < bfla_workspace_size(...) or ws == NULL                       */
+    BFLA_ERR_CAPACITY = 5,         /* mask->tile_list_capacity < bfla_tile_list_capacity(...)                */
+    BFLA_ERR_CUDA = 6              /* a CUDA runtime/driver call failed; detail in bfla_last_error()          */
+} bfla_status;
+
+enum { BFLA_KV_CONTIGUOUS = 0, BFLA_KV_PAGED = 1 };
+/* Stage-1 pooling (R1): FLATTEN = flattening-g pooling + max over group pairs (Eq. 6-10, the
+   paper's operator, default); MEAN = per-block mean of Q and of K, one dot product per block pair
+   (the north_star's wording; an HBM-bound variant). */
+enum { BFLA_POOL_FLATTEN = 0, BFLA_POOL_MEAN = 1 };
+/* Stage-1 selection: MASS = smallest prefix with mass >= gamma (Eq. 16-18); RATIO = the top
+   ceil(keep_ratio * n_causal) blocks per row (north_star's "keep ratio", R9). */
+enum { BFLA_SELECT_MASS = 0, BFLA_SELECT_RATIO = 1 };
+
+/* One attention layer call: Q/K/V in the paper's head-first layout (Eq. 2), GQA m = h_q / h_kv
+   (Eq. 3), head group H_h = {h m, ..., h m + m - 1} (Eq. 8); the batch index is the paper's
+   request index r (Eq. 20, 27).  N_c = n_kv - n_q (Eq. 11): chunked prefill is a request whose
+   query chunk is the LAST n_q tokens of its n_kv-token KV sequence (uniform over the batch). */
+typedef struct {
+    int32_t batch, h_q, h_kv, head_dim;
+    int32_t n_q, n_kv;
+    float softmax_scale;   /* <= 0 -> 1/sqrt(head_dim) (Eq. 1, Eq. 27)                                 */
+    int32_t head_offset;   /* global index of local KV head 0 (a multi-GPU shard passes rank*h_kv);
+                              used only by psi (Eq. 25) so sharded masks equal unsharded ones       */
+    const void* q;         /* bf16 [batch][h_q][n_q][head_dim] with element strides q_stride        */
+    int64_t q_stride[3];   /* (batch, head, token); head_dim contiguous                                */
+    void* o;               /* bf16 output, same shape as q, strides o_stride                           */
+    int64_t o_stride[3];
+    float* lse;            /* optional fp32 [batch][h_q][n_q] natural-log LSE of the scaled scores
+                              over the attended keys; NULL = not written                               */
+    int32_t kv_layout;     /* BFLA_KV_CONTIGUOUS | BFLA_KV_PAGED                                       */
+    const void* k;         /* contiguous: bf16 [batch][h_kv][n_kv][head_dim] with strides kv_stride;
+                              paged (vLLM): bf16 [num_pages][page_size][h_kv][head_dim], dense      */
+    const void* v;
+    int64_t kv_stride[3];  /* contiguous only: (batch, head, token)                                    */
+    int32_t page_size, num_pages, max_pages_per_seq;
+    const int32_t* page_table; /* paged only: device int32 [batch][max_pages_per_seq], logical page
+                                  n of request r lives at physical page page_table[r][n]           */
+} bfla_problem;
+
+/* Method knobs.  Defaults of the paper's strong operating point:
+   b=256, g=64, gamma=0.99, n_local=8, rho=0, eta=16; T=64 and n_sink=1 are our readings (R10, R12). */
+typedef struct {
+    int32_t block_b;    /* b: coarse block size (Eq. 4), power of two                                   */
+    int32_t group_g;    /* g: flattening group (Eq. 6), power of two dividing b; G = b/g <= 8 built    */
+    int32_t tile_t;     /* T: attention tile (Eq. 19), divides b; 64 built                              */
+    int32_t pool;       /* BFLA_POOL_*                                                                  */
+    int32_t select;     /* BFLA_SELECT_*                                                                */
+    float gamma;        /* mass threshold (Eq. 17), (0, 1]; 1 keeps every causal block (R7)           */
+    float keep_ratio;   /* (0, 1], used when select == RATIO                                           */
+    int32_t n_sink;     /* sink tile columns (Eq. 22, R12)                                              */
+    int32_t n_local;    /* band width in tiles (Eq. 21, R11): tiles [d_i - n_local, d_i]              */
+    int32_t eta;        /* stride-rescue period (Eq. 24); 0 = off                                      */
+    float rho;          /* random-rescue probability (Eq. 25), [0, 1]                                  */
+    uint64_t seed;      /* s of Eq. 24-25                                                               */
+} bfla_config;
+
+/* Statistics, accumulated with integer atomics (values are order independent). */
+typedef struct {
+    uint64_t causal_tiles;    /* sum over (r, h) of causal tiles (R20, kappa denominator)             */
+    uint64_t kept_tiles;      /* sum of kept tiles (kappa numerator)                                   */
+    uint64_t label[6];        /* kept tiles by provenance: [1] mass [2] sink [3] band [4] stride [5] random */
+    uint64_t rows;            /* Stage-1 rows (r, p, i)                                                */
+    uint64_t rows_exact_tie;  /* rows whose cut falls between two equal probabilities (R6, reported)  */
+    uint64_t blocks_kept;     /* sum over rows of r* (blocks kept per query head before the OR)       */
+    uint64_t reserved[5];
+} bfla_stats;
+
+/* Caller-owned device buffers written by Stage 1 / Stage 2.  Shapes use
+   Lq = ceil(n_q/b), Lkv = ceil(n_kv/b), Tq = ceil(n_q/T), Tkv = ceil(n_kv/T). */
+typedef struct {
+    uint32_t* coarse_bits;  /* [batch][h_kv][Lq][ceil(Lkv/32)]: Eq. 18 after the OR over H_h (R8);
+                               bit j%32 of word j/32                                              */
+    uint32_t* tile_bits;    /* [batch][h_kv][Tq][ceil(Tkv/32)]: final M^tile (Eq. 26)             */
+    int32_t* tile_list;     /* kept KV tile indices, ascending j; row (r,h,i) starts at
+                               ((r*h_kv + h) * C + c_i) where C = causal tiles per (r,h) and
+                               c_i = causal tiles of rows < i (closed form, no scan)            */
+    int64_t tile_list_capacity; /* entries available in tile_list                              */
+    int32_t* tile_count;    /* [batch][h_kv][Tq]: kept tiles per row                                  */
+    uint8_t* tile_label;    /* optional [batch][h_kv][Tq][Tkv]: 0 drop/non-causal, 1 mass, 2 sink,
+                               3 band, 4 stride, 5 random (precedence in that order, R13)          */
+    float* kept_mass;       /* optional [batch][h_q][Lq]: sum of kept A (Eq. 17 check)               */
+    bfla_stats* stats;      /* optional device bfla_stats (zeroed by bfla_block_mask)                */
+} bfla_mask;
+
+/* Bytes of device scratch the entry points need for (problem, config). */
+size_t bfla_workspace_size(const bfla_problem* problem, const bfla_config* config);
+/* Entries tile_list must hold: batch * h_kv * (causal tiles per (r,h)). */
+int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* config);
+
+/* Stage 1 (Eq. 4-18 + GQA OR): pooling, block scores (Eq. 9-10), causal mask (Eq. 11-14),
+   block softmax with alpha = 1/sqrt(head_dim) (Eq. 15), keep-mass / keep-ratio selection
+   (Eq. 16-18), OR over each head group.  Writes mask->coarse_bits (+ kept_mass, stats).
+   Arithmetic follows the canonical fp32 order of DESIGN.md §4, so coarse_bits are bit-exact
+   against the CPU oracle. */
+bfla_status bfla_block_mask(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Stage 2 (Eq. 19-26): expansion to the T-tile grid with tile causality, local band
+   (Eq. 21, R11), sink (Eq. 22, R12), stride rescue (Eq. 24) and random rescue (Eq. 25) of the
+   dropped set (Eq. 23), final union (Eq. 26, R16).  Reads mask->coarse_bits; writes tile_bits,
+   tile_list, tile_count (+ tile_label, stats).  Integer only: bit-exact by construction. */
+bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/* Fused sparse causal prefill (Eq. 27): for every (r, h, query tile i) and all m query
+   heads of H_h, exact online-softmax attention over the kept KV tiles of mask->tile_list (ascending
+   j), token-exact causal masking inside frontier tiles, dropped tiles contribute nothing.  Writes
+   problem->o (+ lse).  tcgen05/TMEM/TMA kernel, bf16 in, fp32 accumulation, P rounded to bf16. */
+bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                void* ws, size_t ws_bytes, void* stream);
+
+/* The whole path: Stage 1 -> Stage 2 -> sparse prefill.  config == NULL runs DENSE causal attention
+   (Eq. 1, the comparator) with the same kernel.  mask == NULL keeps the mask buffers inside ws. */
+bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* Human-readable status name and the calling thread's detail for its last non-OK status. */
+const char* bfla_status_string(bfla_status status);
+const char* bfla_last_error(void);
+/* Launch counter: number of kernels this process has enqueued through the library (for bench). */
+uint64_t bfla_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFLA_H_ */

@@ -1,0 +1,360 @@
+// api.cu — the C ABI of include/bfla.h: validation, geometry, workspace carving, TMA descriptor
+// encoding and kernel launches.  No allocation, no device synchronisation, no global mutable
+// state beyond the thread-local error detail and a launch counter.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/bfla.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bfla {
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local char g_err[512] = "";
+
+static bfla_status fail(bfla_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+static bool pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+static long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// ---- driver entry point for TMA descriptors (no link-time dependency on libcuda) -------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static int num_sms_current() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  return n;
+}
+
+static bfla_status encode_4d(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
+                             const uint32_t box[4]) {
+  EncodeTiledFn fn = get_encode();
+  if (!fn) return fail(BFLA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t s[3] = {strides_b[0], strides_b[1], strides_b[2]};
+  cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), d, s, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BFLA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BFLA_OK;
+}
+
+// ---- validation -> geometry -----------------------------------------------------------------
+static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom* g) {
+  if (!P) return fail(BFLA_ERR_INVALID_ARGUMENT, "problem is NULL");
+  if (!P->q || !P->k || !P->v || !P->o) return fail(BFLA_ERR_INVALID_ARGUMENT, "q/k/v/o pointer is NULL");
+  if (P->batch < 1 || P->h_q < 1 || P->h_kv < 1) return fail(BFLA_ERR_INVALID_ARGUMENT, "batch/h_q/h_kv must be >= 1");
+  if (P->h_q % P->h_kv) return fail(BFLA_ERR_INVALID_ARGUMENT, "h_q %% h_kv != 0 (GQA, Eq. 3)");
+  if (P->n_q < 1 || P->n_kv < P->n_q)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "need 1 <= n_q <= n_kv (N_c = n_kv - n_q >= 0, Eq. 11)");
+  if (P->head_dim != 128 && P->head_dim != 256)
+    return fail(BFLA_ERR_UNSUPPORTED, "head_dim %d not built (128, 256)", P->head_dim);
+  if (P->kv_layout != BFLA_KV_CONTIGUOUS && P->kv_layout != BFLA_KV_PAGED)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "kv_layout");
+  memset(g, 0, sizeof(*g));
+  g->B = P->batch;
+  g->Hq = P->h_q;
+  g->Hkv = P->h_kv;
+  g->m = P->h_q / P->h_kv;
+  g->D = P->head_dim;
+  g->Nq = P->n_q;
+  g->Nkv = P->n_kv;
+  g->Nc = P->n_kv - P->n_q;
+  g->head_offset = P->head_offset;
+  g->scale = P->softmax_scale > 0.f ? P->softmax_scale : (float)(1.0 / std::sqrt((double)P->head_dim));
+  g->qs0 = P->q_stride[0];
+  g->qs1 = P->q_stride[1];
+  g->qs2 = P->q_stride[2];
+  g->os0 = P->o_stride[0];
+  g->os1 = P->o_stride[1];
+  g->os2 = P->o_stride[2];
+  g->paged = P->kv_layout == BFLA_KV_PAGED;
+  // TMA / 16-byte vector rules
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!a16(P->q) || !a16(P->k) || !a16(P->v) || !a16(P->o))
+    return fail(BFLA_ERR_MISALIGNED, "q/k/v/o base must be 16-byte aligned");
+  for (int d = 0; d < 3; ++d)
+    if ((P->q_stride[d] % 8) || (P->o_stride[d] % 8) || P->q_stride[d] <= 0 || P->o_stride[d] <= 0)
+      return fail(BFLA_ERR_MISALIGNED, "q/o strides must be positive multiples of 8 elements (16 B)");
+  if (g->paged) {
+    if (!P->page_table) return fail(BFLA_ERR_INVALID_ARGUMENT, "paged layout needs page_table");
+    if (P->page_size != 16 && P->page_size != 32 && P->page_size != 64)
+      return fail(BFLA_ERR_UNSUPPORTED, "page_size %d not built (16, 32, 64)", P->page_size);
+    if (P->num_pages < 1 || (long long)P->max_pages_per_seq * P->page_size < P->n_kv)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "max_pages_per_seq * page_size < n_kv");
+    g->page_size = P->page_size;
+    g->num_pages = P->num_pages;
+    g->max_pages = P->max_pages_per_seq;
+  } else {
+    for (int d = 0; d < 3; ++d)
+      if ((P->kv_stride[d] % 8) || P->kv_stride[d] <= 0)
+        return fail(BFLA_ERR_MISALIGNED, "kv strides must be positive multiples of 8 elements (16 B)");
+    g->kvs0 = P->kv_stride[0];
+    g->kvs1 = P->kv_stride[1];
+    g->kvs2 = P->kv_stride[2];
+  }
+  int b = 64, gg = 64, T = 64;
+  if (cfg) {
+    b = cfg->block_b;
+    gg = cfg->group_g;
+    T = cfg->tile_t;
+    if (!pow2(b) || !pow2(gg) || !pow2(T)) return fail(BFLA_ERR_INVALID_ARGUMENT, "b, g, T must be powers of two");
+    if (b % gg) return fail(BFLA_ERR_INVALID_ARGUMENT, "g must divide b (Eq. 6)");
+    if (b % T) return fail(BFLA_ERR_INVALID_ARGUMENT, "T must divide b (Eq. 19)");
+    if (cfg->pool != BFLA_POOL_FLATTEN && cfg->pool != BFLA_POOL_MEAN) return fail(BFLA_ERR_INVALID_ARGUMENT, "pool");
+    if (cfg->select != BFLA_SELECT_MASS && cfg->select != BFLA_SELECT_RATIO)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "select");
+    if (!(cfg->gamma > 0.f && cfg->gamma <= 1.f)) return fail(BFLA_ERR_INVALID_ARGUMENT, "gamma must be in (0, 1] (Eq. 17)");
+    if (cfg->select == BFLA_SELECT_RATIO && !(cfg->keep_ratio > 0.f && cfg->keep_ratio <= 1.f))
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "keep_ratio must be in (0, 1]");
+    if (!(cfg->rho >= 0.f && cfg->rho <= 1.f)) return fail(BFLA_ERR_INVALID_ARGUMENT, "rho must be in [0, 1] (Eq. 25)");
+    if (cfg->eta < 0 || cfg->n_local < 0 || cfg->n_sink < 0)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "eta, n_local, n_sink must be >= 0");
+    if (T != 64) return fail(BFLA_ERR_UNSUPPORTED, "tile_t %d not built (64)", T);
+    if (cfg->pool == BFLA_POOL_FLATTEN && b / gg > 8)
+      return fail(BFLA_ERR_UNSUPPORTED, "G = b/g = %d > 8 not built for FLATTEN", b / gg);
+  }
+  g->b = b;
+  g->g = gg;
+  g->G = b / gg;
+  g->T = T;
+  g->rb = b / T;
+  g->Lq = (int)cdiv(g->Nq, b);
+  g->Lkv = (int)cdiv(g->Nkv, b);
+  g->Lw = (int)cdiv(g->Lkv, 32);
+  g->Tq = (int)cdiv(g->Nq, T);
+  g->Tkv = (int)cdiv(g->Nkv, T);
+  g->Tw = (int)cdiv(g->Tkv, 32);
+  g->causal_per_head = causal_row_offset(*g, g->Tq);
+  return BFLA_OK;
+}
+
+// ---- workspace layout -------------------------------------------------------------------------
+struct WsLayout {
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, total;
+};
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+static WsLayout ws_layout(const Geom& g) {
+  WsLayout L;
+  size_t o = 0;
+  L.S = o;
+  o += al((size_t)g.B * g.Hq * g.Lq * g.Lkv * 4);
+  L.qbar = o;
+  o += al((size_t)g.B * g.Hq * g.Lq * g.D * 4);
+  L.kbar = o;
+  o += al((size_t)g.B * g.Hkv * g.Lkv * g.D * 4);
+  L.coarse = o;  // internal mask buffers (used when bfla_prefill gets mask == NULL)
+  o += al((size_t)g.B * g.Hkv * g.Lq * g.Lw * 4);
+  L.tbits = o;
+  o += al((size_t)g.B * g.Hkv * g.Tq * g.Tw * 4);
+  L.list = o;
+  o += al((size_t)g.B * g.Hkv * g.causal_per_head * 4);
+  L.count = o;
+  o += al((size_t)g.B * g.Hkv * g.Tq * 4);
+  L.stats = o;
+  o += al(sizeof(bfla_stats));
+  L.total = o;
+  return L;
+}
+
+static bfla_status cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BFLA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return BFLA_OK;
+}
+
+static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_mask* mask, unsigned char* ws,
+                                  const bfla_problem* P, cudaStream_t st) {
+  const WsLayout L = ws_layout(g);
+  float* S = reinterpret_cast<float*>(ws + L.S);
+  unsigned long long* stats = reinterpret_cast<unsigned long long*>(mask->stats);
+  if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
+  const int32_t* pt = g.paged ? P->page_table : nullptr;
+  if (cfg->pool == BFLA_POOL_FLATTEN) {
+    if (launch_flatten_scores(g, P->q, P->k, pt, S, st)) return fail(BFLA_ERR_UNSUPPORTED, "G not built");
+  } else {
+    launch_mean_scores(g, P->q, P->k, pt, reinterpret_cast<float*>(ws + L.qbar), reinterpret_cast<float*>(ws + L.kbar),
+                       S, st);
+  }
+  // c_alpha = log2(e) / sqrt(C) rounded once to fp32 (DESIGN.md §4 item 4; alpha = 1/sqrt(C), Eq. 15)
+  const float c_alpha = (float)(1.4426950408889634 / std::sqrt((double)g.D));
+  launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, mask->kept_mass, stats, st);
+  return cuda_check("bfla_block_mask launch");
+}
+
+static bfla_status run_expand(const Geom& g, const bfla_config* cfg, bfla_mask* mask, cudaStream_t st) {
+  launch_expand_rescue(g, mask->coarse_bits, cfg->n_sink, cfg->n_local, cfg->eta, (double)cfg->rho, cfg->seed,
+                       mask->tile_bits, mask->tile_list, mask->tile_count, mask->tile_label,
+                       reinterpret_cast<unsigned long long*>(mask->stats), st);
+  return cuda_check("bfla_expand_rescue launch");
+}
+
+static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int32_t* list, const int32_t* count,
+                                 int dense, cudaStream_t st) {
+  AttnMaps maps;
+  bfla_status s;
+  {
+    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nq, (uint64_t)g.Hq, (uint64_t)g.B};
+    const uint64_t str[3] = {(uint64_t)g.qs2 * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
+    const uint32_t box[4] = {64, (uint32_t)g.T, 1, 1};
+    if ((s = encode_4d(&maps.q, P->q, dims, str, box)) != BFLA_OK) return s;
+  }
+  if (!g.paged) {
+    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv, (uint64_t)g.B};
+    const uint64_t str[3] = {(uint64_t)g.kvs2 * 2, (uint64_t)g.kvs1 * 2, (uint64_t)g.kvs0 * 2};
+    const uint32_t box[4] = {64, 64, 1, 1};
+    if ((s = encode_4d(&maps.k, P->k, dims, str, box)) != BFLA_OK) return s;
+    if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;
+  } else {
+    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Hkv, (uint64_t)g.page_size, (uint64_t)g.num_pages};
+    const uint64_t str[3] = {(uint64_t)g.D * 2, (uint64_t)g.Hkv * g.D * 2, (uint64_t)g.page_size * g.Hkv * g.D * 2};
+    const uint32_t box[4] = {64, 1, (uint32_t)g.page_size, 1};
+    if ((s = encode_4d(&maps.k, P->k, dims, str, box)) != BFLA_OK) return s;
+    if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;
+  }
+  int e = launch_attention(g, maps, list, count, g.paged ? P->page_table : nullptr, dense, P->o, P->lse,
+                           num_sms_current(), st);
+  if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
+  return cuda_check("attention launch");
+}
+
+static bfla_status check_mask(const Geom& g, const bfla_mask* mask, bool need_coarse, bool need_tiles) {
+  if (!mask) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask is NULL");
+  if (need_coarse && !mask->coarse_bits) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask->coarse_bits is NULL");
+  if (need_tiles) {
+    if (!mask->tile_bits || !mask->tile_list || !mask->tile_count)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "mask tile buffers are NULL");
+    if (mask->tile_list_capacity < (long long)g.B * g.Hkv * g.causal_per_head)
+      return fail(BFLA_ERR_CAPACITY, "tile_list_capacity %lld < %lld", (long long)mask->tile_list_capacity,
+                  (long long)g.B * g.Hkv * g.causal_per_head);
+  }
+  return BFLA_OK;
+}
+
+}  // namespace bfla
+
+using namespace bfla;
+
+extern "C" {
+
+size_t bfla_workspace_size(const bfla_problem* problem, const bfla_config* config) {
+  Geom g;
+  if (make_geom(problem, config, &g) != BFLA_OK) return 0;
+  return ws_layout(g).total;
+}
+
+int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* config) {
+  Geom g;
+  if (make_geom(problem, config, &g) != BFLA_OK) return -1;
+  return (int64_t)g.B * g.Hkv * g.causal_per_head;
+}
+
+bfla_status bfla_block_mask(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if ((s = check_mask(g, mask, true, false)) != BFLA_OK) return s;
+  if (!ws || ws_bytes < ws_layout(g).total) return fail(BFLA_ERR_WORKSPACE, "workspace too small");
+  return run_block_mask(g, config, mask, static_cast<unsigned char*>(ws), problem, static_cast<cudaStream_t>(stream));
+}
+
+bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
+                               size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if ((s = check_mask(g, mask, true, true)) != BFLA_OK) return s;
+  return run_expand(g, config, mask, static_cast<cudaStream_t>(stream));
+}
+
+bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if (!mask || !mask->tile_list || !mask->tile_count) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask lists are NULL");
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream));
+}
+
+bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
+                         size_t ws_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if (!config) return run_attention(g, problem, nullptr, nullptr, 1, st);  // dense causal (Eq. 1)
+  const WsLayout L = ws_layout(g);
+  if (!ws || ws_bytes < L.total) return fail(BFLA_ERR_WORKSPACE, "workspace too small");
+  unsigned char* w = static_cast<unsigned char*>(ws);
+  bfla_mask local;
+  if (!mask) {
+    memset(&local, 0, sizeof(local));
+    local.coarse_bits = reinterpret_cast<uint32_t*>(w + L.coarse);
+    local.tile_bits = reinterpret_cast<uint32_t*>(w + L.tbits);
+    local.tile_list = reinterpret_cast<int32_t*>(w + L.list);
+    local.tile_list_capacity = (long long)g.B * g.Hkv * g.causal_per_head;
+    local.tile_count = reinterpret_cast<int32_t*>(w + L.count);
+    mask = &local;
+  }
+  if ((s = check_mask(g, mask, true, true)) != BFLA_OK) return s;
+  if ((s = run_block_mask(g, config, mask, w, problem, st)) != BFLA_OK) return s;
+  if ((s = run_expand(g, config, mask, st)) != BFLA_OK) return s;
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, st);
+}
+
+const char* bfla_status_string(bfla_status status) {
+  switch (status) {
+    case BFLA_OK: return "BFLA_OK";
+    case BFLA_ERR_INVALID_ARGUMENT: return "BFLA_ERR_INVALID_ARGUMENT";
+    case BFLA_ERR_UNSUPPORTED: return "BFLA_ERR_UNSUPPORTED";
+    case BFLA_ERR_MISALIGNED: return "BFLA_ERR_MISALIGNED";
+    case BFLA_ERR_WORKSPACE: return "BFLA_ERR_WORKSPACE";
+    case BFLA_ERR_CAPACITY: return "BFLA_ERR_CAPACITY";
+    case BFLA_ERR_CUDA: return "BFLA_ERR_CUDA";
+  }
+  return "BFLA_UNKNOWN_STATUS";
+}
+
+const char* bfla_last_error(void) { return g_err; }
+
+uint64_t bfla_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,430 @@
+// attention.cu — fused sparse causal prefill of BFLA (Eq. 27) and its dense twin (Eq. 1).
+//
+// One work item = (request r, KV head h, row chunk c, query tile i).  All m query heads of the
+// head group H_h (Eq. 8) share the item's kept-KV-tile list (the mask is per KV head after the OR,
+// R8), so their T-row query tiles are stacked into 128-row MMA tiles (GQA packing): with T = 64,
+// one 128-row tile holds 2 heads; NQT (1 or 2) tiles per CTA share every K/V tile loaded.
+//
+// Warp roles (1 CTA per SM, persistent over a static LPT-ordered item sequence):
+//   warp 0        TMA producer: Q tiles per item, then K_j / V_j for every kept tile j (ring of
+//                 STAGES slots, mbarrier full/empty pairs).  Contiguous [B,H,N,d] via a 4-D
+//                 tensor map, or vLLM pages [P,page,H,d] gathered page by page into the same
+//                 swizzled smem layout.
+//   warp 1        MMA issuer (one thread): S_q = Q_q K_j^T into TMEM (M=128, N=64, K=d) and
+//                 O_q += P_q V_j (M=128, N=d, K=64), tcgen05.mma kind::f16, fp32 accumulators.
+//   warp 2        TMEM allocator (512 columns).
+//   warps 4..     one 128-thread softmax warpgroup per Q tile; thread = one query row (= one
+//                 TMEM lane): loads S, applies the token-exact causal frontier, online softmax in
+//                 the exp2 domain with lazy rescaling (the running max is only raised when it
+//                 grows by > 8, so O in TMEM is rescaled rarely), writes P (bf16) to swizzled
+//                 smem for the PV MMA, and finally O / l -> bf16 -> global (+ LSE).
+// Dropped tiles are never loaded nor computed: they contribute exactly nothing (Eq. 27's -inf).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bfla {
+
+namespace {
+
+constexpr int BM = 128;  // MMA M (rows of a Q tile)
+constexpr int BN = 64;   // KV tile = T
+
+template <int D, int NQT>
+struct Cfg {
+  static constexpr int STAGES = D == 128 ? 3 : 2;
+  static constexpr int QBYTES = BM * D * 2;       // one 128-row Q tile
+  static constexpr int KVBYTES = BN * D * 2;      // one K (or V) tile
+  static constexpr int PBYTES = BM * BN * 2;      // one P tile
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + NQT * QBYTES;
+  static constexpr int OFF_V = OFF_K + STAGES * KVBYTES;
+  static constexpr int OFF_P = OFF_V + STAGES * KVBYTES;
+  static constexpr int OFF_BAR = OFF_P + NQT * PBYTES;
+  static constexpr int NBAR = 2 + 4 * STAGES + 4 * NQT;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + tmem slot + alignment slack
+  static constexpr int THREADS = 128 + 128 * NQT;
+  static constexpr int COL_O = D == 128 ? 128 : 256;  // TMEM column of O_0 (S_q at 64 q)
+};
+
+struct Item {
+  int r, h, c, i;
+};
+__device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
+  // order: (r, h) major, query tile descending (longest rows first: LPT proxy), chunk inner
+  Item it;
+  it.c = idx % NC;
+  int rest = idx / NC;
+  it.i = g.Tq - 1 - rest % g.Tq;
+  rest /= g.Tq;
+  it.h = rest % g.Hkv;
+  it.r = rest / g.Hkv;
+  return it;
+}
+
+template <int D, int NQT, bool PAGED, bool DENSE>
+__global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
+    k_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
+           const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
+           __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
+  using C = Cfg<D, NQT>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + C::STAGES;
+  uint64_t* v_full = k_empty + C::STAGES;
+  uint64_t* v_empty = v_full + C::STAGES;
+  uint64_t* s_full = v_empty + C::STAGES;  // [NQT]
+  uint64_t* p_full = s_full + NQT;         // [NQT]
+  uint64_t* o_full = p_full + NQT;         // [NQT]
+  uint64_t* o_free = o_full + NQT;         // [NQT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int q = 0; q < NQT; ++q) {
+      mbar_init(s_full + q, 1);
+      mbar_init(p_full + q, 128);
+      mbar_init(o_full + q, 1);
+      mbar_init(o_free + q, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int heads_in_chunk = NQT * hpq;
+
+  auto row_count = [&](const Item& it) -> int {
+    if (DENSE) return (int)causal_row_count(g, it.i);
+    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+  };
+  auto row_list = [&](const Item& it) -> const int32_t* {
+    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
+  };
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0) {
+      uint32_t kv = 0, nit = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item it = decode_item(g, idx, NC);
+        const int cnt = row_count(it);
+        if (cnt == 0) continue;
+        const int32_t* lst = DENSE ? nullptr : row_list(it);
+        const uint32_t my_it = nit++;
+        // Q: for each tile q and head slot s, D/64 boxes of (64 cols x 64 rows)
+        mbar_wait(q_empty, (my_it & 1) ^ 1);
+        int nq_boxes = 0;
+        for (int q = 0; q < NQT; ++q)
+          for (int s = 0; s < hpq; ++s)
+            if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
+        mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
+        for (int q = 0; q < NQT; ++q)
+          for (int s = 0; s < hpq; ++s) {
+            const int pl = it.c * heads_in_chunk + q * hpq + s;
+            if (pl >= g.m) continue;
+            const int p = it.h * g.m + pl;
+            for (int cc = 0; cc < D / 64; ++cc)
+              tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
+                          cc * 64, it.i * g.T, p, it.r);
+          }
+        for (int n = 0; n < cnt; ++n, ++kv) {
+          const int j = DENSE ? n : lst[n];
+          const int st = kv % C::STAGES;
+          const uint32_t ph = (kv / C::STAGES) & 1;
+          for (int kvsel = 0; kvsel < 2; ++kvsel) {
+            uint64_t* full = (kvsel ? v_full : k_full) + st;
+            mbar_wait((kvsel ? v_empty : k_empty) + st, ph ^ 1);
+            mbar_arrive_expect_tx(full, C::KVBYTES);
+            unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::KVBYTES;
+            const CUtensorMap* map = kvsel ? &tmV : &tmK;
+            if (!PAGED) {
+              for (int cc = 0; cc < D / 64; ++cc)
+                tma_load_4d(dst + cc * (BN * 128), map, full, cc * 64, j * BN, it.h, it.r);
+            } else {
+              // vLLM pages: the 64-token tile is BN/ps page boxes of (64 cols x ps rows); a page
+              // past the request's last logical page (ragged tail) is replaced by its first page
+              // (finite data; those keys are masked by causality and get P = 0).
+              const int ps = g.page_size;
+              const int npl = (g.Nkv + ps - 1) / ps;
+              const int32_t* table = page_table + (long long)it.r * g.max_pages;
+              for (int pc = 0; pc < BN / ps; ++pc) {
+                const int lp = j * BN / ps + pc;
+                const int phys = __ldg(table + (lp < npl ? lp : 0));
+                for (int cc = 0; cc < D / 64; ++cc)
+                  tma_load_4d(dst + cc * (BN * 128) + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    if (lane == 0) {
+      constexpr uint32_t idS = idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t idO = idesc_bf16(BM, D, 0, 1);
+      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K),
+                     sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
+      uint32_t kv = 0, nit = 0, sp_cnt = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item it = decode_item(g, idx, NC);
+        const int cnt = row_count(it);
+        if (cnt == 0) continue;
+        const uint32_t my_it = nit++;
+        mbar_wait(q_full, my_it & 1);
+        tc_fence_after();
+        uint32_t st_prev = 0;
+        for (int n = 0; n < cnt; ++n, ++kv) {
+          const uint32_t st = kv % C::STAGES, ph = (kv / C::STAGES) & 1;
+          mbar_wait(k_full + st, ph);
+          tc_fence_after();
+          if (n > 0) {
+            mbar_wait(v_full + st_prev, ((kv - 1) / C::STAGES) & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int q = 0; q < NQT; ++q) {
+            if (n > 0) {  // O_q += P_q(n-1) V_{n-1}
+              mbar_wait(p_full + q, (sp_cnt - 1) & 1);
+              tc_fence_after();
+              if (n == 1) {
+                mbar_wait(o_free + q, (my_it & 1) ^ 1);
+                tc_fence_after();
+              }
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk)
+                umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
+                            sdesc_sw128(sV + st_prev * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
+                            (n > 1 || kk > 0) ? 1u : 0u);
+            }
+            // S_q = Q_q K_n^T
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              umma_f16_ss(tmem + q * BN,
+                          sdesc_sw128(sQ + q * C::QBYTES + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024),
+                          sdesc_sw128(sK + st * C::KVBYTES + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024),
+                          idS, kk > 0 ? 1u : 0u);
+            umma_commit(s_full + q);
+          }
+          ++sp_cnt;
+          umma_commit(k_empty + st);
+          if (n > 0) umma_commit(v_empty + st_prev);
+          if (n == cnt - 1) umma_commit(q_empty);  // every S MMA of the item has been issued
+          st_prev = st;
+        }
+        // tail: O_q += P_q(cnt-1) V_{cnt-1}
+        mbar_wait(v_full + st_prev, ((kv - 1) / C::STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < NQT; ++q) {
+          mbar_wait(p_full + q, (sp_cnt - 1) & 1);
+          tc_fence_after();
+          if (cnt == 1) {
+            mbar_wait(o_free + q, (my_it & 1) ^ 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
+                        sdesc_sw128(sV + st_prev * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
+                        (cnt > 1 || kk > 0) ? 1u : 0u);
+          umma_commit(o_full + q);
+        }
+        umma_commit(v_empty + st_prev);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================================ softmax / epilogue ================================
+    const int q = (warp - 4) >> 2;
+    const int lg = warp & 3;              // TMEM lane group of this warp
+    const int row = lg * 32 + lane;       // row of Q tile q = TMEM lane
+    const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + q * BN;
+    const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
+    const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
+    unsigned char* sPq = smem + C::OFF_P + q * C::PBYTES;
+    uint32_t sp_cnt = 0, nit = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const Item it = decode_item(g, idx, NC);
+      const int cnt = row_count(it);
+      const int slot = row / g.T;
+      const int pl = it.c * heads_in_chunk + q * hpq + slot;
+      const int t = it.i * g.T + (row % g.T);
+      const bool valid = slot < hpq && pl < g.m && t < g.Nq;
+      const int p = it.h * g.m + pl;
+      __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2;
+      if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
+        if (valid) {
+          for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
+          if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+        }
+        continue;
+      }
+      const uint32_t my_it = nit++;
+      const int32_t* lst = DENSE ? nullptr : row_list(it);
+      float m_run = -INFINITY, l_run = 0.0f;
+      for (int n = 0; n < cnt; ++n, ++sp_cnt) {
+        const int j = DENSE ? n : __ldg(lst + n);
+        mbar_wait(s_full + q, sp_cnt & 1);
+        tc_fence_after();
+        float s[BN];
+        tmem_ld32(tS, s);
+        tmem_ld32(tS + 32, s + 32);
+        tmem_wait_ld();
+        // token-exact causality inside the tile (Eq. 27): key j*64 + c visible iff <= N_c + t
+        const int lim = g.Nc + t - j * BN;
+        if (lim < BN - 1) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c)
+            if (c > lim) s[c] = -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+        mx *= c2;
+        // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom
+        // in P and l); the decision is per row, the TMEM traffic is warp-uniform (.sync.aligned)
+        const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
+        float alpha = 1.0f;
+        if (need) {
+          alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
+          l_run *= alpha;
+          m_run = mx;
+        }
+        if (n > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+          // O (complete through PV(n-1): the s_full commit covers every earlier MMA) *= alpha
+#pragma unroll 1
+          for (int cc = 0; cc < D; cc += 32) {
+            float ov[32];
+            tmem_ld32(tO + cc, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+            tmem_st32(tO + cc, ov);
+          }
+          tmem_wait_st();
+        }
+        const float msub = m_run == -INFINITY ? 0.0f : m_run;
+        float lsum = 0.0f;
+        uint32_t pk[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN; c += 2) {
+          const float p0 = ex2_approx(fmaf(s[c], c2, -msub));
+          const float p1 = ex2_approx(fmaf(s[c + 1], c2, -msub));
+          lsum += p0 + p1;
+          pk[c / 2] = pack_bf16x2(p0, p1);
+        }
+        l_run += lsum;
+        // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
+        unsigned char* prow = sPq + row * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) << 4)) =
+              make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_full + q);
+      }
+      // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
+      mbar_wait(o_full + q, my_it & 1);
+      tc_fence_after();
+      const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+#pragma unroll 1
+      for (int cc = 0; cc < D; cc += 32) {
+        float ov[32];
+        tmem_ld32(tO + cc, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + cc);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+      }
+      if (valid && lse)
+        lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
+            l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+      tc_fence_before();
+      mbar_arrive(o_free + q);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+size_t attn_smem_bytes(int D, int nqt) {
+  if (D == 128) return nqt == 2 ? Cfg<128, 2>::SMEM : Cfg<128, 1>::SMEM;
+  return Cfg<256, 1>::SMEM;
+}
+
+template <int D, int NQT, bool PAGED, bool DENSE>
+static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                    const int32_t* pt, void* o, float* lse, int n_items, int hpq, int NC, int num_sms,
+                    cudaStream_t st) {
+  using C = Cfg<D, NQT>;
+  auto kern = k_attn<D, NQT, PAGED, DENSE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = n_items < num_sms ? n_items : num_sms;
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
+                                          static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+// Rows of one item: NQT 128-row tiles, each holding hpq = 128/T heads of T rows; NQT = 2 when the
+// group has more than one tile of rows and TMEM allows (d = 128: 2 x (64 S + 128 O) columns).
+int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st) {
+  const int hpq = BM / g.T;
+  const int nqt = (g.D == 128 && g.m > hpq) ? 2 : 1;
+  const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
+  const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
+  if (items == 0) return 0;
+  const int n = (int)items;
+#define BFLA_GO(D_, Q_, P_, X_) return launch_t<D_, Q_, P_, X_>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
+  const bool paged = g.paged != 0;
+  if (g.D == 128 && nqt == 2) {
+    if (paged) { if (dense) BFLA_GO(128, 2, true, true); else BFLA_GO(128, 2, true, false); }
+    else { if (dense) BFLA_GO(128, 2, false, true); else BFLA_GO(128, 2, false, false); }
+  } else if (g.D == 128) {
+    if (paged) { if (dense) BFLA_GO(128, 1, true, true); else BFLA_GO(128, 1, true, false); }
+    else { if (dense) BFLA_GO(128, 1, false, true); else BFLA_GO(128, 1, false, false); }
+  } else {
+    if (paged) { if (dense) BFLA_GO(256, 1, true, true); else BFLA_GO(256, 1, true, false); }
+    else { if (dense) BFLA_GO(256, 1, false, true); else BFLA_GO(256, 1, false, false); }
+  }
+#undef BFLA_GO
+}
+
+}  // namespace bfla

@@ -1,0 +1,35 @@
+// kernels.h — internal launch functions (host side) of the BFLA sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace bfla {
+
+void count_launch();
+
+// Stage 1 scores (Eq. 9-10): FLATTEN (canonical SIMT fp32 chain) or MEAN.
+int launch_flatten_scores(const Geom& g, const void* q, const void* k, const int32_t* page_table, float* S,
+                          cudaStream_t st);
+void launch_mean_scores(const Geom& g, const void* q, const void* k, const int32_t* page_table, float* qbar,
+                        float* kbar, float* S, cudaStream_t st);
+// Stage 1 selection (Eq. 13-18 + OR over H_h)
+size_t select_smem_bytes(const Geom& g, int nwarps);
+void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
+                   uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st);
+// Stage 2 (Eq. 19-26)
+void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int n_local, int eta, double rho,
+                          uint64_t seed, uint32_t* tile_bits, int32_t* list, int32_t* count, uint8_t* label,
+                          unsigned long long* stats, cudaStream_t st);
+
+// Sparse / dense prefill (Eq. 27 / Eq. 1) — tcgen05 + TMEM + TMA.
+struct AttnMaps {
+  CUtensorMap q, k, v;
+};
+size_t attn_smem_bytes(int D, int nqt);
+int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st);
+
+}  // namespace bfla

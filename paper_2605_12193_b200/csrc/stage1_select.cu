@@ -1,0 +1,151 @@
+// stage1_select.cu — Stage 1 selection of BFLA (Eq. 13-18 + the GQA union):
+// causal block mask, block softmax with alpha = 1/sqrt(C), keep-mass (or keep-ratio) selection,
+// OR over each head group H_h.  Canonical fp32 arithmetic: every rounding below
+// is an explicit IEEE round-to-nearest intrinsic and this translation unit is compiled with
+// -fmad=false, so the device computes exactly the canonical value sequence.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bfla {
+
+// Canonical exp2 for t <= 0 (DESIGN.md §4 item 5): n = floor(t), f = t - n, degree-6 Horner
+// polynomial (fp32 FMA, coefficients = Chebyshev fit rounded to fp32), scaled by 2^n (exact).
+__device__ __forceinline__ float exp2_canon(float t) {
+  if (t < -126.0f) return 0.0f;
+  const float fl = floorf(t);
+  const int n = (int)fl;
+  const float f = __fsub_rn(t, fl);
+  float p = 0x1.cacdfep-13f;
+  p = __fmaf_rn(p, f, 0x1.44bd4cp-10f);
+  p = __fmaf_rn(p, f, 0x1.3d5822p-7f);
+  p = __fmaf_rn(p, f, 0x1.c67ee4p-5f);
+  p = __fmaf_rn(p, f, 0x1.ebfdf8p-3f);
+  p = __fmaf_rn(p, f, 0x1.62e428p-1f);
+  p = __fmaf_rn(p, f, 0x1p+0f);
+  return __fmul_rn(p, __int_as_float((n + 127) << 23));
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// One CTA per (request r, KV head h, query block i); warp w handles query heads p = h m + w,
+// h m + w + nwarps, ...  Per row (r, p, i):
+//   1. M = max over causal j of S_j (exact);  t_j = (S_j - M) * c_alpha (two roundings);
+//      e_j = exp2_canon(t_j);  Z = sum_j e_j sequentially (lane 0, ascending j);  A_j = e_j / Z.
+//   2. Selection by repeated extraction of the largest key (A_j bits, ~j): this visits the blocks
+//      in exactly the order (A desc, j asc) (R6), and the prefix P_r is accumulated in that
+//      order, one fp32 add per step (R7), until P_r >= gamma (MASS) or r = ceil(ratio n_causal)
+//      (RATIO).  gamma >= 1 keeps all causal blocks.
+//   3. keep bits OR-ed into the CTA's coarse row (R8), written once at the end.
+__global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restrict__ S, float c_alpha, int select,
+                                                   float gamma, float keep_ratio, uint32_t* __restrict__ coarse,
+                                                   float* __restrict__ kept_mass,
+                                                   unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int nwarps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* row_bits = reinterpret_cast<uint32_t*>(smem);                       // [Lw]
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + ((g.Lw * 4 + 15) / 16) * 16)
+                             + (size_t)warp * g.Lkv;                            // [nwarps][Lkv]
+  const int i = blockIdx.x % g.Lq;
+  const int h = (blockIdx.x / g.Lq) % g.Hkv;
+  const int r = blockIdx.x / (g.Lq * g.Hkv);
+  for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) row_bits[w] = 0u;
+  __syncthreads();
+  // Eq. 11-13 at block size b
+  const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
+  const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;  // causal blocks
+  unsigned ties = 0, kept_sum = 0;
+  for (int pl = warp; pl < g.m; pl += nwarps) {
+    const int p = h * g.m + pl;
+    const float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
+    float M = -INFINITY;
+    for (int j = lane; j < nc; j += 32) M = fmaxf(M, s[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float* e = reinterpret_cast<float*>(keys);  // reuse the key area for e_j (nc floats)
+    for (int j = lane; j < nc; j += 32) e[j] = exp2_canon(__fmul_rn(__fsub_rn(s[j], M), c_alpha));
+    __syncwarp();
+    float Z = 0.0f;
+    if (lane == 0)
+      for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
+    Z = __shfl_sync(0xffffffffu, Z, 0);
+    __syncwarp();
+    // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j.  Built back to front so
+    // the float area (aliasing the low half of the key array) is read before it is overwritten.
+    for (int j0 = ((nc - 1) / 32) * 32; j0 >= 0; j0 -= 32) {
+      const int j = j0 + lane;
+      float a = 0.0f;
+      if (j < nc) a = __fdiv_rn(e[j], Z);
+      __syncwarp();
+      if (j < nc) keys[j] = ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(~(uint32_t)j);
+      __syncwarp();
+    }
+    int target = nc;
+    if (select == 1) {
+      double want = ceil((double)keep_ratio * (double)nc);
+      target = (int)want;
+      if (target < 1) target = 1;
+      if (target > nc) target = nc;
+    }
+    const bool keep_all = (select == 0 && gamma >= 1.0f);
+    float P = 0.0f, a_last = 0.0f;
+    int nsel = 0;
+    while (nsel < nc) {
+      unsigned long long best = 0ull;
+      for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
+      best = warp_max_u64(best);
+      const int jsel = (int)(~(uint32_t)(best & 0xffffffffull));
+      a_last = __uint_as_float((uint32_t)(best >> 32));
+      P = __fadd_rn(P, a_last);
+      ++nsel;
+      if (lane == 0) {
+        keys[jsel] = 0ull;
+        atomicOr(&row_bits[jsel >> 5], 1u << (jsel & 31));
+      }
+      __syncwarp();
+      if (keep_all) continue;
+      if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
+    }
+    if (nsel < nc) {  // report a tie at the cut (R6): next block in order has the same probability
+      unsigned long long best = 0ull;
+      for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
+      best = warp_max_u64(best);
+      if (__uint_as_float((uint32_t)(best >> 32)) == a_last) ties++;
+    }
+    kept_sum += nsel;
+    if (kept_mass && lane == 0) kept_mass[((long long)r * g.Hq + p) * g.Lq + i] = P;
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t* out = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw;
+  for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) out[w] = row_bits[w];
+  if (stats && lane == 0) {
+    const unsigned nrows = (unsigned)((g.m - warp + nwarps - 1) / nwarps > 0 ? (g.m - warp + nwarps - 1) / nwarps : 0);
+    if (nrows) atomicAdd(stats + 8, (unsigned long long)nrows);
+    if (ties) atomicAdd(stats + 9, (unsigned long long)ties);
+    if (kept_sum) atomicAdd(stats + 10, (unsigned long long)kept_sum);
+  }
+}
+
+size_t select_smem_bytes(const Geom& g, int nwarps) {
+  return (size_t)((g.Lw * 4 + 15) / 16) * 16 + (size_t)nwarps * g.Lkv * 8;
+}
+
+void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
+                   uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st) {
+  const int nwarps = g.m < 4 ? g.m : 4;
+  const size_t smem = select_smem_bytes(g, nwarps);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_s1_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_s1_select<<<g.B * g.Hkv * g.Lq, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse,
+                                                              kept_mass, stats);
+  count_launch();
+}
+
+}  // namespace bfla

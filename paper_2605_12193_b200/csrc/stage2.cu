@@ -1,0 +1,102 @@
+// stage2.cu — Stage 2 of BFLA (Eq. 19-26): expansion of the coarse keep mask to the
+// T-tile grid, tile causality, local band, sink, stride and random rescue, final union, and the
+// compacted kept-tile lists that drive the sparse prefill kernel.  Integer only.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bfla {
+
+// chi / psi of Eq. 24-25 (R15): SplitMix64 finalizer over the packed (i, j) key; psi folds in the
+// global KV head index.  Bit-identical definitions are pinned in DESIGN.md §4 item 8.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+// One warp per (request r, KV head h, query tile i).  Labels (precedence mass > sink > band >
+// stride > random, R13): 1 mass (Eq. 20), 2 sink (Eq. 22), 3 band (Eq. 21), 4 stride (Eq. 24),
+// 5 random (Eq. 25); 0 = dropped or non-causal.  The kept list of row (r,h,i) is written in
+// ascending j at its closed-form causal offset, so rows need no global scan.
+__global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t* __restrict__ coarse,
+                                                          int n_sink, int n_local, int eta, double rho,
+                                                          uint64_t seed, uint32_t* __restrict__ tile_bits,
+                                                          int32_t* __restrict__ list, int32_t* __restrict__ count,
+                                                          uint8_t* __restrict__ label,
+                                                          unsigned long long* __restrict__ stats) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nrows = (long long)g.B * g.Hkv * g.Tq;
+  if (row >= nrows) return;
+  const int i = (int)(row % g.Tq);
+  const int h = (int)((row / g.Tq) % g.Hkv);
+  const int r = (int)(row / ((long long)g.Tq * g.Hkv));
+  // Eq. 11-13 at tile size T: causal iff jT <= min(N_c + (i+1)T - 1, N_kv - 1)
+  const long long fr = (long long)g.Nc + (long long)(i + 1) * g.T - 1;
+  const int jmax = (int)((fr < g.Nkv - 1 ? fr : (long long)g.Nkv - 1) / g.T);
+  // R11: band = [max(0, d_i - n_local), d_i], d_i = min(floor(fr / T), Tkv - 1)
+  int d_i = (int)(fr / g.T);
+  if (d_i > g.Tkv - 1) d_i = g.Tkv - 1;
+  const int band_lo = d_i - n_local > 0 ? d_i - n_local : 0;
+  const uint32_t* crow = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i / g.rb) * g.Lw;
+  int32_t* lrow = list + (long long)(r * g.Hkv + h) * g.causal_per_head + causal_row_offset(g, i);
+  const uint64_t hglob = (uint64_t)(g.head_offset + h);
+  int nk = 0;
+  unsigned cnt[6] = {0, 0, 0, 0, 0, 0};
+  for (int j0 = 0; j0 < g.Tkv; j0 += 32) {
+    const int j = j0 + lane;
+    int lab = 0;
+    if (j <= jmax) {
+      const int J = j / g.rb;
+      if ((crow[J >> 5] >> (J & 31)) & 1u) {
+        lab = 1;
+      } else if (j < n_sink) {
+        lab = 2;
+      } else if (j >= band_lo && j <= d_i) {
+        lab = 3;
+      } else {
+        const uint64_t key = ((uint64_t)(uint32_t)i << 32) | (uint64_t)(uint32_t)j;
+        if (eta > 0 && mix64(key ^ seed) % (uint64_t)eta == 0) {
+          lab = 4;
+        } else if (rho > 0.0) {
+          const uint64_t z = mix64(mix64(key ^ seed ^ 0xD1B54A32D192ED03ULL) ^ (hglob * 0x9E3779B97F4A7C15ULL));
+          if ((double)(z >> 11) * 0x1p-53 < rho) lab = 5;
+        }
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, lab != 0);
+    if (lane == 0) tile_bits[row * g.Tw + (j0 >> 5)] = bal;
+    if (lab) lrow[nk + __popc(bal & ((1u << lane) - 1u))] = j;
+    nk += __popc(bal);
+    if (label && j < g.Tkv) label[row * g.Tkv + j] = (uint8_t)lab;
+    cnt[lab]++;
+  }
+  if (lane == 0) count[row] = nk;
+  if (stats) {
+#pragma unroll
+    for (int l = 1; l < 6; ++l) {
+      unsigned v = cnt[l];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v) atomicAdd(stats + 2 + l, (unsigned long long)v);
+    }
+    if (lane == 0) {
+      atomicAdd(stats + 0, (unsigned long long)(jmax + 1));  // causal tiles of this row
+      atomicAdd(stats + 1, (unsigned long long)nk);
+    }
+  }
+}
+
+void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int n_local, int eta, double rho,
+                          uint64_t seed, uint32_t* tile_bits, int32_t* list, int32_t* count, uint8_t* label,
+                          unsigned long long* stats, cudaStream_t st) {
+  const long long rows = (long long)g.B * g.Hkv * g.Tq;
+  const int blocks = (int)((rows + 7) / 8);
+  k_s2_expand_rescue<<<blocks, 256, 0, st>>>(g, coarse, n_sink, n_local, eta, rho, seed, tile_bits, list, count,
+                                               label, stats);
+  count_launch();
+}
+
+}  // namespace bfla

@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Masks (coarse bits, tile labels, lists, counts) must be bit-exact; O within max-abs 2e-2 and
+mean-abs 2e-3 of the fp64 oracle (BASELINE.json).  Sizes span several tiles and ragged tails."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2605_12193_b200 as bf
+import workloads
+from gpu_util import check_lists, compare_o, f32, oracle_attention, oracle_masks, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+TINY = dict(B=1, Hq=2, Hkv=1, Nq=2048, Nkv=2048, d=128)
+TINY_CFG = dict(b=128, g=64, T=64)
+
+
+def _check_masks(gpu, ref, cfg):
+    coarse = np.stack([x["coarse"] for x in ref])
+    labels = np.stack([x["labels"] for x in ref])
+    assert np.array_equal(gpu["coarse"], coarse), "coarse mask mismatch"
+    assert np.array_equal(gpu["labels"], labels), "tile label mismatch"
+    assert np.array_equal(gpu["tiles"], (labels > 0).astype(np.uint8)), "tile bits mismatch"
+    if gpu["kept_mass"] is not None:
+        km = np.stack([x["kept_mass"] for x in ref])
+        assert np.array_equal(gpu["kept_mass"], km), "kept mass mismatch"
+    ties = sum(int(x["tie"].sum()) for x in ref)
+    assert gpu["stats"]["rows_exact_tie"] == ties
+    assert gpu["stats"]["kept_tiles"] == int((labels > 0).sum())
+    return labels
+
+
+@pytest.mark.parametrize("sigma,seed", [(1.0, 1), (0.7, 2), (0.5, 3), (0.3, 4)])
+@pytest.mark.parametrize("gamma", [0.9, 0.99, 0.999])
+def test_tiny_gaussian_masks_and_output(sigma, seed, gamma):
+    prob = workloads.gaussian(seed, **TINY, sigma=sigma)
+    cfg = bf.Config(**TINY_CFG, gamma=gamma)
+    gpu = run_gpu(prob, cfg)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    check_lists(gpu, labels, 2048, 2048, 64)
+    (o_ref, lse_ref), = oracle_attention(prob, labels, 64)
+    compare_o(gpu["o"][0], o_ref, f"sigma={sigma} gamma={gamma}")
+    lse = gpu["lse"][0].cpu().numpy()
+    assert np.abs(lse - lse_ref).max() <= 1e-3
+
+
+def test_tiny_structured():
+    prob = workloads.structured(101, **TINY, block=128)
+    cfg = bf.Config(**TINY_CFG)
+    gpu = run_gpu(prob, cfg)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    (o_ref, _), = oracle_attention(prob, labels, 64)
+    compare_o(gpu["o"][0], o_ref, "structured")
+
+
+@pytest.mark.parametrize("case", [
+    dict(B=2, Hq=4, Hkv=1, Nq=1000, Nkv=1000, b=128, g=64),      # ragged tail, m=4 (NQT=2)
+    dict(B=1, Hq=8, Hkv=1, Nq=777, Nkv=1500, b=256, g=64),       # chunked prefill, m=8 (2 chunks)
+    dict(B=1, Hq=3, Hkv=3, Nq=640, Nkv=640, b=64, g=16),         # m=1 (half-empty Q tile)
+    dict(B=1, Hq=4, Hkv=2, Nq=130, Nkv=4000, b=256, g=32),       # long context, short chunk, G=8
+    dict(B=1, Hq=2, Hkv=1, Nq=1, Nkv=1, b=64, g=64),             # single token
+    dict(B=1, Hq=16, Hkv=2, Nq=520, Nkv=520, b=128, g=128),      # G=1, m=8
+])
+def test_shapes(case):
+    c = dict(case)
+    b, g = c.pop("b"), c.pop("g")
+    prob = workloads.gaussian(11, d=128, sigma=0.8, **c)
+    cfg = bf.Config(b=b, g=g, T=64, gamma=0.95, eta=4, rho=0.2, seed=5)
+    gpu = run_gpu(prob, cfg)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    check_lists(gpu, labels, c["Nq"], c["Nkv"], 64)
+    for r, (o_ref, lse_ref) in enumerate(oracle_attention(prob, labels, 64)):
+        compare_o(gpu["o"][r], o_ref, str(case))
+        assert np.abs(gpu["lse"][r].cpu().numpy() - lse_ref).max() <= 1e-3
+
+
+def test_mean_pool_and_keep_ratio():
+    prob = workloads.gaussian(21, B=1, Hq=4, Hkv=2, Nq=1500, Nkv=1500, d=128, sigma=1.0)
+    for cfg in [bf.Config(b=128, g=64, pool=bf.POOL_MEAN, gamma=0.9),
+                bf.Config(b=128, g=64, select=bf.SELECT_RATIO, keep_ratio=0.2),
+                bf.Config(b=128, g=64, pool=bf.POOL_MEAN, select=bf.SELECT_RATIO, keep_ratio=0.05)]:
+        gpu = run_gpu(prob, cfg)
+        ref = oracle_masks(prob, cfg)
+        labels = _check_masks(gpu, ref, cfg)
+        (o_ref, _), = oracle_attention(prob, labels, 64)
+        compare_o(gpu["o"][0], o_ref, str(cfg))
+
+
+def test_stage2_isolated_rescue_variants():
+    """Stage 2 alone: upload an arbitrary coarse mask, compare labels/lists with the oracle."""
+    rng = np.random.default_rng(3)
+    B, Hkv, N = 2, 3, 3000
+    prob = workloads.gaussian(1, B=B, Hq=Hkv * 2, Hkv=Hkv, Nq=N, Nkv=N, d=128)
+    for kw in [dict(n_sink=1, n_local=8, eta=16, rho=0.0), dict(n_sink=2, n_local=0, eta=0, rho=0.3, seed=99),
+               dict(n_sink=0, n_local=3, eta=1, rho=0.0), dict(n_sink=1, n_local=2, eta=7, rho=0.5, seed=1 << 40)]:
+        cfg = bf.Config(b=256, g=64, **kw)
+        q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+        o = torch.empty_like(q)
+        P = bf.make_problem(q, k, v, o, head_offset=5)
+        m = bf.alloc_mask(P, cfg, labels=True)
+        coarse = (rng.random((B, Hkv, m.Lq, m.Lkv)) < 0.1).astype(np.uint8)
+        words = np.zeros(m.coarse_bits.shape, np.int64)
+        for j in range(m.Lkv):
+            words[..., j // 32] |= coarse[..., j].astype(np.int64) << (j % 32)
+        words = np.where(words >= 2 ** 31, words - 2 ** 32, words)
+        m.coarse_bits.copy_(torch.from_numpy(words.astype(np.int32)))
+        bf.bfla_expand_rescue(P, cfg, m)
+        torch.cuda.synchronize()
+        want = np.stack([oracle.expand_rescue(coarse[r], N, N, 256, 64, cfg.n_sink, cfg.n_local, cfg.eta, cfg.rho,
+                                              cfg.seed, head_offset=5) for r in range(B)])
+        assert np.array_equal(m.tile_label.cpu().numpy(), want)
+        gpu = dict(count=m.tile_count.cpu().numpy(), list=m.tile_list.cpu().numpy())
+        check_lists(gpu, want, N, N, 64)
+
+
+def test_dense_matches_oracle_and_sdpa():
+    prob = workloads.gaussian(31, B=1, Hq=4, Hkv=2, Nq=1100, Nkv=1300, d=128, sigma=1.0)
+    gpu = run_gpu(prob, None)
+    (o_ref, lse_ref), = oracle_attention(prob, None, 64)
+    compare_o(gpu["o"][0], o_ref, "dense")
+    assert np.abs(gpu["lse"][0].cpu().numpy() - lse_ref).max() <= 1e-3
+
+
+def test_keep_all_sparse_equals_dense_bitwise():
+    prob = workloads.gaussian(41, B=1, Hq=8, Hkv=2, Nq=1280, Nkv=1280, d=128, sigma=0.5)
+    dense = run_gpu(prob, None)
+    sparse = run_gpu(prob, bf.Config(b=128, g=64, gamma=1.0))
+    assert torch.equal(dense["o"], sparse["o"])
+    assert torch.equal(dense["lse"], sparse["lse"])
+
+
+@pytest.mark.parametrize("page", [16, 32, 64])
+def test_paged_equals_contiguous(page):
+    prob = workloads.gaussian(51, B=2, Hq=8, Hkv=2, Nq=1000, Nkv=1000, d=128, sigma=0.9)
+    cfg = bf.Config(b=128, g=64, gamma=0.95, eta=8, rho=0.1)
+    a = run_gpu(prob, cfg)
+    b = run_gpu(prob, cfg, paged_page=page)
+    assert np.array_equal(a["labels"], b["labels"])
+    assert torch.equal(a["o"], b["o"]), "paged O differs from contiguous O"
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(b, ref, cfg)
+    for r, (o_ref, _) in enumerate(oracle_attention(prob, labels, 64)):
+        compare_o(b["o"][r], o_ref, f"paged {page}")
+
+
+def test_head_dim_256():
+    prob = workloads.gaussian(61, B=1, Hq=4, Hkv=2, Nq=900, Nkv=900, d=256, sigma=0.8)
+    cfg = bf.Config(b=128, g=64, gamma=0.95)
+    gpu = run_gpu(prob, cfg)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    (o_ref, _), = oracle_attention(prob, labels, 64)
+    compare_o(gpu["o"][0], o_ref, "d=256")
+    dense = run_gpu(prob, None)
+    (o_ref, _), = oracle_attention(prob, None, 64)
+    compare_o(dense["o"][0], o_ref, "d=256 dense")
+
+
+def test_strided_views_and_batch():
+    # q/o as strided views of a [B, N, H, d] buffer (token-major, like a fused QKV projection)
+    B, Hq, Hkv, N, d = 2, 4, 2, 700, 128
+    prob = workloads.gaussian(71, B=B, Hq=Hq, Hkv=Hkv, Nq=N, Nkv=N, d=d)
+    qt = prob.q.cuda().transpose(1, 2).contiguous().transpose(1, 2)  # strides (N*H*d, d, H*d, 1)
+    ot = torch.empty(B, N, Hq, d, dtype=torch.bfloat16, device="cuda").transpose(1, 2)
+    cfg = bf.Config(b=128, g=64)
+    P = bf.make_problem(qt, prob.k.cuda(), prob.v.cuda(), ot)
+    bf.bfla_prefill(P, cfg, None, bf.alloc_workspace(P, cfg))
+    ref = run_gpu(prob, cfg)
+    assert torch.equal(ot.contiguous(), ref["o"])
