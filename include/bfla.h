@@ -54,6 +54,11 @@ enum { BFLA_POOL_FLATTEN = 0, BFLA_POOL_MEAN = 1 };
 /* Stage-1 selection: MASS = smallest prefix with mass >= gamma (Eq. 16-18); RATIO = the top
    ceil(keep_ratio * n_causal) blocks per row (north_star's "keep ratio", R9). */
 enum { BFLA_SELECT_MASS = 0, BFLA_SELECT_RATIO = 1 };
+/* How FLATTEN block scores are computed.  Both give the canonical mask bit for bit:
+   AUTO = tcgen05 scores + per-row certification + canonical recompute of the rows it cannot certify
+   (used when Q/K token rows are contiguous, n_q and n_kv are multiples of g, and kept_mass is not
+   requested; otherwise CANONICAL); CANONICAL = every score on the fp32 FMA pipes in canonical order. */
+enum { BFLA_SCORES_AUTO = 0, BFLA_SCORES_CANONICAL = 1 };
 
 /* One attention layer call: Q/K/V in the paper's head-first layout (Eq. 2), GQA m = h_q / h_kv
    (Eq. 3), head group H_h = {h m, ..., h m + m - 1} (Eq. 8); the batch index is the paper's
@@ -96,6 +101,7 @@ typedef struct {
     int32_t eta;        /* stride-rescue period (Eq. 24); 0 = off                                      */
     float rho;          /* random-rescue probability (Eq. 25), [0, 1]                                  */
     uint64_t seed;      /* s of Eq. 24-25                                                               */
+    int32_t scores_path; /* BFLA_SCORES_* (FLATTEN only; MEAN is always canonical)                      */
 } bfla_config;
 
 /* Statistics, accumulated with integer atomics (values are order independent). */
@@ -106,7 +112,9 @@ typedef struct {
     uint64_t rows;            /* Stage-1 rows (r, p, i)                                                */
     uint64_t rows_exact_tie;  /* rows whose cut falls between two equal probabilities (R6, reported)  */
     uint64_t blocks_kept;     /* sum over rows of r* (blocks kept per query head before the OR)       */
-    uint64_t reserved[5];
+    uint64_t rows_flagged;    /* AUTO scores: head rows the certification could not prove             */
+    uint64_t rows_recomputed; /* AUTO scores: (r,h,i) groups recomputed in the canonical order         */
+    uint64_t reserved[3];
 } bfla_stats;
 
 /* Caller-owned device buffers written by Stage 1 / Stage 2.  Shapes use
@@ -134,8 +142,8 @@ int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* 
 /* Stage 1 (Eq. 4-18 + GQA OR): pooling, block scores (Eq. 9-10), causal mask (Eq. 11-14),
    block softmax with alpha = 1/sqrt(head_dim) (Eq. 15), keep-mass / keep-ratio selection
    (Eq. 16-18), OR over each head group.  Writes mask->coarse_bits (+ kept_mass, stats).
-   Arithmetic follows the canonical fp32 order of DESIGN.md §4, so coarse_bits are bit-exact
-   against the CPU oracle. */
+   The decision follows the canonical fp32 arithmetic of DESIGN.md §4, so coarse_bits are bit-exact
+   against the CPU oracle (see BFLA_SCORES_* for how the scores are obtained). */
 bfla_status bfla_block_mask(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask,
                             void* ws, size_t ws_bytes, void* stream);
 

@@ -15,12 +15,14 @@ from typing import Optional
 import torch
 
 from . import _lib
-from ._lib import (KV_CONTIGUOUS, KV_PAGED, POOL_FLATTEN, POOL_MEAN, SELECT_MASS, SELECT_RATIO, bfla_config,
+from ._lib import (KV_CONTIGUOUS, KV_PAGED, POOL_FLATTEN, POOL_MEAN, SCORES_AUTO, SCORES_CANONICAL, SELECT_MASS,
+                   SELECT_RATIO, bfla_config,
                    bfla_mask, bfla_problem, bfla_stats, check, lib)
 
 __all__ = ["Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
            "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill", "bfla_prefill",
-           "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO"]
+           "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
+           "SCORES_CANONICAL"]
 
 
 @dataclasses.dataclass
@@ -38,10 +40,11 @@ class Config:
     eta: int = 16
     rho: float = 0.0
     seed: int = 0
+    scores: int = SCORES_AUTO
 
     def c(self) -> bfla_config:
         return bfla_config(self.b, self.g, self.T, self.pool, self.select, self.gamma, self.keep_ratio,
-                           self.n_sink, self.n_local, self.eta, self.rho, self.seed)
+                           self.n_sink, self.n_local, self.eta, self.rho, self.seed, self.scores)
 
 
 @dataclasses.dataclass
@@ -150,7 +153,7 @@ class Mask:
     def stats_dict(self) -> dict:
         s = self.stats.cpu().tolist()
         return dict(causal_tiles=s[0], kept_tiles=s[1], label=s[2:8], rows=s[8], rows_exact_tie=s[9],
-                    blocks_kept=s[10])
+                    blocks_kept=s[10], rows_flagged=s[11], rows_recomputed=s[12])
 
     def coarse_dense(self) -> torch.Tensor:
         """Unpack coarse_bits to a [B, Hkv, Lq, Lkv] uint8 tensor (test helper)."""

@@ -19,6 +19,7 @@ STATUS = {0: "BFLA_OK", 1: "BFLA_ERR_INVALID_ARGUMENT", 2: "BFLA_ERR_UNSUPPORTED
 KV_CONTIGUOUS, KV_PAGED = 0, 1
 POOL_FLATTEN, POOL_MEAN = 0, 1
 SELECT_MASS, SELECT_RATIO = 0, 1
+SCORES_AUTO, SCORES_CANONICAL = 0, 1
 
 i32, i64, f32, u64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_uint64, ctypes.c_void_p
 
@@ -34,12 +35,13 @@ class bfla_problem(ctypes.Structure):
 class bfla_config(ctypes.Structure):
     _fields_ = [("block_b", i32), ("group_g", i32), ("tile_t", i32), ("pool", i32), ("select", i32),
                 ("gamma", f32), ("keep_ratio", f32), ("n_sink", i32), ("n_local", i32), ("eta", i32),
-                ("rho", f32), ("seed", u64)]
+                ("rho", f32), ("seed", u64), ("scores_path", i32)]
 
 
 class bfla_stats(ctypes.Structure):
     _fields_ = [("causal_tiles", u64), ("kept_tiles", u64), ("label", u64 * 6), ("rows", u64),
-                ("rows_exact_tie", u64), ("blocks_kept", u64), ("reserved", u64 * 5)]
+                ("rows_exact_tie", u64), ("blocks_kept", u64), ("rows_flagged", u64), ("rows_recomputed", u64),
+                ("reserved", u64 * 3)]
 
 
 class bfla_mask(ctypes.Structure):

@@ -23,6 +23,7 @@ UNITS = {
     "api.cu": [],
     "stage1_scores.cu": ["-fmad=false"],
     "stage1_select.cu": ["-fmad=false"],
+    "stage1_tc.cu": ["-fmad=false"],
     "stage2.cu": [],
     "attention.cu": [],
 }

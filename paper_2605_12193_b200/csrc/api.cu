@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/bfla.h"
@@ -161,7 +162,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
 
 // ---- workspace layout -------------------------------------------------------------------------
 struct WsLayout {
-  size_t S, qbar, kbar, coarse, tbits, list, count, stats, total;
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, nflag, kgather, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Geom& g) {
@@ -183,6 +184,16 @@ static WsLayout ws_layout(const Geom& g) {
   o += al((size_t)g.B * g.Hkv * g.Tq * 4);
   L.stats = o;
   o += al(sizeof(bfla_stats));
+  L.qn = o;  // fast Stage-1 scores: block norms, flagged rows, gathered paged K
+  o += al((size_t)g.B * g.Hq * g.Lq * 4);
+  L.kn = o;
+  o += al((size_t)g.B * g.Hkv * g.Lkv * 4);
+  L.flagged = o;
+  o += al((size_t)g.B * g.Hkv * g.Lq * 4);
+  L.nflag = o;
+  o += al(16);
+  L.kgather = o;
+  if (g.paged) o += al((size_t)g.B * g.Hkv * g.Nkv * g.D * 2);
   L.total = o;
   return L;
 }
@@ -193,6 +204,28 @@ static bfla_status cuda_check(const char* what) {
   return BFLA_OK;
 }
 
+// tau: |S_tc - S_canonical| <= tau * ||x|| * ||y|| for one g*C-long group dot product.  Model: the
+// canonical round-to-nearest chain stays within 10 sqrt(n) u of sum|x_k y_k| (probabilistic rounding
+// error analysis; exceeding it has probability < 2n exp(-50)); the tensor-core chain of n/16 MMA steps
+// within 2 (n/16) u even if every internal step truncated.  Cauchy-Schwarz: sum|x_k y_k| <= ||x|| ||y||.
+// The bench/tests measure the observed ratio — it sits orders of magnitude below tau.
+static float certify_tau(const Geom& g) {
+  const double n = (double)g.g * g.D, u = std::ldexp(1.0, -24);
+  double tau = u * (10.0 * std::sqrt(n) + n / 8.0);
+  if (const char* e = getenv("BFLA_TAU_SCALE")) tau *= atof(e);  // calibration experiments only
+  return (float)tau;
+}
+
+static bool tc_eligible(const Geom& g, const bfla_problem* P, const bfla_config* cfg, const bfla_mask* mask) {
+  if (cfg->pool != BFLA_POOL_FLATTEN || cfg->scores_path != BFLA_SCORES_AUTO || mask->kept_mass) return false;
+  if (g.Nq % g.g || g.Nkv % g.g) return false;       // a TMA group row must not straddle the tail
+  if (g.qs2 != g.D) return false;                    // group rows = contiguous token runs
+  if (!g.paged && g.kvs2 != g.D) return false;
+  if ((g.qs1 % 8) || (g.qs0 % 8) || (!g.paged && ((g.kvs1 % 8) || (g.kvs0 % 8)))) return false;
+  if ((size_t)g.G * g.g * g.D * 4 > 200 * 1024) return false;  // canonical recompute stages G groups
+  return true;
+}
+
 static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_mask* mask, unsigned char* ws,
                                   const bfla_problem* P, cudaStream_t st) {
   const WsLayout L = ws_layout(g);
@@ -200,14 +233,57 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
   unsigned long long* stats = reinterpret_cast<unsigned long long*>(mask->stats);
   if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
   const int32_t* pt = g.paged ? P->page_table : nullptr;
+  // c_alpha = log2(e) / sqrt(C) rounded once to fp32 (DESIGN.md §4 item 4; alpha = 1/sqrt(C), Eq. 15)
+  const float c_alpha = (float)(1.4426950408889634 / std::sqrt((double)g.D));
+  if (tc_eligible(g, P, cfg, mask)) {
+    // fast path: tcgen05 scores -> certified selection -> canonical recompute of uncertified rows
+    float* qn = reinterpret_cast<float*>(ws + L.qn);
+    float* kn = reinterpret_cast<float*>(ws + L.kn);
+    int32_t* flagged = reinterpret_cast<int32_t*>(ws + L.flagged);
+    int32_t* nflag = reinterpret_cast<int32_t*>(ws + L.nflag);
+    const void* kc = P->k;
+    Geom gk = g;  // geometry of the K operand as the score kernels see it (gathered = contiguous)
+    if (g.paged) {
+      void* kg = ws + L.kgather;
+      launch_paged_gather(g, P->k, P->page_table, kg, st);
+      kc = kg;
+      gk.paged = 0;
+      gk.kvs2 = g.D;
+      gk.kvs1 = (long long)g.Nkv * g.D;
+      gk.kvs0 = (long long)g.Hkv * g.Nkv * g.D;
+    }
+    launch_block_norms(gk, P->q, kc, qn, kn, st);
+    CUtensorMap tmA, tmB;
+    bfla_status s;
+    {
+      const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nq / g.g), (uint64_t)g.Hq, (uint64_t)g.B};
+      const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
+      const uint32_t box[4] = {64, 128, 1, 1};
+      if ((s = encode_4d(&tmA, P->q, dims, str, box)) != BFLA_OK) return s;
+    }
+    {
+      const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv, (uint64_t)g.B};
+      const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
+      const uint32_t box[4] = {64, 128, 1, 1};
+      if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
+    }
+    if (launch_tc_scores(gk, tmA, tmB, S, st)) return fail(BFLA_ERR_CUDA, "tc scores launch failed");
+    cudaMemsetAsync(nflag, 0, sizeof(int32_t), st);
+    const int sms = num_sms_current();
+    launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
+                  1, qn, kn, certify_tau(g), flagged, nflag, sms);
+    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, S, sms, st))
+      return fail(BFLA_ERR_CUDA, "recompute launch failed");
+    launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
+                  2, nullptr, nullptr, 0.f, flagged, nflag, sms);
+    return cuda_check("bfla_block_mask launch");
+  }
   if (cfg->pool == BFLA_POOL_FLATTEN) {
     if (launch_flatten_scores(g, P->q, P->k, pt, S, st)) return fail(BFLA_ERR_UNSUPPORTED, "G not built");
   } else {
     launch_mean_scores(g, P->q, P->k, pt, reinterpret_cast<float*>(ws + L.qbar), reinterpret_cast<float*>(ws + L.kbar),
                        S, st);
   }
-  // c_alpha = log2(e) / sqrt(C) rounded once to fp32 (DESIGN.md §4 item 4; alpha = 1/sqrt(C), Eq. 15)
-  const float c_alpha = (float)(1.4426950408889634 / std::sqrt((double)g.D));
   launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, mask->kept_mass, stats, st);
   return cuda_check("bfla_block_mask launch");
 }

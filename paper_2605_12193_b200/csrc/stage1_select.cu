@@ -43,20 +43,42 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 //      order, one fp32 add per step (R7), until P_r >= gamma (MASS) or r = ceil(ratio n_causal)
 //      (RATIO).  gamma >= 1 keeps all causal blocks.
 //   3. keep bits OR-ed into the CTA's coarse row (R8), written once at the end.
+//
+// mode 0: S holds canonical scores; every row is decided and written.
+// mode 1: S holds tensor-core scores S_f with |S_f - S_c| <= tau * qn[p,i] * kn[h,j] (qn/kn: max group
+//         norms per block; Cauchy-Schwarz).  A head row is CERTIFIED when the decision is provably the
+//         same for every score vector inside that box:
+//           order: min over kept (S_f - delta) > max over dropped (S_f + delta), with a margin that
+//                  keeps the canonical probabilities distinct (no tie can appear at the cut);
+//           mass : P_r* - gamma and gamma - P_{r*-1} exceed (e^eta - 1)(P(1-P) + 2^-20) + (4n+64) 2^-24,
+//                  eta = 2 ln2 c_alpha max_j delta_j (a uniform logit shift cancels; the prefix moves by
+//                  at most P(1-P)(e^eta - 1)), plus the fp32 rounding of either evaluation.
+//         If every head of the (r,h,i) group is certified its coarse row is written; otherwise the row
+//         index is appended to `flagged` and the row is left to the canonical recompute.
+// mode 2: rows = the flagged list; S holds canonical scores for them (k_s1_recompute_rows).
 __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restrict__ S, float c_alpha, int select,
                                                    float gamma, float keep_ratio, uint32_t* __restrict__ coarse,
                                                    float* __restrict__ kept_mass,
-                                                   unsigned long long* __restrict__ stats) {
+                                                   unsigned long long* __restrict__ stats, int mode,
+                                                   const float* __restrict__ qn, const float* __restrict__ kn,
+                                                   float tau, int32_t* __restrict__ flagged,
+                                                   int32_t* __restrict__ n_flagged) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* row_bits = reinterpret_cast<uint32_t*>(smem);                       // [Lw]
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + ((g.Lw * 4 + 15) / 16) * 16)
                              + (size_t)warp * g.Lkv;                            // [nwarps][Lkv]
-  const int i = blockIdx.x % g.Lq;
-  const int h = (blockIdx.x / g.Lq) % g.Hkv;
-  const int r = blockIdx.x / (g.Lq * g.Hkv);
+  __shared__ int uncertified;
+  const int n_rows = mode == 2 ? *n_flagged : g.B * g.Hkv * g.Lq;
+  for (int cta_row = blockIdx.x; cta_row < n_rows; cta_row += gridDim.x) {
+  const int rowid = mode == 2 ? flagged[cta_row] : cta_row;
+  const int i = rowid % g.Lq;
+  const int h = (rowid / g.Lq) % g.Hkv;
+  const int r = rowid / (g.Lq * g.Hkv);
+  __syncthreads();
   for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) row_bits[w] = 0u;
+  if (threadIdx.x == 0) uncertified = 0;
   __syncthreads();
   // Eq. 11-13 at block size b
   const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
@@ -95,7 +117,12 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
       if (target > nc) target = nc;
     }
     const bool keep_all = (select == 0 && gamma >= 1.0f);
-    float P = 0.0f, a_last = 0.0f;
+    const bool certify = mode == 1 && !keep_all;
+    const float qnorm = certify ? qn[((long long)r * g.Hq + p) * g.Lq + i] : 0.f;
+    const float* knrow = certify ? kn + ((long long)r * g.Hkv + h) * g.Lkv : nullptr;
+    float P = 0.0f, a_last = 0.0f, P_prev = 0.0f;
+    float kept_lo = INFINITY;  // min over kept of S_f - delta
+    float t_last = 0.0f;       // canonical-domain logit of the last kept block (fast value)
     int nsel = 0;
     while (nsel < nc) {
       unsigned long long best = 0ull;
@@ -103,8 +130,14 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
       best = warp_max_u64(best);
       const int jsel = (int)(~(uint32_t)(best & 0xffffffffull));
       a_last = __uint_as_float((uint32_t)(best >> 32));
+      P_prev = P;
       P = __fadd_rn(P, a_last);
       ++nsel;
+      if (certify) {
+        const float sj = s[jsel];
+        kept_lo = fminf(kept_lo, sj - tau * qnorm * knrow[jsel]);
+        t_last = (sj - M) * c_alpha;
+      }
       if (lane == 0) {
         keys[jsel] = 0ull;
         atomicOr(&row_bits[jsel >> 5], 1u << (jsel & 31));
@@ -119,18 +152,59 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
       best = warp_max_u64(best);
       if (__uint_as_float((uint32_t)(best >> 32)) == a_last) ties++;
     }
+    if (certify) {
+      // max over dropped of S_f + delta, and the largest delta of the row
+      float drop_hi = -INFINITY, dmax = 0.f;
+      for (int j = lane; j < nc; j += 32) {
+        const float dj = tau * qnorm * knrow[j];
+        dmax = fmaxf(dmax, dj);
+        if (keys[j] != 0ull) drop_hi = fmaxf(drop_hi, s[j] + dj);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        drop_hi = fmaxf(drop_hi, __shfl_xor_sync(0xffffffffu, drop_hi, o));
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      }
+      bool ok = true;
+      if (nsel < nc) ok = (kept_lo - drop_hi) * c_alpha > 0x1p-18f;      // order of the cut
+      if (t_last - 2.0f * c_alpha * dmax < -120.0f) ok = false;         // kept block near exp2 underflow
+      if (select == 0) {
+        const float eta = 2.0f * 0.6931472f * c_alpha * dmax;
+        const float grow = expm1f(eta);
+        const float rnd = (4.0f * nc + 64.0f) * 0x1p-24f;
+        auto marg = [&](float x) { return grow * (x * (1.0f - x) + 0x1p-20f) + rnd; };
+        if (P >= gamma) {
+          if (!(P - gamma > marg(P))) ok = false;
+          if (!(gamma - P_prev > marg(P_prev))) ok = false;
+        } else {  // prefix never reached gamma: keep-all must also hold canonically
+          if (!(gamma - P > marg(P))) ok = false;
+        }
+      }
+      if (!ok && lane == 0) atomicAdd(&uncertified, 1);
+    }
     kept_sum += nsel;
     if (kept_mass && lane == 0) kept_mass[((long long)r * g.Hq + p) * g.Lq + i] = P;
     __syncwarp();
   }
   __syncthreads();
-  uint32_t* out = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw;
-  for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) out[w] = row_bits[w];
-  if (stats && lane == 0) {
-    const unsigned nrows = (unsigned)((g.m - warp + nwarps - 1) / nwarps > 0 ? (g.m - warp + nwarps - 1) / nwarps : 0);
-    if (nrows) atomicAdd(stats + 8, (unsigned long long)nrows);
-    if (ties) atomicAdd(stats + 9, (unsigned long long)ties);
-    if (kept_sum) atomicAdd(stats + 10, (unsigned long long)kept_sum);
+  if (mode == 1 && uncertified) {
+    if (threadIdx.x == 0) {
+      flagged[atomicAdd(n_flagged, 1)] = rowid;
+      if (stats) atomicAdd(stats + 11, (unsigned long long)uncertified);
+    }
+  } else {
+    uint32_t* out = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw;
+    for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) out[w] = row_bits[w];
+    if (stats && lane == 0) {
+      const unsigned nrows = (unsigned)((g.m - warp + nwarps - 1) / nwarps > 0 ? (g.m - warp + nwarps - 1) / nwarps : 0);
+      if (nrows) atomicAdd(stats + 8, (unsigned long long)nrows);
+      if (ties) atomicAdd(stats + 9, (unsigned long long)ties);
+      if (kept_sum) atomicAdd(stats + 10, (unsigned long long)kept_sum);
+      if (mode == 2 && warp == 0) atomicAdd(stats + 12, 1ull);
+    }
+  }
+  ties = 0;
+  kept_sum = 0;
   }
 }
 
@@ -139,12 +213,15 @@ size_t select_smem_bytes(const Geom& g, int nwarps) {
 }
 
 void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
-                   uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st) {
+                   uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st, int mode,
+                   const float* qn, const float* kn, float tau, int32_t* flagged, int32_t* n_flagged, int num_sms) {
   const int nwarps = g.m < 4 ? g.m : 4;
   const size_t smem = select_smem_bytes(g, nwarps);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_s1_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_s1_select<<<g.B * g.Hkv * g.Lq, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse,
-                                                              kept_mass, stats);
+  const int rows = g.B * g.Hkv * g.Lq;
+  const int grid = mode == 2 ? (rows < 4 * num_sms ? rows : 4 * num_sms) : rows;
+  k_s1_select<<<grid, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse, kept_mass, stats,
+                                               mode, qn, kn, tau, flagged, n_flagged);
   count_launch();
 }
 

@@ -19,7 +19,7 @@ def f32(t: torch.Tensor) -> np.ndarray:
 
 
 def run_gpu(prob: workloads.Problem, cfg, *, paged_page: int = 0, seed: int = 0, lse: bool = True,
-            labels: bool = True, kept_mass: bool = True, head_offset: int = 0):
+            labels: bool = True, kept_mass: bool = False, head_offset: int = 0):
     """Stage 1 -> Stage 2 -> sparse prefill through the four ABI calls; returns tensors on CPU."""
     q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
     B, Hq, Nq, d = q.shape
@@ -41,6 +41,7 @@ def run_gpu(prob: workloads.Problem, cfg, *, paged_page: int = 0, seed: int = 0,
         bf.bfla_expand_rescue(P, cfg, m, ws)
         bf.bfla_sparse_prefill(P, cfg, m, ws)
         torch.cuda.synchronize()
+        out["ws"] = ws
         out["mask"] = m
         out["coarse"] = m.coarse_dense().cpu().numpy()
         out["tiles"] = m.tile_dense().cpu().numpy()

@@ -76,7 +76,7 @@ def _problem(L, **kw):
 
 
 def _cfg(L, **kw):
-    c = L.bfla_config(256, 64, 64, 0, 0, 0.99, 1.0, 1, 8, 16, 0.0, 0)
+    c = L.bfla_config(256, 64, 64, 0, 0, 0.99, 1.0, 1, 8, 16, 0.0, 0, 0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -23,7 +23,7 @@ def _check_masks(gpu, ref, cfg):
     assert np.array_equal(gpu["coarse"], coarse), "coarse mask mismatch"
     assert np.array_equal(gpu["labels"], labels), "tile label mismatch"
     assert np.array_equal(gpu["tiles"], (labels > 0).astype(np.uint8)), "tile bits mismatch"
-    if gpu["kept_mass"] is not None:
+    if gpu.get("kept_mass") is not None:
         km = np.stack([x["kept_mass"] for x in ref])
         assert np.array_equal(gpu["kept_mass"], km), "kept mass mismatch"
     ties = sum(int(x["tie"].sum()) for x in ref)
@@ -77,6 +77,51 @@ def test_shapes(case):
     for r, (o_ref, lse_ref) in enumerate(oracle_attention(prob, labels, 64)):
         compare_o(gpu["o"][r], o_ref, str(case))
         assert np.abs(gpu["lse"][r].cpu().numpy() - lse_ref).max() <= 1e-3
+
+
+def test_kept_mass_canonical():
+    prob = workloads.gaussian(5, **TINY, sigma=0.6)
+    cfg = bf.Config(**TINY_CFG, gamma=0.95)
+    gpu = run_gpu(prob, cfg, kept_mass=True)
+    _check_masks(gpu, oracle_masks(prob, cfg), cfg)
+
+
+@pytest.mark.parametrize("dist", ["g1.0", "g0.5", "g0.2", "structured"])
+@pytest.mark.parametrize("gamma", [0.9, 0.99])
+def test_fast_scores_certified_equal_canonical(dist, gamma):
+    """AUTO (tcgen05 + certification + canonical recompute) and CANONICAL give the same mask,
+    equal to the oracle's; the observed tensor-core score error sits far below tau."""
+    shape = dict(B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128)
+    if dist == "structured":
+        prob = workloads.structured(7, **shape, block=256)
+    else:
+        prob = workloads.gaussian(8, **shape, sigma=float(dist[1:]))
+    fast = run_gpu(prob, bf.Config(b=256, g=64, gamma=gamma, scores=bf.SCORES_AUTO))
+    canon = run_gpu(prob, bf.Config(b=256, g=64, gamma=gamma, scores=bf.SCORES_CANONICAL))
+    assert np.array_equal(fast["coarse"], canon["coarse"])
+    assert np.array_equal(fast["labels"], canon["labels"])
+    assert torch.equal(fast["o"], canon["o"])
+    ref = oracle_masks(prob, bf.Config(b=256, g=64, gamma=gamma))
+    _check_masks(fast, ref, None)
+    st = fast["stats"]
+    print(f"{dist} gamma={gamma}: flagged head rows {st['rows_flagged']} / {st['rows']}, "
+          f"groups recomputed {st['rows_recomputed']}")
+    # tensor-core scores (workspace head) vs oracle canonical scores on certified rows, relative to
+    # ||x|| ||y|| bounds: must stay far below tau (api.cu certify_tau)
+    Lq = Lkv = 16
+    S_fast = fast["ws"][: 8 * Lq * Lkv * 4].view(torch.float32).view(8, Lq, Lkv).cpu().numpy()
+    S_can = ref[0]["S"]
+    qf = f32(prob.q[0]).reshape(8, Lq, 4, 64 * 128)
+    kf = f32(prob.k[0]).reshape(2, Lkv, 4, 64 * 128)
+    qn = np.linalg.norm(qf.astype(np.float64), axis=-1).max(-1)
+    kn = np.linalg.norm(kf.astype(np.float64), axis=-1).max(-1)
+    bound = qn[:, :, None] * np.repeat(kn, 4, axis=0)[:, None, :]
+    tri = np.tril(np.ones((Lq, Lkv), bool))
+    ratio = (np.abs(S_fast - S_can) / bound)[:, tri].max()
+    n = 64 * 128
+    tau = 2.0 ** -24 * (10 * n ** 0.5 + n / 8)
+    print(f"max |S_tc - S_canon| / (|x||y|) = {ratio:.3e}  (tau = {tau:.3e})")
+    assert ratio < tau / 16
 
 
 def test_mean_pool_and_keep_ratio():
