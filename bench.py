@@ -328,6 +328,9 @@ def main():
             "config": config,
             "stages_ms": {"stage1_scores_select": r["s1"], "stage2_expand_rescue": r["s2"], "sparse_prefill": r["at"]},
             "kappa": r["kappa"],
+            "stage1_certification": {"head_rows": r["stats"]["rows"], "rows_flagged": r["stats"]["rows_flagged"],
+                                     "groups_recomputed": r["stats"]["rows_recomputed"],
+                                     "rows_exact_tie": r["stats"]["rows_exact_tie"]},
             "dense_ms": r["dense_ms"], "speedup_vs_dense": r["dense_ms"] / r["ms_per_step"],
             "dense_roofline": {"bound": "tensor", "achieved": r["dense_tf"], "peak": peaks["bf16"],
                                "unit": "TFLOP/s", "frac": r["dense_tf"] / peaks["bf16"]},

@@ -112,8 +112,8 @@ typedef struct {
     uint64_t rows;            /* Stage-1 rows (r, p, i)                                                */
     uint64_t rows_exact_tie;  /* rows whose cut falls between two equal probabilities (R6, reported)  */
     uint64_t blocks_kept;     /* sum over rows of r* (blocks kept per query head before the OR)       */
-    uint64_t rows_flagged;    /* AUTO scores: head rows the certification could not prove             */
-    uint64_t rows_recomputed; /* AUTO scores: (r,h,i) groups recomputed in the canonical order         */
+    uint64_t rows_flagged;    /* AUTO scores: head rows (r,p,i) the certification could not prove     */
+    uint64_t rows_recomputed; /* AUTO scores: head rows recomputed in the canonical order              */
     uint64_t reserved[3];
 } bfla_stats;
 

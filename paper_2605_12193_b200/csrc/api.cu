@@ -189,7 +189,7 @@ static WsLayout ws_layout(const Geom& g) {
   L.kn = o;
   o += al((size_t)g.B * g.Hkv * g.Lkv * 4);
   L.flagged = o;
-  o += al((size_t)g.B * g.Hkv * g.Lq * 4);
+  o += al((size_t)g.B * g.Hq * g.Lq * 4);
   L.nflag = o;
   o += al(16);
   L.kgather = o;
@@ -264,7 +264,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     {
       const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv, (uint64_t)g.B};
       const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
-      const uint32_t box[4] = {64, 128, 1, 1};
+      const uint32_t box[4] = {64, (uint32_t)kTcTileN, 1, 1};
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
     if (launch_tc_scores(gk, tmA, tmB, S, st)) return fail(BFLA_ERR_CUDA, "tc scores launch failed");

@@ -22,6 +22,7 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
                    const float* qn = nullptr, const float* kn = nullptr, float tau = 0.f,
                    int32_t* flagged = nullptr, int32_t* n_flagged = nullptr, int num_sms = 148);
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
+constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, cudaStream_t st);
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st);

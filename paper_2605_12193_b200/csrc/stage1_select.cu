@@ -34,28 +34,138 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
-// One CTA per (request r, KV head h, query block i); warp w handles query heads p = h m + w,
-// h m + w + nwarps, ...  Per row (r, p, i):
+// Selection of one head row (r, p, i) by one warp (Eq. 13-18):
 //   1. M = max over causal j of S_j (exact);  t_j = (S_j - M) * c_alpha (two roundings);
 //      e_j = exp2_canon(t_j);  Z = sum_j e_j sequentially (lane 0, ascending j);  A_j = e_j / Z.
-//   2. Selection by repeated extraction of the largest key (A_j bits, ~j): this visits the blocks
-//      in exactly the order (A desc, j asc) (R6), and the prefix P_r is accumulated in that
-//      order, one fp32 add per step (R7), until P_r >= gamma (MASS) or r = ceil(ratio n_causal)
-//      (RATIO).  gamma >= 1 keeps all causal blocks.
-//   3. keep bits OR-ed into the CTA's coarse row (R8), written once at the end.
-//
-// mode 0: S holds canonical scores; every row is decided and written.
-// mode 1: S holds tensor-core scores S_f with |S_f - S_c| <= tau * qn[p,i] * kn[h,j] (qn/kn: max group
-//         norms per block; Cauchy-Schwarz).  A head row is CERTIFIED when the decision is provably the
-//         same for every score vector inside that box:
-//           order: min over kept (S_f - delta) > max over dropped (S_f + delta), with a margin that
-//                  keeps the canonical probabilities distinct (no tie can appear at the cut);
-//           mass : P_r* - gamma and gamma - P_{r*-1} exceed (e^eta - 1)(P(1-P) + 2^-20) + (4n+64) 2^-24,
-//                  eta = 2 ln2 c_alpha max_j delta_j (a uniform logit shift cancels; the prefix moves by
-//                  at most P(1-P)(e^eta - 1)), plus the fp32 rounding of either evaluation.
-//         If every head of the (r,h,i) group is certified its coarse row is written; otherwise the row
-//         index is appended to `flagged` and the row is left to the canonical recompute.
-// mode 2: rows = the flagged list; S holds canonical scores for them (k_s1_recompute_rows).
+//   2. Repeated extraction of the largest key (A_j bits, ~j): visits the blocks in exactly the order
+//      (A desc, j asc) (R6); the prefix P_r is accumulated in that order, one fp32 add per step (R7),
+//      until P_r >= gamma (MASS) or r = ceil(ratio n_causal) (RATIO).  gamma >= 1 keeps all causal
+//      blocks.  Kept blocks end with keys[j] == 0.
+//   3. certify (mode 1 only): with |S_f - S_c| <= delta_j = tau qn kn_j, the decision is provably the
+//      canonical one iff
+//        order: min over kept (S_f - delta) > max over dropped (S_f + delta), with a margin that keeps
+//               the canonical probabilities distinct (no tie can appear at the cut), and the last kept
+//               block is far from exp2 underflow;
+//        mass : P_r* - gamma and gamma - P_{r*-1} exceed (e^eta - 1)(P(1-P) + 2^-20) + (4n+64) 2^-24,
+//               eta = 2 ln2 c_alpha max_j delta_j (a uniform logit shift cancels; the prefix moves by at
+//               most P(1-P)(e^eta - 1)), plus the fp32 rounding of either evaluation.
+struct RowResult {
+  int nsel;
+  float P;
+  bool tie, certified;
+};
+
+__device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int nc, float c_alpha, int select,
+                                float gamma, float keep_ratio, unsigned long long* keys, bool certify, float qnorm,
+                                const float* __restrict__ knrow, float tau) {
+  const int lane = threadIdx.x & 31;
+  float M = -INFINITY;
+  for (int j = lane; j < nc; j += 32) M = fmaxf(M, s[j]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float* e = reinterpret_cast<float*>(keys);  // reuse the key area for e_j (nc floats)
+  for (int j = lane; j < nc; j += 32) e[j] = exp2_canon(__fmul_rn(__fsub_rn(s[j], M), c_alpha));
+  __syncwarp();
+  float Z = 0.0f;
+  if (lane == 0)
+    for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
+  Z = __shfl_sync(0xffffffffu, Z, 0);
+  __syncwarp();
+  // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j.  Built back to front so the
+  // float area (aliasing the low half of the key array) is read before it is overwritten.
+  for (int j0 = ((nc - 1) / 32) * 32; j0 >= 0; j0 -= 32) {
+    const int j = j0 + lane;
+    float a = 0.0f;
+    if (j < nc) a = __fdiv_rn(e[j], Z);
+    __syncwarp();
+    if (j < nc) keys[j] = ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(~(uint32_t)j);
+    __syncwarp();
+  }
+  int target = nc;
+  if (select == 1) {
+    double want = ceil((double)keep_ratio * (double)nc);
+    target = (int)want;
+    if (target < 1) target = 1;
+    if (target > nc) target = nc;
+  }
+  const bool keep_all = (select == 0 && gamma >= 1.0f);
+  certify = certify && !keep_all;
+  float P = 0.0f, a_last = 0.0f, P_prev = 0.0f, kept_lo = INFINITY, t_last = 0.0f;
+  int nsel = 0;
+  while (nsel < nc) {
+    unsigned long long best = 0ull;
+    for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
+    best = warp_max_u64(best);
+    const int jsel = (int)(~(uint32_t)(best & 0xffffffffull));
+    a_last = __uint_as_float((uint32_t)(best >> 32));
+    P_prev = P;
+    P = __fadd_rn(P, a_last);
+    ++nsel;
+    if (certify) {
+      const float sj = s[jsel];
+      kept_lo = fminf(kept_lo, sj - tau * qnorm * knrow[jsel]);
+      t_last = (sj - M) * c_alpha;
+    }
+    if (lane == 0) keys[jsel] = 0ull;
+    __syncwarp();
+    if (keep_all) continue;
+    if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
+  }
+  RowResult res{nsel, P, false, true};
+  if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
+    unsigned long long best = 0ull;
+    for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
+    best = warp_max_u64(best);
+    res.tie = __uint_as_float((uint32_t)(best >> 32)) == a_last;
+  }
+  if (certify) {
+    float drop_hi = -INFINITY, dmax = 0.f;
+    for (int j = lane; j < nc; j += 32) {
+      const float dj = tau * qnorm * knrow[j];
+      dmax = fmaxf(dmax, dj);
+      if (keys[j] != 0ull) drop_hi = fmaxf(drop_hi, s[j] + dj);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      drop_hi = fmaxf(drop_hi, __shfl_xor_sync(0xffffffffu, drop_hi, o));
+      dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    bool ok = true;
+    if (nsel < nc) ok = (kept_lo - drop_hi) * c_alpha > 0x1p-18f;  // order of the cut
+    if (t_last - 2.0f * c_alpha * dmax < -120.0f) ok = false;     // kept block near exp2 underflow
+    if (select == 0) {
+      const float eta = 2.0f * 0.6931472f * c_alpha * dmax;
+      const float grow = expm1f(eta);
+      const float rnd = (4.0f * nc + 64.0f) * 0x1p-24f;
+      auto marg = [&](float x) { return grow * (x * (1.0f - x) + 0x1p-20f) + rnd; };
+      if (P >= gamma) {
+        if (!(P - gamma > marg(P))) ok = false;
+        if (!(gamma - P_prev > marg(P_prev))) ok = false;
+      } else {  // the prefix never reached gamma: keep-all must also hold canonically
+        if (!(gamma - P > marg(P))) ok = false;
+      }
+    }
+    res.certified = ok;
+  }
+  return res;
+}
+
+// OR the kept blocks (keys[j] == 0) of one head row into a coarse row (smem or global).
+__device__ __forceinline__ void or_kept(const unsigned long long* keys, int nc, uint32_t* row) {
+  const int lane = threadIdx.x & 31;
+  for (int j0 = 0; j0 < nc; j0 += 32) {
+    const int j = j0 + lane;
+    const uint32_t bal = __ballot_sync(0xffffffffu, j < nc && keys[j] == 0ull);
+    if (lane == 0 && bal) atomicOr(row + (j0 >> 5), bal);
+  }
+}
+
+// mode 0: S holds canonical scores; one CTA per (r, h, i), warp w handles query heads p = h m + w,
+//         h m + w + nwarps, ...; the OR over H_h (R8) is built in smem and written once.
+// mode 1: S holds tensor-core scores; the same, but a head row that fails certification is not OR-ed:
+//         its id (r * Hq + p) * Lq + i is appended to `flagged` for the canonical recompute.
+// mode 2: grid-stride over the flagged head rows (S now canonical for them); each row's kept bits are
+//         OR-ed atomically into the already written coarse row (OR is order independent).
 __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restrict__ S, float c_alpha, int select,
                                                    float gamma, float keep_ratio, uint32_t* __restrict__ coarse,
                                                    float* __restrict__ kept_mass,
@@ -66,145 +176,63 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* row_bits = reinterpret_cast<uint32_t*>(smem);                       // [Lw]
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + ((g.Lw * 4 + 15) / 16) * 16)
-                             + (size_t)warp * g.Lkv;                            // [nwarps][Lkv]
-  __shared__ int uncertified;
-  const int n_rows = mode == 2 ? *n_flagged : g.B * g.Hkv * g.Lq;
-  for (int cta_row = blockIdx.x; cta_row < n_rows; cta_row += gridDim.x) {
-  const int rowid = mode == 2 ? flagged[cta_row] : cta_row;
-  const int i = rowid % g.Lq;
-  const int h = (rowid / g.Lq) % g.Hkv;
-  const int r = rowid / (g.Lq * g.Hkv);
-  __syncthreads();
-  for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) row_bits[w] = 0u;
-  if (threadIdx.x == 0) uncertified = 0;
-  __syncthreads();
-  // Eq. 11-13 at block size b
-  const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-  const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;  // causal blocks
-  unsigned ties = 0, kept_sum = 0;
-  for (int pl = warp; pl < g.m; pl += nwarps) {
-    const int p = h * g.m + pl;
-    const float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    float M = -INFINITY;
-    for (int j = lane; j < nc; j += 32) M = fmaxf(M, s[j]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float* e = reinterpret_cast<float*>(keys);  // reuse the key area for e_j (nc floats)
-    for (int j = lane; j < nc; j += 32) e[j] = exp2_canon(__fmul_rn(__fsub_rn(s[j], M), c_alpha));
-    __syncwarp();
-    float Z = 0.0f;
-    if (lane == 0)
-      for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
-    Z = __shfl_sync(0xffffffffu, Z, 0);
-    __syncwarp();
-    // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j.  Built back to front so
-    // the float area (aliasing the low half of the key array) is read before it is overwritten.
-    for (int j0 = ((nc - 1) / 32) * 32; j0 >= 0; j0 -= 32) {
-      const int j = j0 + lane;
-      float a = 0.0f;
-      if (j < nc) a = __fdiv_rn(e[j], Z);
+  uint32_t* row_bits = reinterpret_cast<uint32_t*>(smem);  // [Lw]
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + ((g.Lw * 4 + 15) / 16) * 16) +
+                             (size_t)warp * g.Lkv;  // [nwarps][Lkv]
+  unsigned rows = 0, ties = 0, kept_sum = 0, unc = 0, recomputed = 0;
+  if (mode == 2) {
+    const int nf = *n_flagged;
+    for (int f = blockIdx.x * nwarps + warp; f < nf; f += gridDim.x * nwarps) {
+      const int row = flagged[f];
+      const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq), h = p / g.m;
+      const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
+      const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;
+      const float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
+      const RowResult res = select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, false, 0.f, nullptr, 0.f);
+      or_kept(keys, nc, coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw);
+      rows++, recomputed++;
+      ties += res.tie;
+      kept_sum += res.nsel;
       __syncwarp();
-      if (j < nc) keys[j] = ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(~(uint32_t)j);
-      __syncwarp();
-    }
-    int target = nc;
-    if (select == 1) {
-      double want = ceil((double)keep_ratio * (double)nc);
-      target = (int)want;
-      if (target < 1) target = 1;
-      if (target > nc) target = nc;
-    }
-    const bool keep_all = (select == 0 && gamma >= 1.0f);
-    const bool certify = mode == 1 && !keep_all;
-    const float qnorm = certify ? qn[((long long)r * g.Hq + p) * g.Lq + i] : 0.f;
-    const float* knrow = certify ? kn + ((long long)r * g.Hkv + h) * g.Lkv : nullptr;
-    float P = 0.0f, a_last = 0.0f, P_prev = 0.0f;
-    float kept_lo = INFINITY;  // min over kept of S_f - delta
-    float t_last = 0.0f;       // canonical-domain logit of the last kept block (fast value)
-    int nsel = 0;
-    while (nsel < nc) {
-      unsigned long long best = 0ull;
-      for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
-      best = warp_max_u64(best);
-      const int jsel = (int)(~(uint32_t)(best & 0xffffffffull));
-      a_last = __uint_as_float((uint32_t)(best >> 32));
-      P_prev = P;
-      P = __fadd_rn(P, a_last);
-      ++nsel;
-      if (certify) {
-        const float sj = s[jsel];
-        kept_lo = fminf(kept_lo, sj - tau * qnorm * knrow[jsel]);
-        t_last = (sj - M) * c_alpha;
-      }
-      if (lane == 0) {
-        keys[jsel] = 0ull;
-        atomicOr(&row_bits[jsel >> 5], 1u << (jsel & 31));
-      }
-      __syncwarp();
-      if (keep_all) continue;
-      if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
-    }
-    if (nsel < nc) {  // report a tie at the cut (R6): next block in order has the same probability
-      unsigned long long best = 0ull;
-      for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
-      best = warp_max_u64(best);
-      if (__uint_as_float((uint32_t)(best >> 32)) == a_last) ties++;
-    }
-    if (certify) {
-      // max over dropped of S_f + delta, and the largest delta of the row
-      float drop_hi = -INFINITY, dmax = 0.f;
-      for (int j = lane; j < nc; j += 32) {
-        const float dj = tau * qnorm * knrow[j];
-        dmax = fmaxf(dmax, dj);
-        if (keys[j] != 0ull) drop_hi = fmaxf(drop_hi, s[j] + dj);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        drop_hi = fmaxf(drop_hi, __shfl_xor_sync(0xffffffffu, drop_hi, o));
-        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-      }
-      bool ok = true;
-      if (nsel < nc) ok = (kept_lo - drop_hi) * c_alpha > 0x1p-18f;      // order of the cut
-      if (t_last - 2.0f * c_alpha * dmax < -120.0f) ok = false;         // kept block near exp2 underflow
-      if (select == 0) {
-        const float eta = 2.0f * 0.6931472f * c_alpha * dmax;
-        const float grow = expm1f(eta);
-        const float rnd = (4.0f * nc + 64.0f) * 0x1p-24f;
-        auto marg = [&](float x) { return grow * (x * (1.0f - x) + 0x1p-20f) + rnd; };
-        if (P >= gamma) {
-          if (!(P - gamma > marg(P))) ok = false;
-          if (!(gamma - P_prev > marg(P_prev))) ok = false;
-        } else {  // prefix never reached gamma: keep-all must also hold canonically
-          if (!(gamma - P > marg(P))) ok = false;
-        }
-      }
-      if (!ok && lane == 0) atomicAdd(&uncertified, 1);
-    }
-    kept_sum += nsel;
-    if (kept_mass && lane == 0) kept_mass[((long long)r * g.Hq + p) * g.Lq + i] = P;
-    __syncwarp();
-  }
-  __syncthreads();
-  if (mode == 1 && uncertified) {
-    if (threadIdx.x == 0) {
-      flagged[atomicAdd(n_flagged, 1)] = rowid;
-      if (stats) atomicAdd(stats + 11, (unsigned long long)uncertified);
     }
   } else {
+    const int i = blockIdx.x % g.Lq;
+    const int h = (blockIdx.x / g.Lq) % g.Hkv;
+    const int r = blockIdx.x / (g.Lq * g.Hkv);
+    for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) row_bits[w] = 0u;
+    __syncthreads();
+    const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
+    const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;  // causal blocks
+    for (int pl = warp; pl < g.m; pl += nwarps) {
+      const int p = h * g.m + pl;
+      const long long rowid = ((long long)r * g.Hq + p) * g.Lq + i;
+      const float* s = S + rowid * g.Lkv;
+      const bool cert = mode == 1;
+      const RowResult res = select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, cert,
+                                       cert ? qn[rowid] : 0.f, cert ? kn + ((long long)r * g.Hkv + h) * g.Lkv : nullptr,
+                                       tau);
+      if (res.certified) {
+        or_kept(keys, nc, row_bits);
+        rows++;
+        ties += res.tie;
+        kept_sum += res.nsel;
+        if (kept_mass && lane == 0) kept_mass[rowid] = res.P;
+      } else {
+        unc++;
+        if (lane == 0) flagged[atomicAdd(n_flagged, 1)] = (int32_t)rowid;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
     uint32_t* out = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw;
     for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) out[w] = row_bits[w];
-    if (stats && lane == 0) {
-      const unsigned nrows = (unsigned)((g.m - warp + nwarps - 1) / nwarps > 0 ? (g.m - warp + nwarps - 1) / nwarps : 0);
-      if (nrows) atomicAdd(stats + 8, (unsigned long long)nrows);
-      if (ties) atomicAdd(stats + 9, (unsigned long long)ties);
-      if (kept_sum) atomicAdd(stats + 10, (unsigned long long)kept_sum);
-      if (mode == 2 && warp == 0) atomicAdd(stats + 12, 1ull);
-    }
   }
-  ties = 0;
-  kept_sum = 0;
+  if (stats && lane == 0) {
+    if (rows) atomicAdd(stats + 8, (unsigned long long)rows);
+    if (ties) atomicAdd(stats + 9, (unsigned long long)ties);
+    if (kept_sum) atomicAdd(stats + 10, (unsigned long long)kept_sum);
+    if (unc) atomicAdd(stats + 11, (unsigned long long)unc);
+    if (recomputed) atomicAdd(stats + 12, (unsigned long long)recomputed);
   }
 }
 
@@ -219,7 +247,7 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
   const size_t smem = select_smem_bytes(g, nwarps);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_s1_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int rows = g.B * g.Hkv * g.Lq;
-  const int grid = mode == 2 ? (rows < 4 * num_sms ? rows : 4 * num_sms) : rows;
+  const int grid = mode == 2 ? num_sms : rows;
   k_s1_select<<<grid, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse, kept_mass, stats,
                                                mode, qn, kn, tau, flagged, n_flagged);
   count_launch();

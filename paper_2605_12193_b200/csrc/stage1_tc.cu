@@ -19,46 +19,60 @@ namespace bfla {
 namespace {
 
 constexpr int TM = 128;   // query groups per tile (MMA M)
-constexpr int TN = 128;   // key groups per tile (MMA N)
+constexpr int TN = kTcTileN;  // key groups per tile (MMA N = 256)
 constexpr int TK = 64;    // K elements per stage (one 128-byte swizzle row)
-constexpr int ST = 6;     // pipeline stages
+constexpr int ST = 4;     // pipeline stages (48 KB each)
 constexpr int ABYTES = TM * TK * 2;
 constexpr int BBYTES = TN * TK * 2;
 constexpr int SMEM = ST * (ABYTES + BBYTES) + 2 * ST * 8 + 8 + 16 + 1024;
 
-// ---- group norms: one warp per (request, head, block); each lane sums squares sequentially over a
-// strided slice of each group, lanes combine by shuffles, max over the block's groups.  The result is
-// rounded up by a relative 2^-20 so it bounds the exact norm despite fp32 rounding.
+// ---- group norms: one CTA per (request, head, block) of Q (first) or K; warp w sums the squares of
+// group w (16-byte loads, 4 in flight per lane), lanes combine by shuffles, the block keeps the max
+// over its groups.  Rounded up by a relative 2^-10 so it bounds the exact norm despite fp32 rounding.
 __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloat16* __restrict__ q,
                                                         const __nv_bfloat16* __restrict__ k, float* __restrict__ qn,
                                                         float* __restrict__ kn) {
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long nq = (long long)g.B * g.Hq * g.Lq, nk = (long long)g.B * g.Hkv * g.Lkv;
-  if (w >= nq + nk) return;
-  const bool isq = w < nq;
-  const long long u = isq ? w : w - nq;
+  __shared__ float wmax[8];
+  const long long u = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long nq = (long long)g.B * g.Hq * g.Lq;
+  const bool isq = u < nq;
+  const long long w = isq ? u : u - nq;
   const int L = isq ? g.Lq : g.Lkv, H = isq ? g.Hq : g.Hkv, N = isq ? g.Nq : g.Nkv;
-  const int blk = (int)(u % L), hh = (int)((u / L) % H), r = (int)(u / ((long long)L * H));
+  const int blk = (int)(w % L), hh = (int)((w / L) % H), r = (int)(w / ((long long)L * H));
+  const int vec_per_tok = g.D / 8;
   float best = 0.f;
-  for (int grp = 0; grp < g.G; ++grp) {
+  for (int grp = warp; grp < g.G; grp += 8) {
     const int t0 = blk * g.b + grp * g.g;
+    const int ntok = min(g.g, N - t0);
     float acc = 0.f;
-    for (int t = t0; t < t0 + g.g && t < N; ++t) {
-      const __nv_bfloat16* row = isq ? q + (long long)r * g.qs0 + (long long)hh * g.qs1 + (long long)t * g.qs2
-                                     : k + (long long)r * g.kvs0 + (long long)hh * g.kvs1 + (long long)t * g.kvs2;
-      for (int c = lane * 4; c < g.D; c += 128) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(row + c);
-        const float a = __uint_as_float(raw.x << 16), b2 = __uint_as_float(raw.x & 0xffff0000u);
-        const float c3 = __uint_as_float(raw.y << 16), d4 = __uint_as_float(raw.y & 0xffff0000u);
-        acc = fmaf(a, a, fmaf(b2, b2, fmaf(c3, c3, fmaf(d4, d4, acc))));
+    if (ntok > 0) {
+      const int nvec = ntok * vec_per_tok;
+#pragma unroll 4
+      for (int x = lane; x < nvec; x += 32) {
+        const int t = t0 + x / vec_per_tok, c = (x % vec_per_tok) * 8;
+        const __nv_bfloat16* row = isq ? q + (long long)r * g.qs0 + (long long)hh * g.qs1 + (long long)t * g.qs2
+                                       : k + (long long)r * g.kvs0 + (long long)hh * g.kvs1 + (long long)t * g.kvs2;
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + c));
+        const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a = __uint_as_float(w4[e] << 16), b2 = __uint_as_float(w4[e] & 0xffff0000u);
+          acc = fmaf(a, a, fmaf(b2, b2, acc));
+        }
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     best = fmaxf(best, acc);
   }
-  if (lane == 0) (isq ? qn : kn)[u] = sqrtf(best) * (1.0f + 0x1p-10f) + 1e-30f;  // fp32 sum slack
+  if (lane == 0) wmax[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    for (int e = 0; e < 8; ++e) m = fmaxf(m, wmax[e]);
+    (isq ? qn : kn)[w] = sqrtf(m) * (1.0f + 0x1p-10f) + 1e-30f;  // fp32 sum slack
+  }
 }
 
 // ---- tcgen05 scores: one CTA per (request, query head, M tile of 128 query groups, N tile of 128 key
@@ -95,7 +109,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<128>(tslot);
+  if (warp == 2) tmem_alloc<TN>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -156,94 +170,105 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<128>(tmem);
+    tmem_dealloc<TN>(tmem);
   }
 }
 
-// ---- canonical recompute of flagged rows: for each flagged (request, KV head, query block) and each
-// query head p of its group, S[p,i,j] for all causal j in exactly the canonical order (one fp32 FMA
-// per element, ascending).  Work unit = (flagged row, head p, chunk of 32 KV blocks); a thread owns one
-// (j, u, v) dot product and reads its key group straight from L2; the CTA stages the query groups.
+// ---- canonical recompute of flagged head rows.  Work unit = (flagged head row (r,p,i), chunk of 16 KV
+// blocks).  Per k-chunk of 32 elements the CTA stages the G query groups and the 16*G key groups of
+// the chunk (coalesced 16-byte loads, fp32 in padded smem); thread t owns dot product (j, u, v) and
+// adds the chunk's 32 products in ascending order with single-rounding FMAs — exactly the canonical
+// chain (the k loop is outermost and ascending).  The G x G max is taken through smem.
+template <int G>
 __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bfloat16* __restrict__ q,
                                                            const __nv_bfloat16* __restrict__ k,
-                                                           const int32_t* __restrict__ pt,
                                                            const int32_t* __restrict__ flagged,
-                                                           const int32_t* __restrict__ n_flagged, float* __restrict__ S) {
-  extern __shared__ __align__(16) float sq[];  // [G][g*D] query groups of (p, i) as fp32
-  __shared__ float part[256];
+                                                           const int32_t* __restrict__ n_flagged,
+                                                           float* __restrict__ S) {
+  constexpr int KC = 32, KP = 33, JB = 16;
+  constexpr int NA = G, NB = JB * G, NDOT = JB * G * G;
+  __shared__ float sa[NA * KP];
+  __shared__ float sb[NB * KP];
+  __shared__ float part[NDOT];
   const int nf = *n_flagged;
-  const int chunks = (g.Lkv + 31) / 32;
-  const long long units = (long long)nf * g.m * chunks;
+  const int chunks = (g.Lkv + JB - 1) / JB;
+  const long long units = (long long)nf * chunks;
   const int gc = g.g * g.D;
   for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
     const int chunk = (int)(unit % chunks);
-    const int pl = (int)((unit / chunks) % g.m);
-    const int row = flagged[unit / ((long long)chunks * g.m)];  // (r * Hkv + h) * Lq + i
-    const int i = row % g.Lq, h = (row / g.Lq) % g.Hkv, r = row / (g.Lq * g.Hkv);
-    const int p = h * g.m + pl;
+    const int row = flagged[unit / chunks];  // (r * Hq + p) * Lq + i
+    const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
+    const int h = p / g.m;
     long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
     if (e_i > g.Nkv - 1) e_i = g.Nkv - 1;
     const int jmax = (int)(e_i / g.b);
-    const int j0 = chunk * 32;
-    __syncthreads();
-    if (j0 > jmax) continue;
-    // stage the G query groups (fp32, zero padded)
-    for (int x = threadIdx.x; x < g.G * gc; x += blockDim.x) {
-      const int u = x / gc, e = x % gc;
-      const int t = i * g.b + u * g.g + e / g.D;
-      sq[x] = t < g.Nq ? __bfloat162float(q[(long long)r * g.qs0 + (long long)p * g.qs1 + (long long)t * g.qs2 + e % g.D])
-                       : 0.0f;
-    }
-    __syncthreads();
-    const int per = 32 * g.G * g.G;  // dot products in this chunk
-    for (int d0 = 0; d0 < per; d0 += blockDim.x) {
-      const int di = d0 + threadIdx.x;
-      float acc = -INFINITY;
-      if (di < per) {
-        const int jl = di / (g.G * g.G), uv = di % (g.G * g.G), u = uv / g.G, v = uv % g.G;
-        const int j = j0 + jl;
-        const int s0 = j * g.b + v * g.g;
-        if (j <= jmax && i * g.b + u * g.g < g.Nq && s0 < g.Nkv) {
-          const float* x = sq + u * gc;
-          acc = 0.0f;
-          for (int t = 0; t < g.g; ++t) {
-            const int s = s0 + t;
-            const __nv_bfloat16* kr = nullptr;
-            if (s < g.Nkv) {
-              if (!g.paged) kr = k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2;
-              else kr = k + (((long long)pt[(long long)r * g.max_pages + s / g.page_size] * g.page_size + s % g.page_size) * g.Hkv + h) * g.D;
-            }
-            for (int c = 0; c < g.D; c += 8) {
-              float y[8];
-              if (kr) {
-                const uint4 raw = __ldg(reinterpret_cast<const uint4*>(kr + c));
-                const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+    const int j0 = chunk * JB;
+    if (j0 > jmax) continue;  // uniform over the CTA
+    float acc[(NDOT + 255) / 256];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  y[2 * e] = __uint_as_float(w4[e] << 16);
-                  y[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
-                }
-              } else {
+    for (int e = 0; e < (NDOT + 255) / 256; ++e) acc[e] = 0.0f;
+    for (int x0 = 0; x0 < gc; x0 += KC) {
+      const int tk = x0 / g.D, c0 = x0 % g.D;  // token within the group, channel offset
+      __syncthreads();
+      // stage: NA + NB rows x 32 elements, 4 x 16 B per row
+      for (int sidx = threadIdx.x; sidx < (NA + NB) * 4; sidx += blockDim.x) {
+        const int rr = sidx >> 2, piece = sidx & 3;
+        uint4 raw = make_uint4(0, 0, 0, 0);
+        float* dst;
+        if (rr < NA) {
+          const int t = i * g.b + rr * g.g + tk;
+          if (t < g.Nq)
+            raw = __ldg(reinterpret_cast<const uint4*>(q + (long long)r * g.qs0 + (long long)p * g.qs1 +
+                                                       (long long)t * g.qs2 + c0 + piece * 8));
+          dst = sa + rr * KP + piece * 8;
+        } else {
+          const int bi = rr - NA, jl = bi / G, v = bi % G;
+          const int s = (j0 + jl) * g.b + v * g.g + tk;
+          if (j0 + jl <= jmax && s < g.Nkv)
+            raw = __ldg(reinterpret_cast<const uint4*>(k + (long long)r * g.kvs0 + (long long)h * g.kvs1 +
+                                                       (long long)s * g.kvs2 + c0 + piece * 8));
+          dst = sb + bi * KP + piece * 8;
+        }
+        const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-                for (int e = 0; e < 8; ++e) y[e] = 0.0f;
-              }
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc = __fmaf_rn(x[t * g.D + c + e], y[e], acc);
-            }
-          }
+        for (int e = 0; e < 4; ++e) {
+          dst[2 * e] = __uint_as_float(w4[e] << 16);
+          dst[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
         }
       }
-      part[threadIdx.x] = acc;
       __syncthreads();
-      // max over the G x G pairs of each block (exact)
-      if (threadIdx.x < blockDim.x / (g.G * g.G) && d0 + threadIdx.x * g.G * g.G < per) {
-        const int jl = (d0 / (g.G * g.G)) + threadIdx.x;
-        float mx = -INFINITY;
-        for (int e = 0; e < g.G * g.G; ++e) mx = fmaxf(mx, part[threadIdx.x * g.G * g.G + e]);
-        const int j = j0 + jl;
-        if (j <= jmax && j < g.Lkv) S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = mx;
+#pragma unroll
+      for (int e = 0; e < (NDOT + 255) / 256; ++e) {
+        const int di = threadIdx.x + e * 256;
+        if (di < NDOT) {
+          const int jl = di / (G * G), u = (di / G) % G, v = di % G;
+          const float* xa = sa + u * KP;
+          const float* yb = sb + (jl * G + v) * KP;
+          float a = acc[e];
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) a = __fmaf_rn(xa[kk], yb[kk], a);
+          acc[e] = a;
+        }
       }
-      __syncthreads();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < (NDOT + 255) / 256; ++e) {
+      const int di = threadIdx.x + e * 256;
+      if (di < NDOT) part[di] = acc[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < JB) {
+      const int jl = threadIdx.x, j = j0 + jl;
+      if (j <= jmax) {
+        float mx = -INFINITY;
+        for (int u = 0; u < G; ++u) {
+          if (i * g.b + u * g.g >= g.Nq) continue;  // padding-only query group (R3)
+          for (int v = 0; v < G; ++v)
+            if (j * g.b + v * g.g < g.Nkv) mx = fmaxf(mx, part[(jl * G + u) * G + v]);
+        }
+        S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = mx;
+      }
     }
   }
 }
@@ -290,20 +315,25 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
 }
 
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st) {
-  const long long warps = (long long)g.B * g.Hq * g.Lq + (long long)g.B * g.Hkv * g.Lkv;
-  k_s1_block_norms<<<(int)((warps * 32 + 255) / 256), 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(q),
+  const long long ctas = (long long)g.B * g.Hq * g.Lq + (long long)g.B * g.Hkv * g.Lkv;
+  k_s1_block_norms<<<(int)ctas, 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(q),
                                                                      static_cast<const __nv_bfloat16*>(k), qn, kn);
   count_launch();
 }
 
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
                           const int32_t* n_flagged, float* S, int num_sms, cudaStream_t st) {
-  const size_t smem = (size_t)g.G * g.g * g.D * sizeof(float);
-  if (smem > 200 * 1024) return -1;
-  cudaError_t e = cudaFuncSetAttribute(k_s1_recompute_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  k_s1_recompute_rows<<<num_sms, 256, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),
-                                                  static_cast<const __nv_bfloat16*>(k), pt, flagged, n_flagged, S);
+  (void)pt;
+  auto qq = static_cast<const __nv_bfloat16*>(q);
+  auto kk = static_cast<const __nv_bfloat16*>(k);
+  const int grid = 4 * num_sms;
+  switch (g.G) {
+    case 1: k_s1_recompute_rows<1><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
+    case 2: k_s1_recompute_rows<2><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
+    case 4: k_s1_recompute_rows<4><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
+    case 8: k_s1_recompute_rows<8><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
+    default: return -1;
+  }
   count_launch();
   return (int)cudaGetLastError();
 }
