@@ -51,6 +51,29 @@ struct Cfg {
 struct Item {
   int r, h, c, i;
 };
+
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, f in [-1/2, 1/2]),
+// 2^f by a degree-3 polynomial (relative error 7.7e-5), 2^j folded into the exponent bits.
+// x is clamped at -127 so masked entries (-inf) give +0.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(make_float2(0x1.c34984p-5f, 0x1.c34984p-5f), f, make_float2(0x1.f0dab6p-3f, 0x1.f0dab6p-3f));
+  p = __ffma2_rn(p, f, make_float2(0x1.62f51cp-1f, 0x1.62f51cp-1f));
+  p = __ffma2_rn(p, f, make_float2(0x1.fff6aep-1f, 0x1.fff6aep-1f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
 __device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
   // order: (r, h) major, query tile descending (longest rows first: LPT proxy), chunk inner
   Item it;
@@ -300,9 +323,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           for (int c = 0; c < BN; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        float mx = -INFINITY;
+        float mx = max3f(s[0], s[1], s[2]);
 #pragma unroll
-        for (int c = 0; c < BN; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 3; c + 1 < BN; c += 2) mx = max3f(mx, s[c], s[c + 1]);
+        mx = fmaxf(mx, s[BN - 1]);
         mx *= c2;
         // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom
         // in P and l); the decision is per row, the TMEM traffic is warp-uniform (.sync.aligned)
@@ -327,15 +351,26 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           tmem_wait_st();
         }
         const float msub = m_run == -INFINITY ? 0.0f : m_run;
-        float lsum = 0.0f;
+        // p = 2^(s c2 - m): pairs through FFMA2; 3 of every 8 pairs evaluate 2^x on the FMA pipe
+        // (Cody-Waite split + degree-3 polynomial, rel. err 8e-5 << bf16 rounding of P), the rest on
+        // MUFU.EX2 — balancing the two pipes (MUFU alone would match the MMA time per tile).
+        const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
+        float2 lsum2 = make_float2(0.f, 0.f);
         uint32_t pk[BN / 2];
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
-          const float p0 = ex2_approx(fmaf(s[c], c2, -msub));
-          const float p1 = ex2_approx(fmaf(s[c + 1], c2, -msub));
-          lsum += p0 + p1;
-          pk[c / 2] = pack_bf16x2(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, nm2);
+          float2 pr;
+          if ((c / 2) % 8 < 3) {
+            pr = exp2_poly2(x);
+          } else {
+            pr.x = ex2_approx(x.x);
+            pr.y = ex2_approx(x.y);
+          }
+          lsum2 = __fadd2_rn(lsum2, pr);
+          pk[c / 2] = pack_bf16x2(pr.x, pr.y);
         }
+        const float lsum = lsum2.x + lsum2.y;
         l_run += lsum;
         // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
         unsigned char* prow = sPq + row * 128;

@@ -175,25 +175,34 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 }
 
 // ---- canonical recompute of flagged head rows.  Work unit = (flagged head row (r,p,i), chunk of 16 KV
-// blocks).  Per k-chunk of 32 elements the CTA stages the G query groups and the 16*G key groups of
-// the chunk (coalesced 16-byte loads, fp32 in padded smem); thread t owns dot product (j, u, v) and
-// adds the chunk's 32 products in ascending order with single-rounding FMAs — exactly the canonical
-// chain (the k loop is outermost and ascending).  The G x G max is taken through smem.
+// blocks); thread t owns one dot product (j, u, v).  The G query groups and 16 G key groups stream
+// through a 4-stage cp.async ring in k-chunks of 128 elements (bf16, 16-byte copies, padded rows);
+// each thread adds its chunk's 128 products in ascending order with single-rounding FMAs, so every
+// dot product is exactly the canonical chain (k is the outer loop and ascending).  The G x G max is
+// taken through smem.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int G>
 __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bfloat16* __restrict__ q,
                                                            const __nv_bfloat16* __restrict__ k,
                                                            const int32_t* __restrict__ flagged,
                                                            const int32_t* __restrict__ n_flagged,
                                                            float* __restrict__ S) {
-  constexpr int KC = 32, KP = 33, JB = 16;
-  constexpr int NA = G, NB = JB * G, NDOT = JB * G * G;
-  __shared__ float sa[NA * KP];
-  __shared__ float sb[NB * KP];
-  __shared__ float part[NDOT];
+  constexpr int KC = 128, JB = 16, NST = 4;
+  constexpr int ROWS = G + JB * G, RB = KC * 2 + 16;  // row bytes padded by 16 (bank spread)
+  constexpr int NDOT = JB * G * G, PER = (NDOT + 255) / 256;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  float* part = reinterpret_cast<float*>(rsm + NST * ROWS * RB);
   const int nf = *n_flagged;
   const int chunks = (g.Lkv + JB - 1) / JB;
   const long long units = (long long)nf * chunks;
-  const int gc = g.g * g.D;
+  const int gc = g.g * g.D, nk = gc / KC;
   for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
     const int chunk = (int)(unit % chunks);
     const int row = flagged[unit / chunks];  // (r * Hq + p) * Lq + i
@@ -204,56 +213,65 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
     const int jmax = (int)(e_i / g.b);
     const int j0 = chunk * JB;
     if (j0 > jmax) continue;  // uniform over the CTA
-    float acc[(NDOT + 255) / 256];
-#pragma unroll
-    for (int e = 0; e < (NDOT + 255) / 256; ++e) acc[e] = 0.0f;
-    for (int x0 = 0; x0 < gc; x0 += KC) {
-      const int tk = x0 / g.D, c0 = x0 % g.D;  // token within the group, channel offset
-      __syncthreads();
-      // stage: NA + NB rows x 32 elements, 4 x 16 B per row
-      for (int sidx = threadIdx.x; sidx < (NA + NB) * 4; sidx += blockDim.x) {
-        const int rr = sidx >> 2, piece = sidx & 3;
-        uint4 raw = make_uint4(0, 0, 0, 0);
-        float* dst;
-        if (rr < NA) {
+    __syncthreads();          // the previous unit's readers are done with the ring
+    auto issue = [&](int kc) {
+      unsigned char* buf = rsm + (kc % NST) * ROWS * RB;
+      const int x0 = kc * KC, tk = x0 / g.D, c0 = x0 % g.D;
+      for (int sidx = threadIdx.x; sidx < ROWS * (KC / 8); sidx += blockDim.x) {
+        const int rr = sidx / (KC / 8), piece = sidx % (KC / 8);
+        const __nv_bfloat16* src = q;
+        bool ok = false;
+        if (rr < G) {
           const int t = i * g.b + rr * g.g + tk;
-          if (t < g.Nq)
-            raw = __ldg(reinterpret_cast<const uint4*>(q + (long long)r * g.qs0 + (long long)p * g.qs1 +
-                                                       (long long)t * g.qs2 + c0 + piece * 8));
-          dst = sa + rr * KP + piece * 8;
+          ok = t < g.Nq;
+          if (ok) src = q + (long long)r * g.qs0 + (long long)p * g.qs1 + (long long)t * g.qs2 + c0 + piece * 8;
         } else {
-          const int bi = rr - NA, jl = bi / G, v = bi % G;
+          const int bi = rr - G, jl = bi / G, v = bi % G;
           const int s = (j0 + jl) * g.b + v * g.g + tk;
-          if (j0 + jl <= jmax && s < g.Nkv)
-            raw = __ldg(reinterpret_cast<const uint4*>(k + (long long)r * g.kvs0 + (long long)h * g.kvs1 +
-                                                       (long long)s * g.kvs2 + c0 + piece * 8));
-          dst = sb + bi * KP + piece * 8;
+          ok = j0 + jl <= jmax && s < g.Nkv;
+          if (ok) src = k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2 + c0 + piece * 8;
         }
-        const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          dst[2 * e] = __uint_as_float(w4[e] << 16);
-          dst[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
-        }
+        cp_async16(buf + rr * RB + piece * 16, src, ok);  // zero-filled when !ok (padding)
       }
-      __syncthreads();
+      cp_async_commit();
+    };
+    float acc[PER];
 #pragma unroll
-      for (int e = 0; e < (NDOT + 255) / 256; ++e) {
+    for (int e = 0; e < PER; ++e) acc[e] = 0.0f;
+    for (int kc = 0; kc < NST - 1; ++kc) {
+      if (kc < nk) issue(kc);
+      else cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      cp_async_wait<NST - 2>();
+      __syncthreads();
+      if (kc + NST - 1 < nk) issue(kc + NST - 1);
+      else cp_async_commit();
+      const unsigned char* buf = rsm + (kc % NST) * ROWS * RB;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
         const int di = threadIdx.x + e * 256;
         if (di < NDOT) {
           const int jl = di / (G * G), u = (di / G) % G, v = di % G;
-          const float* xa = sa + u * KP;
-          const float* yb = sb + (jl * G + v) * KP;
+          const uint2* xa = reinterpret_cast<const uint2*>(buf + u * RB);
+          const uint2* yb = reinterpret_cast<const uint2*>(buf + (G + jl * G + v) * RB);
           float a = acc[e];
-#pragma unroll
-          for (int kk = 0; kk < KC; ++kk) a = __fmaf_rn(xa[kk], yb[kk], a);
+#pragma unroll 8
+          for (int q4 = 0; q4 < KC / 4; ++q4) {
+            const uint2 xv = xa[q4], yv = yb[q4];
+            a = __fmaf_rn(__uint_as_float(xv.x << 16), __uint_as_float(yv.x << 16), a);
+            a = __fmaf_rn(__uint_as_float(xv.x & 0xffff0000u), __uint_as_float(yv.x & 0xffff0000u), a);
+            a = __fmaf_rn(__uint_as_float(xv.y << 16), __uint_as_float(yv.y << 16), a);
+            a = __fmaf_rn(__uint_as_float(xv.y & 0xffff0000u), __uint_as_float(yv.y & 0xffff0000u), a);
+          }
           acc[e] = a;
         }
       }
     }
+    cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < (NDOT + 255) / 256; ++e) {
+    for (int e = 0; e < PER; ++e) {
       const int di = threadIdx.x + e * 256;
       if (di < NDOT) part[di] = acc[e];
     }
@@ -326,12 +344,16 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
   (void)pt;
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
-  const int grid = 4 * num_sms;
+  auto go = [&](auto kern, int G) {
+    const size_t smem = (size_t)4 * (G + 16 * G) * (128 * 2 + 16) + (size_t)16 * G * G * 4;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<2 * num_sms, 256, smem, st>>>(g, qq, kk, flagged, n_flagged, S);
+  };
   switch (g.G) {
-    case 1: k_s1_recompute_rows<1><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
-    case 2: k_s1_recompute_rows<2><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
-    case 4: k_s1_recompute_rows<4><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
-    case 8: k_s1_recompute_rows<8><<<grid, 256, 0, st>>>(g, qq, kk, flagged, n_flagged, S); break;
+    case 1: go(k_s1_recompute_rows<1>, 1); break;
+    case 2: go(k_s1_recompute_rows<2>, 2); break;
+    case 4: go(k_s1_recompute_rows<4>, 4); break;
+    case 8: go(k_s1_recompute_rows<8>, 8); break;
     default: return -1;
   }
   count_launch();
