@@ -42,10 +42,12 @@ struct Cfg {
   static constexpr int OFF_V = OFF_K + STAGES * KVBYTES;
   static constexpr int OFF_P = OFF_V + STAGES * KVBYTES;
   static constexpr int OFF_BAR = OFF_P + NQT * PBYTES;
-  static constexpr int NBAR = 2 + 4 * STAGES + 4 * NQT;
+  static constexpr int NBAR = 2 + 4 * STAGES + 7 * NQT;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + tmem slot + alignment slack
   static constexpr int THREADS = 128 + 128 * NQT;
-  static constexpr int COL_O = D == 128 ? 128 : 256;  // TMEM column of O_0 (S_q at 64 q)
+  // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q after them
+  static constexpr int COL_S = 0;
+  static constexpr int COL_O = D == 128 ? 256 : 256;
 };
 
 struct Item {
@@ -60,10 +62,10 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
 
 // 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, f in [-1/2, 1/2]),
 // 2^f by a degree-3 polynomial (relative error 7.7e-5), 2^j folded into the exponent bits.
-// x is clamped at -127 so masked entries (-inf) give +0.
+// x is clamped at -126 so the exponent field cannot wrap: masked entries (-inf) give a denormal ~2^-126.
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
   const float2 t = __fadd2_rn(x, magic);
   const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
@@ -102,10 +104,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
   uint64_t* k_empty = k_full + C::STAGES;
   uint64_t* v_full = k_empty + C::STAGES;
   uint64_t* v_empty = v_full + C::STAGES;
-  uint64_t* s_full = v_empty + C::STAGES;  // [NQT]
-  uint64_t* p_full = s_full + NQT;         // [NQT]
-  uint64_t* o_full = p_full + NQT;         // [NQT]
-  uint64_t* o_free = o_full + NQT;         // [NQT]
+  uint64_t* s_full = v_empty + C::STAGES;  // [NQT][2]: S_q(n) landed in TMEM buffer n % 2
+  uint64_t* p_full = s_full + 2 * NQT;     // [NQT]: P_q(n) written to smem (128 arrivals)
+  uint64_t* p_free = p_full + NQT;         // [NQT]: PV_q(n) done (P buffer free, O includes PV(n))
+  uint64_t* o_full = p_free + NQT;         // [NQT]: last PV of the item done
+  uint64_t* o_free = o_full + NQT;         // [NQT]: epilogue has read O (128 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,8 +122,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
       mbar_init(v_empty + s, 1);
     }
     for (int q = 0; q < NQT; ++q) {
-      mbar_init(s_full + q, 1);
+      mbar_init(s_full + 2 * q, 1);
+      mbar_init(s_full + 2 * q + 1, 1);
       mbar_init(p_full + q, 128);
+      mbar_init(p_free + q, 1);
       mbar_init(o_full + q, 1);
       mbar_init(o_free + q, 128);
     }
@@ -172,6 +177,17 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
               tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
                           cc * 64, it.i * g.T, p, it.r);
           }
+        // warm L2 with the next item's Q (it is read from HBM exactly once)
+        if (idx + (int)gridDim.x < n_items) {
+          const Item nx = decode_item(g, idx + gridDim.x, NC);
+          for (int q = 0; q < NQT; ++q)
+            for (int s = 0; s < hpq; ++s) {
+              const int pl = nx.c * heads_in_chunk + q * hpq + s;
+              if (pl >= g.m) continue;
+              for (int cc = 0; cc < D / 64; ++cc)
+                tma_prefetch_4d(&tmQ, cc * 64, nx.i * g.T, nx.h * g.m + pl, nx.r);
+            }
+        }
         for (int n = 0; n < cnt; ++n, ++kv) {
           const int j = DENSE ? n : lst[n];
           const int st = kv % C::STAGES;
@@ -205,12 +221,24 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
+    // Per item: S_q(0), S_q(1) up front; then for each tile n: PV_q(n) as soon as P_q(n) is ready,
+    // followed by S_q(n+2) into the TMEM buffer S_q(n) just vacated — so the tensor core always has
+    // the next S ready while the softmax warps work on the current one.
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t idO = idesc_bf16(BM, D, 0, 1);
       const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K),
                      sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
-      uint32_t kv = 0, nit = 0, sp_cnt = 0;
+      uint32_t kv0 = 0, nit = 0, tc0 = 0;  // kv0: tiles loaded before this item; tc0: tiles before
+      auto issue_S = [&](int q, uint32_t tcn, uint32_t st) {
+        const uint32_t dS = tmem + C::COL_S + q * 2 * BN + (tcn & 1) * BN;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(dS, sdesc_sw128(sQ + q * C::QBYTES + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024),
+                      sdesc_sw128(sK + st * C::KVBYTES + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024), idS,
+                      kk > 0 ? 1u : 0u);
+        umma_commit(s_full + 2 * q + (tcn & 1));
+      };
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
         const Item it = decode_item(g, idx, NC);
         const int cnt = row_count(it);
@@ -218,64 +246,45 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         const uint32_t my_it = nit++;
         mbar_wait(q_full, my_it & 1);
         tc_fence_after();
-        uint32_t st_prev = 0;
-        for (int n = 0; n < cnt; ++n, ++kv) {
-          const uint32_t st = kv % C::STAGES, ph = (kv / C::STAGES) & 1;
-          mbar_wait(k_full + st, ph);
+        const int pre = cnt < 2 ? cnt : 2;
+        for (int n = 0; n < pre; ++n) {
+          const uint32_t st = (kv0 + n) % C::STAGES;
+          mbar_wait(k_full + st, ((kv0 + n) / C::STAGES) & 1);
           tc_fence_after();
-          if (n > 0) {
-            mbar_wait(v_full + st_prev, ((kv - 1) / C::STAGES) & 1);
-            tc_fence_after();
-          }
+#pragma unroll
+          for (int q = 0; q < NQT; ++q) issue_S(q, tc0 + n, st);
+          umma_commit(k_empty + st);
+          if (n == cnt - 1) umma_commit(q_empty);
+        }
+        for (int n = 0; n < cnt; ++n) {
+          const uint32_t kvn = kv0 + n, stv = kvn % C::STAGES;
+          mbar_wait(v_full + stv, (kvn / C::STAGES) & 1);
+          const bool more = n + 2 < cnt;
+          const uint32_t stk = (kvn + 2) % C::STAGES;
+          if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::STAGES) & 1);
+          tc_fence_after();
 #pragma unroll
           for (int q = 0; q < NQT; ++q) {
-            if (n > 0) {  // O_q += P_q(n-1) V_{n-1}
-              mbar_wait(p_full + q, (sp_cnt - 1) & 1);
-              tc_fence_after();
-              if (n == 1) {
-                mbar_wait(o_free + q, (my_it & 1) ^ 1);
-                tc_fence_after();
-              }
-#pragma unroll
-              for (int kk = 0; kk < BN / 16; ++kk)
-                umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
-                            sdesc_sw128(sV + st_prev * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
-                            (n > 1 || kk > 0) ? 1u : 0u);
-            }
-            // S_q = Q_q K_n^T
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              umma_f16_ss(tmem + q * BN,
-                          sdesc_sw128(sQ + q * C::QBYTES + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024),
-                          sdesc_sw128(sK + st * C::KVBYTES + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024),
-                          idS, kk > 0 ? 1u : 0u);
-            umma_commit(s_full + q);
-          }
-          ++sp_cnt;
-          umma_commit(k_empty + st);
-          if (n > 0) umma_commit(v_empty + st_prev);
-          if (n == cnt - 1) umma_commit(q_empty);  // every S MMA of the item has been issued
-          st_prev = st;
-        }
-        // tail: O_q += P_q(cnt-1) V_{cnt-1}
-        mbar_wait(v_full + st_prev, ((kv - 1) / C::STAGES) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int q = 0; q < NQT; ++q) {
-          mbar_wait(p_full + q, (sp_cnt - 1) & 1);
-          tc_fence_after();
-          if (cnt == 1) {
-            mbar_wait(o_free + q, (my_it & 1) ^ 1);
+            mbar_wait(p_full + q, (tc0 + n) & 1);
+            if (n == 0) mbar_wait(o_free + q, (my_it & 1) ^ 1);  // epilogue of the previous item read O
             tc_fence_after();
-          }
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
-                        sdesc_sw128(sV + st_prev * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
-                        (cnt > 1 || kk > 0) ? 1u : 0u);
-          umma_commit(o_full + q);
+            for (int kk = 0; kk < BN / 16; ++kk)
+              umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
+                          sdesc_sw128(sV + stv * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
+                          (n > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(p_free + q);
+            if (n == cnt - 1) umma_commit(o_full + q);
+            if (more) issue_S(q, tc0 + n + 2, stk);
+          }
+          umma_commit(v_empty + stv);
+          if (more) {
+            umma_commit(k_empty + stk);
+            if (n + 2 == cnt - 1) umma_commit(q_empty);  // every S MMA of the item has been issued
+          }
         }
-        umma_commit(v_empty + st_prev);
+        kv0 += cnt;
+        tc0 += cnt;
       }
     }
   } else if (warp >= 4) {
@@ -284,11 +293,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     const int lg = warp & 3;              // TMEM lane group of this warp
     const int row = lg * 32 + lane;       // row of Q tile q = TMEM lane
     const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + q * BN;
+    const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     unsigned char* sPq = smem + C::OFF_P + q * C::PBYTES;
-    uint32_t sp_cnt = 0, nit = 0;
+    uint32_t tc = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
       const int cnt = row_count(it);
@@ -308,13 +317,13 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
       const uint32_t my_it = nit++;
       const int32_t* lst = DENSE ? nullptr : row_list(it);
       float m_run = -INFINITY, l_run = 0.0f;
-      for (int n = 0; n < cnt; ++n, ++sp_cnt) {
+      for (int n = 0; n < cnt; ++n, ++tc) {
         const int j = DENSE ? n : __ldg(lst + n);
-        mbar_wait(s_full + q, sp_cnt & 1);
+        mbar_wait(s_full + 2 * q + (tc & 1), (tc >> 1) & 1);
         tc_fence_after();
         float s[BN];
-        tmem_ld32(tS, s);
-        tmem_ld32(tS + 32, s + 32);
+        tmem_ld32(tS0 + (tc & 1) * BN, s);
+        tmem_ld32(tS0 + (tc & 1) * BN + 32, s + 32);
         tmem_wait_ld();
         // token-exact causality inside the tile (Eq. 27): key j*64 + c visible iff <= N_c + t
         const int lim = g.Nc + t - j * BN;
@@ -323,13 +332,18 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           for (int c = 0; c < BN; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        float mx = max3f(s[0], s[1], s[2]);
+        // row max: 4 independent FMNMX3 chains, then combined
+        float m4[4];
 #pragma unroll
-        for (int c = 3; c + 1 < BN; c += 2) mx = max3f(mx, s[c], s[c + 1]);
-        mx = fmaxf(mx, s[BN - 1]);
-        mx *= c2;
-        // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom
-        // in P and l); the decision is per row, the TMEM traffic is warp-uniform (.sync.aligned)
+        for (int k4 = 0; k4 < 4; ++k4) {
+          float a = max3f(s[16 * k4], s[16 * k4 + 1], s[16 * k4 + 2]);
+#pragma unroll
+          for (int c = 3; c < 15; c += 2) a = max3f(a, s[16 * k4 + c], s[16 * k4 + c + 1]);
+          m4[k4] = fmaxf(a, s[16 * k4 + 15]);
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
+        // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in
+        // P and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
         const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
         float alpha = 1.0f;
         if (need) {
@@ -337,25 +351,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           l_run *= alpha;
           m_run = mx;
         }
-        if (n > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-          // O (complete through PV(n-1): the s_full commit covers every earlier MMA) *= alpha
-#pragma unroll 1
-          for (int cc = 0; cc < D; cc += 32) {
-            float ov[32];
-            tmem_ld32(tO + cc, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
-            tmem_st32(tO + cc, ov);
-          }
-          tmem_wait_st();
-        }
         const float msub = m_run == -INFINITY ? 0.0f : m_run;
         // p = 2^(s c2 - m): pairs through FFMA2; 3 of every 8 pairs evaluate 2^x on the FMA pipe
-        // (Cody-Waite split + degree-3 polynomial, rel. err 8e-5 << bf16 rounding of P), the rest on
-        // MUFU.EX2 — balancing the two pipes (MUFU alone would match the MMA time per tile).
+        // (rel. err 8e-5 << bf16 rounding of P), the rest on MUFU.EX2 — balancing the two pipes.
         const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
-        float2 lsum2 = make_float2(0.f, 0.f);
+        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         uint32_t pk[BN / 2];
 #pragma unroll
         for (int c = 0; c < BN; c += 2) {
@@ -367,11 +367,26 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
             pr.x = ex2_approx(x.x);
             pr.y = ex2_approx(x.y);
           }
-          lsum2 = __fadd2_rn(lsum2, pr);
+          ls[(c / 2) & 3] = __fadd2_rn(ls[(c / 2) & 3], pr);
           pk[c / 2] = pack_bf16x2(pr.x, pr.y);
         }
-        const float lsum = lsum2.x + lsum2.y;
-        l_run += lsum;
+        l_run += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+        // PV_q(n-1) must be complete: it read the P buffer we overwrite, and O must include it
+        // before a rescale.  (Issued as soon as P_q(n-1) was ready; normally long finished.)
+        if (tc > 0) mbar_wait(p_free + q, (tc - 1) & 1);
+        tc_fence_after();
+        if (n > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+#pragma unroll 1
+          for (int cc = 0; cc < D; cc += 32) {
+            float ov[32];
+            tmem_ld32(tO + cc, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+            tmem_st32(tO + cc, ov);
+          }
+          tmem_wait_st();
+        }
         // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
         unsigned char* prow = sPq + row * 128;
 #pragma unroll
