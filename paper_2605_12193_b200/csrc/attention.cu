@@ -41,8 +41,8 @@ struct Cfg {
   static constexpr int OFF_K = OFF_Q + NQT * QBYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KVBYTES;
   static constexpr int OFF_P = OFF_V + STAGES * KVBYTES;
-  static constexpr int OFF_BAR = OFF_P + NQT * PBYTES;
-  static constexpr int NBAR = 2 + 4 * STAGES + 7 * NQT;
+  static constexpr int OFF_BAR = OFF_P + 2 * NQT * PBYTES;  // P double buffer per Q tile
+  static constexpr int NBAR = 2 + 4 * STAGES + 10 * NQT;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + tmem slot + alignment slack
   static constexpr int THREADS = 128 + 128 * NQT;
   // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q after them
@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
   uint64_t* v_full = k_empty + C::STAGES;
   uint64_t* v_empty = v_full + C::STAGES;
   uint64_t* s_full = v_empty + C::STAGES;  // [NQT][2]: S_q(n) landed in TMEM buffer n % 2
-  uint64_t* p_full = s_full + 2 * NQT;     // [NQT]: P_q(n) written to smem (128 arrivals)
-  uint64_t* p_free = p_full + NQT;         // [NQT]: PV_q(n) done (P buffer free, O includes PV(n))
-  uint64_t* o_full = p_free + NQT;         // [NQT]: last PV of the item done
+  uint64_t* p_full = s_full + 2 * NQT;     // [NQT][2]: P_q(n) written to smem buffer n % 2 (128 arrivals)
+  uint64_t* p_free = p_full + 2 * NQT;     // [NQT][2]: PV_q(n) done (P buffer n % 2 free, O includes PV(n))
+  uint64_t* o_full = p_free + 2 * NQT;     // [NQT]: last PV of the item done
   uint64_t* o_free = o_full + NQT;         // [NQT]: epilogue has read O (128 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     for (int q = 0; q < NQT; ++q) {
       mbar_init(s_full + 2 * q, 1);
       mbar_init(s_full + 2 * q + 1, 1);
-      mbar_init(p_full + q, 128);
-      mbar_init(p_free + q, 1);
+      mbar_init(p_full + 2 * q, 128);
+      mbar_init(p_full + 2 * q + 1, 128);
+      mbar_init(p_free + 2 * q, 1);
+      mbar_init(p_free + 2 * q + 1, 1);
       mbar_init(o_full + q, 1);
       mbar_init(o_free + q, 128);
     }
@@ -265,15 +267,17 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < NQT; ++q) {
-            mbar_wait(p_full + q, (tc0 + n) & 1);
+            mbar_wait(p_full + 2 * q + ((tc0 + n) & 1), ((tc0 + n) >> 1) & 1);
             if (n == 0) mbar_wait(o_free + q, (my_it & 1) ^ 1);  // epilogue of the previous item read O
             tc_fence_after();
+            const uint32_t pb = (tc0 + n) & 1;
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk)
-              umma_f16_ss(tmem + C::COL_O + q * D, sdesc_sw128(sP + q * C::PBYTES + kk * 32, 16, 1024),
+              umma_f16_ss(tmem + C::COL_O + q * D,
+                          sdesc_sw128(sP + (2 * q + pb) * C::PBYTES + kk * 32, 16, 1024),
                           sdesc_sw128(sV + stv * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
                           (n > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(p_free + q);
+            umma_commit(p_free + 2 * q + pb);
             if (n == cnt - 1) umma_commit(o_full + q);
             if (more) issue_S(q, tc0 + n + 2, stk);
           }
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
-    unsigned char* sPq = smem + C::OFF_P + q * C::PBYTES;
+    unsigned char* sPq = smem + C::OFF_P + 2 * q * C::PBYTES;  // + (tc & 1) * PBYTES
     uint32_t tc = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
@@ -371,11 +375,13 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           pk[c / 2] = pack_bf16x2(pr.x, pr.y);
         }
         l_run += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
-        // PV_q(n-1) must be complete: it read the P buffer we overwrite, and O must include it
-        // before a rescale.  (Issued as soon as P_q(n-1) was ready; normally long finished.)
-        if (tc > 0) mbar_wait(p_free + q, (tc - 1) & 1);
+        // P buffer tc % 2 was last read by PV_q(tc - 2); an O rescale additionally needs PV_q(tc - 1)
+        // (O must contain it).  PV latency is hidden behind a whole softmax step in the common case.
+        if (tc >= 2) mbar_wait(p_free + 2 * q + (tc & 1), ((tc - 2) >> 1) & 1);
+        const bool resc = n > 0 && __any_sync(0xffffffffu, alpha != 1.0f);
+        if (resc) mbar_wait(p_free + 2 * q + ((tc - 1) & 1), ((tc - 1) >> 1) & 1);
         tc_fence_after();
-        if (n > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+        if (resc) {
 #pragma unroll 1
           for (int cc = 0; cc < D; cc += 32) {
             float ov[32];
@@ -388,14 +394,14 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           tmem_wait_st();
         }
         // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
-        unsigned char* prow = sPq + row * 128;
+        unsigned char* prow = sPq + (tc & 1) * C::PBYTES + row * 128;
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc)
           *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) << 4)) =
               make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(p_full + q);
+        mbar_arrive(p_full + 2 * q + (tc & 1));
       }
       // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
       mbar_wait(o_full + q, my_it & 1);
