@@ -225,71 +225,75 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     // ================================ MMA issuer ================================
     // Per item: S_q(0), S_q(1) up front; then for each tile n: PV_q(n) as soon as P_q(n) is ready,
     // followed by S_q(n+2) into the TMEM buffer S_q(n) just vacated — so the tensor core always has
-    // the next S ready while the softmax warps work on the current one.
-    if (lane == 0) {
-      constexpr uint32_t idS = idesc_bf16(BM, BN, 0, 0);
-      constexpr uint32_t idO = idesc_bf16(BM, D, 0, 1);
-      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K),
-                     sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
-      uint32_t kv0 = 0, nit = 0, tc0 = 0;  // kv0: tiles loaded before this item; tc0: tiles before
-      auto issue_S = [&](int q, uint32_t tcn, uint32_t st) {
-        const uint32_t dS = tmem + C::COL_S + q * 2 * BN + (tcn & 1) * BN;
+    // the next S ready while the softmax warps work on the current one.  The whole warp runs this
+    // loop converged; one elected lane issues each tcgen05 instruction.
+    constexpr uint32_t idS = idesc_bf16(BM, BN, 0, 0);
+    constexpr uint32_t idO = idesc_bf16(BM, D, 0, 1);
+    // descriptor bases; advancing a SW128 descriptor = adding (bytes >> 4) to its start-address field
+    const uint64_t dQ = sdesc_sw128(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t dK = sdesc_sw128(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV = sdesc_sw128(smem_u32(smem + C::OFF_V), BN * 128, 1024);
+    const uint64_t dP = sdesc_sw128(smem_u32(smem + C::OFF_P), 16, 1024);
+    uint32_t kv0 = 0, nit = 0, tc0 = 0;  // kv0: tiles loaded before this item; tc0: tiles before
+    auto issue_S = [&](int q, uint32_t tcn, uint32_t st) {
+      const uint32_t dS = tmem + C::COL_S + q * 2 * BN + (tcn & 1) * BN;
+      const uint64_t a0 = dQ + (uint64_t)((q * C::QBYTES) >> 4), b0 = dK + (uint64_t)((st * C::KVBYTES) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ss(dS, sdesc_sw128(sQ + q * C::QBYTES + (kk >> 2) * (BM * 128) + (kk & 3) * 32, 16, 1024),
-                      sdesc_sw128(sK + st * C::KVBYTES + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024), idS,
-                      kk > 0 ? 1u : 0u);
-        umma_commit(s_full + 2 * q + (tcn & 1));
-      };
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-        const Item it = decode_item(g, idx, NC);
-        const int cnt = row_count(it);
-        if (cnt == 0) continue;
-        const uint32_t my_it = nit++;
-        mbar_wait(q_full, my_it & 1);
-        tc_fence_after();
-        const int pre = cnt < 2 ? cnt : 2;
-        for (int n = 0; n < pre; ++n) {
-          const uint32_t st = (kv0 + n) % C::STAGES;
-          mbar_wait(k_full + st, ((kv0 + n) / C::STAGES) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int q = 0; q < NQT; ++q) issue_S(q, tc0 + n, st);
-          umma_commit(k_empty + st);
-          if (n == cnt - 1) umma_commit(q_empty);
-        }
-        for (int n = 0; n < cnt; ++n) {
-          const uint32_t kvn = kv0 + n, stv = kvn % C::STAGES;
-          mbar_wait(v_full + stv, (kvn / C::STAGES) & 1);
-          const bool more = n + 2 < cnt;
-          const uint32_t stk = (kvn + 2) % C::STAGES;
-          if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::STAGES) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int q = 0; q < NQT; ++q) {
-            mbar_wait(p_full + 2 * q + ((tc0 + n) & 1), ((tc0 + n) >> 1) & 1);
-            if (n == 0) mbar_wait(o_free + q, (my_it & 1) ^ 1);  // epilogue of the previous item read O
-            tc_fence_after();
-            const uint32_t pb = (tc0 + n) & 1;
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
-              umma_f16_ss(tmem + C::COL_O + q * D,
-                          sdesc_sw128(sP + (2 * q + pb) * C::PBYTES + kk * 32, 16, 1024),
-                          sdesc_sw128(sV + stv * C::KVBYTES + kk * 2048, BN * 128, 1024), idO,
-                          (n > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(p_free + 2 * q + pb);
-            if (n == cnt - 1) umma_commit(o_full + q);
-            if (more) issue_S(q, tc0 + n + 2, stk);
-          }
-          umma_commit(v_empty + stv);
-          if (more) {
-            umma_commit(k_empty + stk);
-            if (n + 2 == cnt - 1) umma_commit(q_empty);  // every S MMA of the item has been issued
-          }
-        }
-        kv0 += cnt;
-        tc0 += cnt;
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
+        const uint32_t offk = ((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4;
+        umma_f16_ss_warp(dS, a0 + off, b0 + offk, idS, kk > 0 ? 1u : 0u);
       }
+      umma_commit_warp(s_full + 2 * q + (tcn & 1));
+    };
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const Item it = decode_item(g, idx, NC);
+      const int cnt = row_count(it);
+      if (cnt == 0) continue;
+      const uint32_t my_it = nit++;
+      mbar_wait(q_full, my_it & 1);
+      tc_fence_after();
+      const int pre = cnt < 2 ? cnt : 2;
+      for (int n = 0; n < pre; ++n) {
+        const uint32_t st = (kv0 + n) % C::STAGES;
+        mbar_wait(k_full + st, ((kv0 + n) / C::STAGES) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < NQT; ++q) issue_S(q, tc0 + n, st);
+        umma_commit_warp(k_empty + st);
+        if (n == cnt - 1) umma_commit_warp(q_empty);
+      }
+      for (int n = 0; n < cnt; ++n) {
+        const uint32_t kvn = kv0 + n, stv = kvn % C::STAGES;
+        mbar_wait(v_full + stv, (kvn / C::STAGES) & 1);
+        const bool more = n + 2 < cnt;
+        const uint32_t stk = (kvn + 2) % C::STAGES;
+        if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t pb = (tc0 + n) & 1;
+#pragma unroll
+        for (int q = 0; q < NQT; ++q) {
+          mbar_wait(p_full + 2 * q + pb, ((tc0 + n) >> 1) & 1);
+          if (n == 0) mbar_wait(o_free + q, (my_it & 1) ^ 1);  // epilogue of the previous item read O
+          tc_fence_after();
+          const uint64_t a0 = dP + (uint64_t)(((2 * q + pb) * C::PBYTES) >> 4);
+          const uint64_t b0 = dV + (uint64_t)((stv * C::KVBYTES) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            umma_f16_ss_warp(tmem + C::COL_O + q * D, a0 + (uint64_t)((kk * 32) >> 4),
+                             b0 + (uint64_t)((kk * 2048) >> 4), idO, (n > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_warp(p_free + 2 * q + pb);
+          if (n == cnt - 1) umma_commit_warp(o_full + q);
+          if (more) issue_S(q, tc0 + n + 2, stk);
+        }
+        umma_commit_warp(v_empty + stv);
+        if (more) {
+          umma_commit_warp(k_empty + stk);
+          if (n + 2 == cnt - 1) umma_commit_warp(q_empty);  // every S MMA of the item has been issued
+        }
+      }
+      kv0 += cnt;
+      tc0 += cnt;
     }
   } else if (warp >= 4) {
     // ================================ softmax / epilogue ================================

@@ -124,21 +124,20 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
       tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
       tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h, r);
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {  // converged warp, one elected lane issues (see umma_f16_ss_warp)
     constexpr uint32_t idesc = idesc_bf16(TM, TN, 0, 0);
-    const uint32_t base = smem_u32(smem);
+    const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
     for (int kk = 0; kk < nk; ++kk) {
       const int s = kk % ST;
       mbar_wait(full + s, (kk / ST) & 1);
       tc_fence_after();
-      const uint32_t a = base + s * (ABYTES + BBYTES), b = a + ABYTES;
+      const uint64_t a = d0 + (uint64_t)((s * (ABYTES + BBYTES)) >> 4), b = a + (uint64_t)(ABYTES >> 4);
 #pragma unroll
       for (int k16 = 0; k16 < TK / 16; ++k16)
-        umma_f16_ss(tmem, sdesc_sw128(a + k16 * 32, 16, 1024), sdesc_sw128(b + k16 * 32, 16, 1024), idesc,
-                    (kk | k16) ? 1u : 0u);
-      umma_commit(empty + s);
+        umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk | k16) ? 1u : 0u);
+      umma_commit_warp(empty + s);
     }
-    umma_commit(done);
+    umma_commit_warp(done);
   } else if (warp >= 4) {
     const int lg = warp & 3;
     const int row = lg * 32 + lane;  // query group within the tile
