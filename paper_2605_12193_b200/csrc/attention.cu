@@ -7,7 +7,7 @@
 //
 // Warp roles (1 CTA per SM, persistent over a static LPT-ordered item sequence):
 //   warp 0        TMA producer: Q tiles per item, then K_j / V_j for every kept tile j (ring of
-//                 STAGES slots, mbarrier full/empty pairs).  Contiguous [B,H,N,d] via a 4-D
+//                 K/V stage slots, mbarrier full/empty pairs).  Contiguous [B,H,N,d] via a 4-D
 //                 tensor map, or vLLM pages [P,page,H,d] gathered page by page into the same
 //                 swizzled smem layout.
 //   warp 1        MMA issuer (one thread): S_q = Q_q K_j^T into TMEM (M=128, N=64, K=d) and
@@ -33,21 +33,24 @@ constexpr int BN = 64;   // KV tile = T
 
 template <int D, int NQT>
 struct Cfg {
-  static constexpr int STAGES = D == 128 ? 3 : 2;
+  static constexpr int KST = D == 128 ? 3 : 2;     // K stages (S runs two tiles ahead)
+  static constexpr int VST = 2;                     // V stages
   static constexpr int QBYTES = BM * D * 2;       // one 128-row Q tile
   static constexpr int KVBYTES = BN * D * 2;      // one K (or V) tile
   static constexpr int PBYTES = BM * BN * 2;      // one P tile
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQT * QBYTES;
-  static constexpr int OFF_V = OFF_K + STAGES * KVBYTES;
-  static constexpr int OFF_P = OFF_V + STAGES * KVBYTES;
+  static constexpr int OFF_V = OFF_K + KST * KVBYTES;
+  static constexpr int OFF_P = OFF_V + VST * KVBYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * NQT * PBYTES;  // P double buffer per Q tile
-  static constexpr int NBAR = 2 + 4 * STAGES + 10 * NQT;
-  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + tmem slot + alignment slack
-  static constexpr int THREADS = 128 + 128 * NQT;
-  // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q after them
+  static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 10 * NQT;
+  static constexpr int OFF_RED = OFF_BAR + ((NBAR * 8 + 16 + 127) / 128) * 128;  // row-max exchange
+  static constexpr int SMEM_TOTAL = OFF_RED + NQT * 2 * 2 * 128 * 4;  // [NQT][tc parity][half][row]
+  static constexpr int THREADS = 128 + 256 * NQT;  // 4 control warps + 2 softmax warpgroups per Q tile
+  // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q from column 256
   static constexpr int COL_S = 0;
-  static constexpr int COL_O = D == 128 ? 256 : 256;
+  static constexpr int COL_O = 256;
+  static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
 struct Item {
@@ -95,16 +98,16 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
            const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
   using C = Cfg<D, NQT>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) unsigned char smem[];
+  if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = k_full + C::STAGES;
-  uint64_t* v_full = k_empty + C::STAGES;
-  uint64_t* v_empty = v_full + C::STAGES;
-  uint64_t* s_full = v_empty + C::STAGES;  // [NQT][2]: S_q(n) landed in TMEM buffer n % 2
+  uint64_t* k_empty = k_full + C::KST;
+  uint64_t* v_full = k_empty + C::KST;
+  uint64_t* v_empty = v_full + C::VST;
+  uint64_t* s_full = v_empty + C::VST;  // [NQT][2]: S_q(n) landed in TMEM buffer n % 2
   uint64_t* p_full = s_full + 2 * NQT;     // [NQT][2]: P_q(n) written to smem buffer n % 2 (128 arrivals)
   uint64_t* p_free = p_full + 2 * NQT;     // [NQT][2]: PV_q(n) done (P buffer n % 2 free, O includes PV(n))
   uint64_t* o_full = p_free + 2 * NQT;     // [NQT]: last PV of the item done
@@ -115,21 +118,23 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < C::KST; ++s) {
       mbar_init(k_full + s, 1);
       mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
       mbar_init(v_full + s, 1);
       mbar_init(v_empty + s, 1);
     }
     for (int q = 0; q < NQT; ++q) {
       mbar_init(s_full + 2 * q, 1);
       mbar_init(s_full + 2 * q + 1, 1);
-      mbar_init(p_full + 2 * q, 128);
-      mbar_init(p_full + 2 * q + 1, 128);
+      mbar_init(p_full + 2 * q, 256);
+      mbar_init(p_full + 2 * q + 1, 256);
       mbar_init(p_free + 2 * q, 1);
       mbar_init(p_free + 2 * q + 1, 1);
       mbar_init(o_full + q, 1);
-      mbar_init(o_free + q, 128);
+      mbar_init(o_free + q, 256);
     }
     fence_barrier_init();
   }
@@ -192,9 +197,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         }
         for (int n = 0; n < cnt; ++n, ++kv) {
           const int j = DENSE ? n : lst[n];
-          const int st = kv % C::STAGES;
-          const uint32_t ph = (kv / C::STAGES) & 1;
           for (int kvsel = 0; kvsel < 2; ++kvsel) {
+            const int nst = kvsel ? C::VST : C::KST;
+            const int st = kv % nst;
+            const uint32_t ph = (kv / nst) & 1;
             uint64_t* full = (kvsel ? v_full : k_full) + st;
             mbar_wait((kvsel ? v_empty : k_empty) + st, ph ^ 1);
             mbar_arrive_expect_tx(full, C::KVBYTES);
@@ -255,8 +261,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
       tc_fence_after();
       const int pre = cnt < 2 ? cnt : 2;
       for (int n = 0; n < pre; ++n) {
-        const uint32_t st = (kv0 + n) % C::STAGES;
-        mbar_wait(k_full + st, ((kv0 + n) / C::STAGES) & 1);
+        const uint32_t st = (kv0 + n) % C::KST;
+        mbar_wait(k_full + st, ((kv0 + n) / C::KST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int q = 0; q < NQT; ++q) issue_S(q, tc0 + n, st);
@@ -264,11 +270,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         if (n == cnt - 1) umma_commit_warp(q_empty);
       }
       for (int n = 0; n < cnt; ++n) {
-        const uint32_t kvn = kv0 + n, stv = kvn % C::STAGES;
-        mbar_wait(v_full + stv, (kvn / C::STAGES) & 1);
+        const uint32_t kvn = kv0 + n, stv = kvn % C::VST;
+        mbar_wait(v_full + stv, (kvn / C::VST) & 1);
         const bool more = n + 2 < cnt;
-        const uint32_t stk = (kvn + 2) % C::STAGES;
-        if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::STAGES) & 1);
+        const uint32_t stk = (kvn + 2) % C::KST;
+        if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::KST) & 1);
         tc_fence_after();
         const uint32_t pb = (tc0 + n) & 1;
 #pragma unroll
@@ -297,14 +303,22 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     }
   } else if (warp >= 4) {
     // ================================ softmax / epilogue ================================
-    const int q = (warp - 4) >> 2;
+    // Two warpgroups per Q tile: thread (half, row) owns columns [32 half, 32 half + 32) of its row
+    // of S and [D/2 half, D/2 half + D/2) of O.  The row max is exchanged through smem once per
+    // tile (named barrier per Q tile); the running sum l stays split until the epilogue.
+    const int q = (warp - 4) >> 3;
+    const int half = ((warp - 4) >> 2) & 1;
     const int lg = warp & 3;              // TMEM lane group of this warp
     const int row = lg * 32 + lane;       // row of Q tile q = TMEM lane
     const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
-    const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN;
-    const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
+    const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN + half * (BN / 2);
+    constexpr int DH = D / 2;
+    const uint32_t tO = tmem + lane_addr + C::COL_O + q * D + half * DH;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     unsigned char* sPq = smem + C::OFF_P + 2 * q * C::PBYTES;  // + (tc & 1) * PBYTES
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + q * 512;  // [tc & 1][half][row]
+    const uint32_t bar_id = 1 + q;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory"); };
     uint32_t tc = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
@@ -314,11 +328,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
       const int t = it.i * g.T + (row % g.T);
       const bool valid = slot < hpq && pl < g.m && t < g.Nq;
       const int p = it.h * g.m + pl;
-      __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2;
+      __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2 + half * DH;
       if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
         if (valid) {
-          for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
-          if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          for (int c = 0; c < DH; ++c) orow[c] = __float2bfloat16(0.0f);
+          if (lse && half == 0) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
         }
         continue;
       }
@@ -329,29 +343,30 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         const int j = DENSE ? n : __ldg(lst + n);
         mbar_wait(s_full + 2 * q + (tc & 1), (tc >> 1) & 1);
         tc_fence_after();
-        float s[BN];
+        float s[32];
         tmem_ld32(tS0 + (tc & 1) * BN, s);
-        tmem_ld32(tS0 + (tc & 1) * BN + 32, s + 32);
         tmem_wait_ld();
-        // token-exact causality inside the tile (Eq. 27): key j*64 + c visible iff <= N_c + t
-        const int lim = g.Nc + t - j * BN;
-        if (lim < BN - 1) {
+        // token-exact causality inside the tile (Eq. 27): key j*64 + 32 half + c visible iff <= N_c + t
+        const int lim = g.Nc + t - j * BN - half * 32;
+        if (lim < 31) {
 #pragma unroll
-          for (int c = 0; c < BN; ++c)
+          for (int c = 0; c < 32; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        // row max: 4 independent FMNMX3 chains, then combined
-        float m4[4];
+        float m2[2];
 #pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          float a = max3f(s[16 * k4], s[16 * k4 + 1], s[16 * k4 + 2]);
+        for (int k2 = 0; k2 < 2; ++k2) {
+          float a = max3f(s[16 * k2], s[16 * k2 + 1], s[16 * k2 + 2]);
 #pragma unroll
-          for (int c = 3; c < 15; c += 2) a = max3f(a, s[16 * k4 + c], s[16 * k4 + c + 1]);
-          m4[k4] = fmaxf(a, s[16 * k4 + 15]);
+          for (int c = 3; c < 15; c += 2) a = max3f(a, s[16 * k2 + c], s[16 * k2 + c + 1]);
+          m2[k2] = fmaxf(a, s[16 * k2 + 15]);
         }
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
+        float* rslot = red + (tc & 1) * 256;
+        rslot[half * 128 + row] = fmaxf(m2[0], m2[1]);
+        pair_sync();
+        const float mx = fmaxf(rslot[row], rslot[128 + row]) * c2;
         // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in
-        // P and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
+        // P and l); both halves see the same mx, so they take the same decision
         const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
         float alpha = 1.0f;
         if (need) {
@@ -360,25 +375,25 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           m_run = mx;
         }
         const float msub = m_run == -INFINITY ? 0.0f : m_run;
-        // p = 2^(s c2 - m): pairs through FFMA2; 3 of every 8 pairs evaluate 2^x on the FMA pipe
-        // (rel. err 8e-5 << bf16 rounding of P), the rest on MUFU.EX2 — balancing the two pipes.
+        // p = 2^(s c2 - m): pairs through FFMA2; 1 of every 4 pairs evaluates 2^x on the FMA pipe
+        // (rel. err 8e-5 << bf16 rounding of P), the rest on MUFU.EX2.
         const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
-        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        uint32_t pk[BN / 2];
+        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t pk[16];
 #pragma unroll
-        for (int c = 0; c < BN; c += 2) {
+        for (int c = 0; c < 32; c += 2) {
           const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, nm2);
           float2 pr;
-          if ((c / 2) % 8 < 3) {
+          if ((c / 2) % 4 == 1) {
             pr = exp2_poly2(x);
           } else {
             pr.x = ex2_approx(x.x);
             pr.y = ex2_approx(x.y);
           }
-          ls[(c / 2) & 3] = __fadd2_rn(ls[(c / 2) & 3], pr);
+          ls[(c / 2) & 1] = __fadd2_rn(ls[(c / 2) & 1], pr);
           pk[c / 2] = pack_bf16x2(pr.x, pr.y);
         }
-        l_run += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+        l_run += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
         // P buffer tc % 2 was last read by PV_q(tc - 2); an O rescale additionally needs PV_q(tc - 1)
         // (O must contain it).  PV latency is hidden behind a whole softmax step in the common case.
         if (tc >= 2) mbar_wait(p_free + 2 * q + (tc & 1), ((tc - 2) >> 1) & 1);
@@ -387,7 +402,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         tc_fence_after();
         if (resc) {
 #pragma unroll 1
-          for (int cc = 0; cc < D; cc += 32) {
+          for (int cc = 0; cc < DH; cc += 32) {
             float ov[32];
             tmem_ld32(tO + cc, ov);
             tmem_wait_ld();
@@ -400,19 +415,23 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
         unsigned char* prow = sPq + (tc & 1) * C::PBYTES + row * 128;
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          *reinterpret_cast<uint4*>(prow + ((cc ^ (row & 7)) << 4)) =
+        for (int cc = 0; cc < 4; ++cc)
+          *reinterpret_cast<uint4*>(prow + (((half * 4 + cc) ^ (row & 7)) << 4)) =
               make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(p_full + 2 * q + (tc & 1));
       }
-      // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
+      // epilogue: combine the two partial sums; O / l -> bf16 -> global; LSE = (m + log2 l) ln 2
+      float* lslot = red + (tc & 1) * 256;  // the slot parity tc hasn't been written for this item
+      lslot[half * 128 + row] = l_run;
+      pair_sync();
+      const float l_tot = lslot[row] + lslot[128 + row];
       mbar_wait(o_full + q, my_it & 1);
       tc_fence_after();
-      const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+      const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
 #pragma unroll 1
-      for (int cc = 0; cc < D; cc += 32) {
+      for (int cc = 0; cc < DH; cc += 32) {
         float ov[32];
         tmem_ld32(tO + cc, ov);
         tmem_wait_ld();
@@ -425,11 +444,12 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
         }
       }
-      if (valid && lse)
+      if (valid && lse && half == 0)
         lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
-            l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+            l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
       tc_fence_before();
       mbar_arrive(o_free + q);
+      pair_sync();  // partner has read lslot before the slot is reused by the next item's tile tc
     }
   }
   tc_fence_before();
@@ -443,8 +463,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
 }  // namespace
 
 size_t attn_smem_bytes(int D, int nqt) {
-  if (D == 128) return nqt == 2 ? Cfg<128, 2>::SMEM : Cfg<128, 1>::SMEM;
-  return Cfg<256, 1>::SMEM;
+  if (D == 128) return nqt == 2 ? Cfg<128, 2>::SMEM_TOTAL : Cfg<128, 1>::SMEM_TOTAL;
+  return Cfg<256, 1>::SMEM_TOTAL;
 }
 
 template <int D, int NQT, bool PAGED, bool DENSE>
@@ -453,10 +473,10 @@ static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, co
                     cudaStream_t st) {
   using C = Cfg<D, NQT>;
   auto kern = k_attn<D, NQT, PAGED, DENSE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
+  kern<<<grid, C::THREADS, C::SMEM_TOTAL, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
                                           static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC);
   count_launch();
   return (int)cudaGetLastError();
