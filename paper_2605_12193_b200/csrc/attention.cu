@@ -158,8 +158,36 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
   };
 
+  // one K (kvsel = 0) or V (kvsel = 1) tile j of item `it` into ring slot kv % stages
+  auto load_kv = [&](int kvsel, uint32_t kv, int j, const Item& it) {
+    const int nst = kvsel ? C::VST : C::KST;
+    const int st = kv % nst;
+    const uint32_t ph = (kv / nst) & 1;
+    uint64_t* full = (kvsel ? v_full : k_full) + st;
+    mbar_wait((kvsel ? v_empty : k_empty) + st, ph ^ 1);
+    mbar_arrive_expect_tx(full, C::KVBYTES);
+    unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::KVBYTES;
+    const CUtensorMap* map = kvsel ? &tmV : &tmK;
+    if (!PAGED) {
+      for (int cc = 0; cc < D / 64; ++cc) tma_load_4d(dst + cc * (BN * 128), map, full, cc * 64, j * BN, it.h, it.r);
+    } else {
+      // vLLM pages: the 64-token tile is BN/ps page boxes of (64 cols x ps rows); a page past the
+      // request's last logical page (ragged tail) is replaced by its first page (finite data; those
+      // keys are masked by causality and get P = 0).
+      const int ps = g.page_size;
+      const int npl = (g.Nkv + ps - 1) / ps;
+      const int32_t* table = page_table + (long long)it.r * g.max_pages;
+      for (int pc = 0; pc < BN / ps; ++pc) {
+        const int lp = j * BN / ps + pc;
+        const int phys = __ldg(table + (lp < npl ? lp : 0));
+        for (int cc = 0; cc < D / 64; ++cc)
+          tma_load_4d(dst + cc * (BN * 128) + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
+      }
+    }
+  };
+
   if (warp == 0) {
-    // ================================ TMA producer ================================
+    // ================================ TMA producer (Q, K) ================================
     if (lane == 0) {
       uint32_t kv = 0, nit = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
@@ -197,34 +225,22 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         }
         for (int n = 0; n < cnt; ++n, ++kv) {
           const int j = DENSE ? n : lst[n];
-          for (int kvsel = 0; kvsel < 2; ++kvsel) {
-            const int nst = kvsel ? C::VST : C::KST;
-            const int st = kv % nst;
-            const uint32_t ph = (kv / nst) & 1;
-            uint64_t* full = (kvsel ? v_full : k_full) + st;
-            mbar_wait((kvsel ? v_empty : k_empty) + st, ph ^ 1);
-            mbar_arrive_expect_tx(full, C::KVBYTES);
-            unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::KVBYTES;
-            const CUtensorMap* map = kvsel ? &tmV : &tmK;
-            if (!PAGED) {
-              for (int cc = 0; cc < D / 64; ++cc)
-                tma_load_4d(dst + cc * (BN * 128), map, full, cc * 64, j * BN, it.h, it.r);
-            } else {
-              // vLLM pages: the 64-token tile is BN/ps page boxes of (64 cols x ps rows); a page
-              // past the request's last logical page (ragged tail) is replaced by its first page
-              // (finite data; those keys are masked by causality and get P = 0).
-              const int ps = g.page_size;
-              const int npl = (g.Nkv + ps - 1) / ps;
-              const int32_t* table = page_table + (long long)it.r * g.max_pages;
-              for (int pc = 0; pc < BN / ps; ++pc) {
-                const int lp = j * BN / ps + pc;
-                const int phys = __ldg(table + (lp < npl ? lp : 0));
-                for (int cc = 0; cc < D / 64; ++cc)
-                  tma_load_4d(dst + cc * (BN * 128) + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
-              }
-            }
-          }
+          load_kv(0, kv, j, it);
         }
+      }
+    }
+  } else if (warp == 3) {
+    // ================================ TMA producer (V) ================================
+    // V has its own ring and thread so that K loads (needed two tiles ahead by the S MMAs) never
+    // queue behind a V slot that is still being read.
+    if (lane == 0) {
+      uint32_t kv = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item it = decode_item(g, idx, NC);
+        const int cnt = row_count(it);
+        if (cnt == 0) continue;
+        const int32_t* lst = DENSE ? nullptr : row_list(it);
+        for (int n = 0; n < cnt; ++n, ++kv) load_kv(1, kv, DENSE ? n : lst[n], it);
       }
     }
   } else if (warp == 1) {
@@ -274,7 +290,6 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         mbar_wait(v_full + stv, (kvn / C::VST) & 1);
         const bool more = n + 2 < cnt;
         const uint32_t stk = (kvn + 2) % C::KST;
-        if (more) mbar_wait(k_full + stk, ((kvn + 2) / C::KST) & 1);
         tc_fence_after();
         const uint32_t pb = (tc0 + n) & 1;
 #pragma unroll
@@ -290,7 +305,13 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
                              b0 + (uint64_t)((kk * 2048) >> 4), idO, (n > 0 || kk > 0) ? 1u : 0u);
           umma_commit_warp(p_free + 2 * q + pb);
           if (n == cnt - 1) umma_commit_warp(o_full + q);
-          if (more) issue_S(q, tc0 + n + 2, stk);
+          if (more) {
+            if (q == 0) {
+              mbar_wait(k_full + stk, ((kvn + 2) / C::KST) & 1);
+              tc_fence_after();
+            }
+            issue_S(q, tc0 + n + 2, stk);
+          }
         }
         umma_commit_warp(v_empty + stv);
         if (more) {
