@@ -21,6 +21,8 @@
 // Dropped tiles are never loaded nor computed: they contribute exactly nothing (Eq. 27's -inf).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,10 +33,10 @@ namespace {
 constexpr int BM = 128;  // MMA M (rows of a Q tile)
 constexpr int BN = 64;   // KV tile = T
 
-template <int D, int NQT>
+template <int D, int NQT, int SPL>
 struct Cfg {
   static constexpr int KST = D == 128 ? 3 : 2;     // K stages (S runs two tiles ahead)
-  static constexpr int VST = 2;                     // V stages
+  static constexpr int VST = (D == 128 && SPL == 1) ? 3 : 2;  // V stages
   static constexpr int QBYTES = BM * D * 2;       // one 128-row Q tile
   static constexpr int KVBYTES = BN * D * 2;      // one K (or V) tile
   static constexpr int PBYTES = BM * BN * 2;      // one P tile
@@ -45,8 +47,8 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_P + 2 * NQT * PBYTES;  // P double buffer per Q tile
   static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 10 * NQT;
   static constexpr int OFF_RED = OFF_BAR + ((NBAR * 8 + 16 + 127) / 128) * 128;  // row-max exchange
-  static constexpr int SMEM_TOTAL = OFF_RED + NQT * 2 * 2 * 128 * 4;  // [NQT][tc parity][half][row]
-  static constexpr int THREADS = 128 + 256 * NQT;  // 4 control warps + 2 softmax warpgroups per Q tile
+  static constexpr int SMEM_TOTAL = OFF_RED + (SPL == 2 ? NQT * 2 * 2 * 128 * 4 : 0);  // [NQT][parity][half][row]
+  static constexpr int THREADS = 128 + 128 * SPL * NQT;  // 4 control warps + SPL softmax warpgroups per Q tile
   // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q from column 256
   static constexpr int COL_S = 0;
   static constexpr int COL_O = 256;
@@ -91,13 +93,13 @@ __device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
   return it;
 }
 
-template <int D, int NQT, bool PAGED, bool DENSE>
-__global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
+template <int D, int NQT, bool PAGED, bool DENSE, int SPL>
+__global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     k_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
            const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
-  using C = Cfg<D, NQT>;
+  using C = Cfg<D, NQT, SPL>;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -129,12 +131,12 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     for (int q = 0; q < NQT; ++q) {
       mbar_init(s_full + 2 * q, 1);
       mbar_init(s_full + 2 * q + 1, 1);
-      mbar_init(p_full + 2 * q, 256);
-      mbar_init(p_full + 2 * q + 1, 256);
+      mbar_init(p_full + 2 * q, 128 * SPL);
+      mbar_init(p_full + 2 * q + 1, 128 * SPL);
       mbar_init(p_free + 2 * q, 1);
       mbar_init(p_free + 2 * q + 1, 1);
       mbar_init(o_full + q, 1);
-      mbar_init(o_free + q, 256);
+      mbar_init(o_free + q, 128 * SPL);
     }
     fence_barrier_init();
   }
@@ -327,19 +329,22 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
     // Two warpgroups per Q tile: thread (half, row) owns columns [32 half, 32 half + 32) of its row
     // of S and [D/2 half, D/2 half + D/2) of O.  The row max is exchanged through smem once per
     // tile (named barrier per Q tile); the running sum l stays split until the epilogue.
-    const int q = (warp - 4) >> 3;
-    const int half = ((warp - 4) >> 2) & 1;
+    constexpr int NCOL = BN / SPL;       // S columns per thread
+    const int q = (warp - 4) / (4 * SPL);
+    const int half = SPL == 2 ? ((warp - 4) >> 2) & 1 : 0;
     const int lg = warp & 3;              // TMEM lane group of this warp
     const int row = lg * 32 + lane;       // row of Q tile q = TMEM lane
     const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
-    const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN + half * (BN / 2);
-    constexpr int DH = D / 2;
+    const uint32_t tS0 = tmem + lane_addr + C::COL_S + q * 2 * BN + half * NCOL;
+    constexpr int DH = D / SPL;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D + half * DH;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     unsigned char* sPq = smem + C::OFF_P + 2 * q * C::PBYTES;  // + (tc & 1) * PBYTES
-    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + q * 512;  // [tc & 1][half][row]
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + q * 512;  // [tc & 1][half][row] (SPL = 2)
     const uint32_t bar_id = 1 + q;
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory"); };
+    auto pair_sync = [&]() {
+      if (SPL == 2) asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
+    };
     uint32_t tc = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
@@ -364,28 +369,38 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         const int j = DENSE ? n : __ldg(lst + n);
         mbar_wait(s_full + 2 * q + (tc & 1), (tc >> 1) & 1);
         tc_fence_after();
-        float s[32];
-        tmem_ld32(tS0 + (tc & 1) * BN, s);
-        tmem_wait_ld();
-        // token-exact causality inside the tile (Eq. 27): key j*64 + 32 half + c visible iff <= N_c + t
-        const int lim = g.Nc + t - j * BN - half * 32;
-        if (lim < 31) {
+        float s[NCOL];
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
+        for (int c0 = 0; c0 < NCOL; c0 += 32) tmem_ld32(tS0 + (tc & 1) * BN + c0, s + c0);
+        tmem_wait_ld();
+        // token-exact causality inside the tile (Eq. 27): key j*64 + NCOL half + c visible iff <= N_c + t
+        const int lim = g.Nc + t - j * BN - half * NCOL;
+        if (lim < NCOL - 1) {
+#pragma unroll
+          for (int c = 0; c < NCOL; ++c)
             if (c > lim) s[c] = -INFINITY;
         }
-        float m2[2];
+        constexpr int NCH = NCOL / 16;  // independent FMNMX3 chains of 16
+        float mc[NCH];
 #pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) {
+        for (int k2 = 0; k2 < NCH; ++k2) {
           float a = max3f(s[16 * k2], s[16 * k2 + 1], s[16 * k2 + 2]);
 #pragma unroll
           for (int c = 3; c < 15; c += 2) a = max3f(a, s[16 * k2 + c], s[16 * k2 + c + 1]);
-          m2[k2] = fmaxf(a, s[16 * k2 + 15]);
+          mc[k2] = fmaxf(a, s[16 * k2 + 15]);
         }
-        float* rslot = red + (tc & 1) * 256;
-        rslot[half * 128 + row] = fmaxf(m2[0], m2[1]);
-        pair_sync();
-        const float mx = fmaxf(rslot[row], rslot[128 + row]) * c2;
+#pragma unroll
+        for (int w2 = NCH / 2; w2 >= 1; w2 /= 2)
+#pragma unroll
+          for (int k2 = 0; k2 < w2; ++k2) mc[k2] = fmaxf(mc[k2], mc[k2 + w2]);
+        float mrow = mc[0];
+        if (SPL == 2) {
+          float* rslot = red + (tc & 1) * 256;
+          rslot[half * 128 + row] = mrow;
+          pair_sync();
+          mrow = fmaxf(rslot[row], rslot[128 + row]);
+        }
+        const float mx = mrow * c2;
         // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in
         // P and l); both halves see the same mx, so they take the same decision
         const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
@@ -399,10 +414,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         // p = 2^(s c2 - m): pairs through FFMA2; 1 of every 4 pairs evaluates 2^x on the FMA pipe
         // (rel. err 8e-5 << bf16 rounding of P), the rest on MUFU.EX2.
         const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
-        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        uint32_t pk[16];
+        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t pk[NCOL / 2];
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
+        for (int c = 0; c < NCOL; c += 2) {
           const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, nm2);
           float2 pr;
           if ((c / 2) % 4 == 1) {
@@ -411,10 +426,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
             pr.x = ex2_approx(x.x);
             pr.y = ex2_approx(x.y);
           }
-          ls[(c / 2) & 1] = __fadd2_rn(ls[(c / 2) & 1], pr);
+          ls[(c / 2) & 3] = __fadd2_rn(ls[(c / 2) & 3], pr);
           pk[c / 2] = pack_bf16x2(pr.x, pr.y);
         }
-        l_run += (ls[0].x + ls[0].y) + (ls[1].x + ls[1].y);
+        l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
         // P buffer tc % 2 was last read by PV_q(tc - 2); an O rescale additionally needs PV_q(tc - 1)
         // (O must contain it).  PV latency is hidden behind a whole softmax step in the common case.
         if (tc >= 2) mbar_wait(p_free + 2 * q + (tc & 1), ((tc - 2) >> 1) & 1);
@@ -436,18 +451,21 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
         // P row -> smem, 128B-swizzled K-major (16-byte chunk cc of row r at cc ^ (r & 7))
         unsigned char* prow = sPq + (tc & 1) * C::PBYTES + row * 128;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<uint4*>(prow + (((half * 4 + cc) ^ (row & 7)) << 4)) =
+        for (int cc = 0; cc < NCOL / 8; ++cc)
+          *reinterpret_cast<uint4*>(prow + (((half * (NCOL / 8) + cc) ^ (row & 7)) << 4)) =
               make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(p_full + 2 * q + (tc & 1));
       }
       // epilogue: combine the two partial sums; O / l -> bf16 -> global; LSE = (m + log2 l) ln 2
-      float* lslot = red + (tc & 1) * 256;  // the slot parity tc hasn't been written for this item
-      lslot[half * 128 + row] = l_run;
-      pair_sync();
-      const float l_tot = lslot[row] + lslot[128 + row];
+      float l_tot = l_run;
+      if (SPL == 2) {
+        float* lslot = red + (tc & 1) * 256;  // the slot parity tc hasn't been written for this item
+        lslot[half * 128 + row] = l_run;
+        pair_sync();
+        l_tot = lslot[row] + lslot[128 + row];
+      }
       mbar_wait(o_full + q, my_it & 1);
       tc_fence_after();
       const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
@@ -484,16 +502,16 @@ __global__ void __launch_bounds__(Cfg<D, NQT>::THREADS, 1)
 }  // namespace
 
 size_t attn_smem_bytes(int D, int nqt) {
-  if (D == 128) return nqt == 2 ? Cfg<128, 2>::SMEM_TOTAL : Cfg<128, 1>::SMEM_TOTAL;
-  return Cfg<256, 1>::SMEM_TOTAL;
+  if (D == 128) return nqt == 2 ? Cfg<128, 2, 1>::SMEM_TOTAL : Cfg<128, 1, 1>::SMEM_TOTAL;
+  return Cfg<256, 1, 1>::SMEM_TOTAL;
 }
 
-template <int D, int NQT, bool PAGED, bool DENSE>
+template <int D, int NQT, bool PAGED, bool DENSE, int SPL>
 static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
                     const int32_t* pt, void* o, float* lse, int n_items, int hpq, int NC, int num_sms,
                     cudaStream_t st) {
-  using C = Cfg<D, NQT>;
-  auto kern = k_attn<D, NQT, PAGED, DENSE>;
+  using C = Cfg<D, NQT, SPL>;
+  auto kern = k_attn<D, NQT, PAGED, DENSE, SPL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;
@@ -513,7 +531,14 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
   const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
   if (items == 0) return 0;
   const int n = (int)items;
-#define BFLA_GO(D_, Q_, P_, X_) return launch_t<D_, Q_, P_, X_>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
+  // softmax warpgroups per Q tile: 1 (default) or 2 (BFLA_SOFTMAX_SPLIT=2, A/B experiments)
+  static const int spl = [] {
+    const char* e = getenv("BFLA_SOFTMAX_SPLIT");
+    return (e && atoi(e) == 2) ? 2 : 1;
+  }();
+#define BFLA_GO(D_, Q_, P_, X_)                                                                          \
+  return spl == 2 ? launch_t<D_, Q_, P_, X_, 2>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st) \
+                  : launch_t<D_, Q_, P_, X_, 1>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
   const bool paged = g.paged != 0;
   if (g.D == 128 && nqt == 2) {
     if (paged) { if (dense) BFLA_GO(128, 2, true, true); else BFLA_GO(128, 2, true, false); }
