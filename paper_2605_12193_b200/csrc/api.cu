@@ -222,7 +222,6 @@ static bool tc_eligible(const Geom& g, const bfla_problem* P, const bfla_config*
   if (g.qs2 != g.D) return false;                    // group rows = contiguous token runs
   if (!g.paged && g.kvs2 != g.D) return false;
   if ((g.qs1 % 8) || (g.qs0 % 8) || (!g.paged && ((g.kvs1 % 8) || (g.kvs0 % 8)))) return false;
-  if ((size_t)g.G * g.g * g.D * 4 > 200 * 1024) return false;  // canonical recompute stages G groups
   return true;
 }
 
