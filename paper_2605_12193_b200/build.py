@@ -26,6 +26,7 @@ UNITS = {
     "stage1_tc.cu": ["-fmad=false"],
     "stage2.cu": [],
     "attention.cu": [],
+    "attention2.cu": [],
 }
 
 

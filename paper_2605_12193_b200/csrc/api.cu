@@ -317,8 +317,14 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     if ((s = encode_4d(&maps.k, P->k, dims, str, box)) != BFLA_OK) return s;
     if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;
   }
-  int e = launch_attention(g, maps, list, count, g.paged ? P->page_table : nullptr, dense, P->o, P->lse,
-                           num_sms_current(), st);
+  // d = 128: the paired-tile kernel (attention2.cu); d = 256 (or BFLA_ATTN=1): one tile per step
+  static const bool v1 = [] {
+    const char* e = getenv("BFLA_ATTN");
+    return e && atoi(e) == 1;
+  }();
+  const int32_t* pt = g.paged ? P->page_table : nullptr;
+  int e = (g.D == 128 && !v1) ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st)
+                              : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st);
   if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
   return cuda_check("attention launch");
 }

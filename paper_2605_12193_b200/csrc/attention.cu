@@ -23,12 +23,14 @@
 
 #include <cstdlib>
 
+#include "attn_common.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
 namespace bfla {
 
 namespace {
+using namespace attn;
 
 constexpr int BM = 128;  // MMA M (rows of a Q tile)
 constexpr int BN = 64;   // KV tile = T
@@ -54,44 +56,6 @@ struct Cfg {
   static constexpr int COL_O = 256;
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
-
-struct Item {
-  int r, h, c, i;
-};
-
-__device__ __forceinline__ float max3f(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-
-// 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, f in [-1/2, 1/2]),
-// 2^f by a degree-3 polynomial (relative error 7.7e-5), 2^j folded into the exponent bits.
-// x is clamped at -126 so the exponent field cannot wrap: masked entries (-inf) give a denormal ~2^-126.
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float2 t = __fadd2_rn(x, magic);
-  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
-  float2 p = __ffma2_rn(make_float2(0x1.c34984p-5f, 0x1.c34984p-5f), f, make_float2(0x1.f0dab6p-3f, 0x1.f0dab6p-3f));
-  p = __ffma2_rn(p, f, make_float2(0x1.62f51cp-1f, 0x1.62f51cp-1f));
-  p = __ffma2_rn(p, f, make_float2(0x1.fff6aep-1f, 0x1.fff6aep-1f));
-  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-__device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
-  // order: (r, h) major, query tile descending (longest rows first: LPT proxy), chunk inner
-  Item it;
-  it.c = idx % NC;
-  int rest = idx / NC;
-  it.i = g.Tq - 1 - rest % g.Tq;
-  rest /= g.Tq;
-  it.h = rest % g.Hkv;
-  it.r = rest / g.Hkv;
-  return it;
-}
 
 template <int D, int NQT, bool PAGED, bool DENSE, int SPL>
 __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)

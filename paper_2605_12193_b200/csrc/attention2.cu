@@ -1,0 +1,467 @@
+// attention2.cu — fused sparse causal prefill (Eq. 27) and dense twin (Eq. 1), head_dim 128,
+// processing the kept-tile list TWO TILES PER STEP.
+//
+// Any two kept KV tiles (j_a, j_b) of a row fill rows 0-63 / 64-127 of one K (and V) ring slot, so
+// S = Q [K_a; K_b]^T is a single full-rate M128 x N128 tcgen05 MMA chain (an N=64 MMA reading both
+// operands from shared memory runs at 2/3 rate: operand bandwidth) and O += P [V_a; V_b] is one K=128
+// chain.  The mask granularity stays T = 64 (R10): pairing is an execution detail — each half is
+// masked with its own tile's token-exact causal frontier, and a lone last tile runs as an N=64 step.
+//
+// P is written by the softmax threads straight into TMEM over the S columns it came from (packed
+// bf16 pairs, row = lane) and consumed by the PV MMA as its A operand ("TS" form), so shared memory
+// holds only Q and the K/V rings.  The two Q tiles (GQA packing: 2 heads x 64 rows each) ping-pong:
+// while one softmax warpgroup works, the tensor core runs the other tile's PV and next S.
+//
+// Roles: warp 0 TMA Q + K, warp 3 TMA V, warp 1 MMA issue (converged, elect.sync), warp 2 TMEM
+// allocation, warps 4.. one softmax warpgroup per Q tile (thread = row = TMEM lane).
+#include <cuda_bf16.h>
+
+#include "attn_common.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bfla {
+
+namespace {
+using namespace attn;
+
+constexpr int D = 128;
+constexpr int BM = 128;   // MMA M (rows of a Q tile)
+constexpr int BN = 64;    // mask tile T
+constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
+
+template <int NQT>
+struct Cfg2 {
+  static constexpr int KS = 3, VS = NQT == 2 ? 2 : 3;
+  static constexpr int QBYTES = BM * D * 2;       // 32 KB
+  static constexpr int SLOT = RS * D * 2;         // 32 KB (two 64-row tiles)
+  static constexpr int HALF = BN * 128;           // bytes of one 64-row half of a 64-column chunk
+  static constexpr int CHUNK = RS * 128;          // bytes of one 64-column chunk of a slot
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + NQT * QBYTES;
+  static constexpr int OFF_V = OFF_K + KS * SLOT;
+  static constexpr int OFF_BAR = OFF_V + VS * SLOT;
+  static constexpr int NBAR = 2 + 2 * KS + 2 * VS + 4 * NQT;
+  static constexpr int SMEM_TOTAL = OFF_BAR + NBAR * 8 + 16;
+  static constexpr int THREADS = 128 + 128 * NQT;
+  static constexpr int COL_S = 0;    // S_q / P_q at columns [128 q, 128 q + 128)
+  static constexpr int COL_O = 256;  // O_q at [256 + 128 q, ...)
+  static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+};
+
+template <int NQT, bool PAGED, bool DENSE>
+__global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
+    k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+            const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
+            const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
+            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
+  using C = Cfg2<NQT>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + C::KS;
+  uint64_t* v_full = k_empty + C::KS;
+  uint64_t* v_empty = v_full + C::VS;
+  uint64_t* s_full = v_empty + C::VS;  // [NQT]: S_q(s) in TMEM (also: PV_q(s-1) done)
+  uint64_t* p_full = s_full + NQT;     // [NQT]: P_q(s) in TMEM (128 arrivals)
+  uint64_t* o_full = p_full + NQT;     // [NQT]: last PV of the item done
+  uint64_t* o_free = o_full + NQT;     // [NQT]: epilogue has read O (128 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < C::KS; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < C::VS; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int q = 0; q < NQT; ++q) {
+      mbar_init(s_full + q, 1);
+      mbar_init(p_full + q, 128);
+      mbar_init(o_full + q, 1);
+      mbar_init(o_free + q, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int heads_in_chunk = NQT * hpq;
+
+  auto row_count = [&](const Item& it) -> int {
+    if (DENSE) return (int)causal_row_count(g, it.i);
+    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+  };
+  auto row_list = [&](const Item& it) -> const int32_t* {
+    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
+  };
+  auto tile_at = [&](const int32_t* lst, int n) -> int { return DENSE ? n : __ldg(lst + n); };
+
+  // one 64-row tile j of item `it` into half `hf` of K (kvsel = 0) or V (kvsel = 1) slot `dst`
+  auto load_tile = [&](int kvsel, unsigned char* dst, uint64_t* full, int hf, int j, const Item& it) {
+    const CUtensorMap* map = kvsel ? &tmV : &tmK;
+    if (!PAGED) {
+      for (int cc = 0; cc < D / 64; ++cc)
+        tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF, map, full, cc * 64, j * BN, it.h, it.r);
+    } else {
+      // vLLM pages: BN/ps page boxes of (64 columns x ps rows); a page past the request's last
+      // logical page (ragged tail) is replaced by its first page (finite data; those keys are
+      // masked by causality and get P = 0).
+      const int ps = g.page_size;
+      const int npl = (g.Nkv + ps - 1) / ps;
+      const int32_t* table = page_table + (long long)it.r * g.max_pages;
+      for (int pc = 0; pc < BN / ps; ++pc) {
+        const int lp = j * BN / ps + pc;
+        const int phys = __ldg(table + (lp < npl ? lp : 0));
+        for (int cc = 0; cc < D / 64; ++cc)
+          tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
+      }
+    }
+  };
+  auto load_step = [&](int kvsel, uint32_t ks, const int32_t* lst, int cnt, int s, const Item& it) {
+    const int nst = kvsel ? C::VS : C::KS;
+    const int st = ks % nst;
+    uint64_t* full = (kvsel ? v_full : k_full) + st;
+    mbar_wait((kvsel ? v_empty : k_empty) + st, ((ks / nst) & 1) ^ 1);
+    const bool two = 2 * s + 1 < cnt;
+    mbar_arrive_expect_tx(full, (two ? 2 : 1) * BN * D * 2);
+    unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::SLOT;
+    load_tile(kvsel, dst, full, 0, tile_at(lst, 2 * s), it);
+    if (two) load_tile(kvsel, dst, full, 1, tile_at(lst, 2 * s + 1), it);
+  };
+
+  if (warp == 0) {
+    // ================================ TMA producer (Q, K) ================================
+    if (lane == 0) {
+      uint32_t ks = 0, nit = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item it = decode_item(g, idx, NC);
+        const int cnt = row_count(it);
+        if (cnt == 0) continue;
+        const int32_t* lst = DENSE ? nullptr : row_list(it);
+        const uint32_t my_it = nit++;
+        mbar_wait(q_empty, (my_it & 1) ^ 1);
+        int nq_boxes = 0;
+        for (int q = 0; q < NQT; ++q)
+          for (int s = 0; s < hpq; ++s)
+            if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
+        mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
+        for (int q = 0; q < NQT; ++q)
+          for (int s = 0; s < hpq; ++s) {
+            const int pl = it.c * heads_in_chunk + q * hpq + s;
+            if (pl >= g.m) continue;
+            const int p = it.h * g.m + pl;
+            for (int cc = 0; cc < D / 64; ++cc)
+              tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
+                          cc * 64, it.i * g.T, p, it.r);
+          }
+        if (idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read from HBM once)
+          const Item nx = decode_item(g, idx + gridDim.x, NC);
+          for (int q = 0; q < NQT; ++q)
+            for (int s = 0; s < hpq; ++s) {
+              const int pl = nx.c * heads_in_chunk + q * hpq + s;
+              if (pl >= g.m) continue;
+              for (int cc = 0; cc < D / 64; ++cc) tma_prefetch_4d(&tmQ, cc * 64, nx.i * g.T, nx.h * g.m + pl, nx.r);
+            }
+        }
+        const int ns = (cnt + 1) / 2;
+        for (int s = 0; s < ns; ++s, ++ks) load_step(0, ks, lst, cnt, s, it);
+      }
+    }
+  } else if (warp == 3) {
+    // ================================ TMA producer (V) ================================
+    if (lane == 0) {
+      uint32_t ks = 0;
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+        const Item it = decode_item(g, idx, NC);
+        const int cnt = row_count(it);
+        if (cnt == 0) continue;
+        const int32_t* lst = DENSE ? nullptr : row_list(it);
+        const int ns = (cnt + 1) / 2;
+        for (int s = 0; s < ns; ++s, ++ks) load_step(1, ks, lst, cnt, s, it);
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ================================
+    // Step s: [PV_q(s-1) (A = P_q in TMEM), S_q(s)] per Q tile.  S_q(s) overwrites the TMEM columns
+    // P_q(s-1) occupies, after the PV that reads them (tcgen05 MMAs of one thread execute in order).
+    const uint64_t dQ = sdesc_sw128(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t dK = sdesc_sw128(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV = sdesc_sw128(smem_u32(smem + C::OFF_V), C::CHUNK, 1024);
+    uint32_t ks0 = 0, nit = 0, st0 = 0;
+    auto issue_PV = [&](int q, uint32_t vslot, int ntile, bool acc_first) {
+      const uint32_t idO = idesc_bf16(BM, D, 0, 1);
+      const uint64_t b0 = dV + (uint64_t)((vslot * C::SLOT) >> 4);
+      const uint32_t aP = tmem + C::COL_S + q * 128;
+#pragma unroll 8
+      for (int kk = 0; kk < ntile * 4; ++kk)
+        umma_f16_ts_warp(tmem + C::COL_O + q * D, aP + kk * 8, b0 + (uint64_t)((kk * 2048) >> 4), idO,
+                         (acc_first || kk > 0) ? 1u : 0u);
+    };
+    auto issue_S = [&](int q, uint32_t kslot, int ntile) {
+      const uint32_t idS = ntile == 2 ? idesc_bf16(BM, 2 * BN, 0, 0) : idesc_bf16(BM, BN, 0, 0);
+      const uint64_t a0 = dQ + (uint64_t)((q * C::QBYTES) >> 4), b0 = dK + (uint64_t)((kslot * C::SLOT) >> 4);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t offa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
+        const uint32_t offb = ((kk >> 2) * C::CHUNK + (kk & 3) * 32) >> 4;
+        umma_f16_ss_warp(tmem + C::COL_S + q * 128, a0 + offa, b0 + offb, idS, kk > 0 ? 1u : 0u);
+      }
+      umma_commit_warp(s_full + q);
+    };
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const Item it = decode_item(g, idx, NC);
+      const int cnt = row_count(it);
+      if (cnt == 0) continue;
+      const uint32_t my_it = nit++;
+      const int ns = (cnt + 1) / 2;
+      mbar_wait(q_full, my_it & 1);
+      tc_fence_after();
+      for (int s = 0; s < ns; ++s) {
+        const uint32_t ksn = ks0 + s, kst = ksn % C::KS;
+        mbar_wait(k_full + kst, (ksn / C::KS) & 1);
+        uint32_t vst = 0;
+        if (s > 0) {
+          vst = (ksn - 1) % C::VS;
+          mbar_wait(v_full + vst, ((ksn - 1) / C::VS) & 1);
+        }
+        tc_fence_after();
+        const int nt = 2 * s + 1 < cnt ? 2 : 1;
+#pragma unroll
+        for (int q = 0; q < NQT; ++q) {
+          if (s > 0) {  // O_q += P_q(s-1) [V]
+            mbar_wait(p_full + q, (st0 + s - 1) & 1);
+            if (s == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
+            tc_fence_after();
+            issue_PV(q, vst, 2, s > 1);  // every step but the last holds two tiles
+          }
+          issue_S(q, kst, nt);
+        }
+        umma_commit_warp(k_empty + kst);
+        if (s > 0) umma_commit_warp(v_empty + vst);
+        if (s == ns - 1) umma_commit_warp(q_empty);  // every S MMA of the item has been issued
+      }
+      // tail: O_q += P_q(ns-1) [V]
+      const uint32_t ksl = ks0 + ns - 1, vst = ksl % C::VS;
+      mbar_wait(v_full + vst, (ksl / C::VS) & 1);
+      tc_fence_after();
+      const int ntl = cnt - 2 * (ns - 1);
+#pragma unroll
+      for (int q = 0; q < NQT; ++q) {
+        mbar_wait(p_full + q, (st0 + ns - 1) & 1);
+        if (ns == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
+        tc_fence_after();
+        issue_PV(q, vst, ntl, ns > 1);
+        umma_commit_warp(o_full + q);
+      }
+      umma_commit_warp(v_empty + vst);
+      ks0 += ns;
+      st0 += ns;
+    }
+  } else if (warp >= 4) {
+    // ================================ softmax / epilogue ================================
+    const int q = (warp - 4) >> 2;
+    const int lg = warp & 3;         // TMEM lane group of this warp
+    const int row = lg * 32 + lane;  // row of Q tile q = TMEM lane
+    const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + C::COL_S + q * 128;
+    const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
+    const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
+    uint32_t st = 0, nit = 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const Item it = decode_item(g, idx, NC);
+      const int cnt = row_count(it);
+      const int slot = row / g.T;
+      const int pl = it.c * heads_in_chunk + q * hpq + slot;
+      const int t = it.i * g.T + (row % g.T);
+      const bool valid = slot < hpq && pl < g.m && t < g.Nq;
+      const int p = it.h * g.m + pl;
+      __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2;
+      if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
+        if (valid) {
+          for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
+          if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+        }
+        continue;
+      }
+      const uint32_t my_it = nit++;
+      const int32_t* lst = DENSE ? nullptr : row_list(it);
+      const int ns = (cnt + 1) / 2;
+      float m_run = -INFINITY, l_run = 0.0f;
+      for (int s = 0; s < ns; ++s, ++st) {
+        const bool two = 2 * s + 1 < cnt;
+        const int ja = tile_at(lst, 2 * s), jb = two ? tile_at(lst, 2 * s + 1) : 0;
+        mbar_wait(s_full + q, st & 1);
+        tc_fence_after();
+        // pass 1: row max over the step's columns (TMEM read in two halves of 64 to bound registers)
+        // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
+        const int la = g.Nc + t - ja * BN, lb = two ? g.Nc + t - jb * BN : -1;
+        float mrow = -INFINITY;
+#pragma unroll 1
+        for (int hf = 0; hf < (two ? 2 : 1); ++hf) {
+          float v[64];
+          tmem_ld32(tS + hf * 64, v);
+          tmem_ld32(tS + hf * 64 + 32, v + 32);
+          tmem_wait_ld();
+          const int lim = hf ? lb : la;
+          if (lim < BN - 1) {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (c > lim) v[c] = -INFINITY;
+          }
+          float mc[4];
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            float a = max3f(v[16 * k4], v[16 * k4 + 1], v[16 * k4 + 2]);
+#pragma unroll
+            for (int c = 3; c < 15; c += 2) a = max3f(a, v[16 * k4 + c], v[16 * k4 + c + 1]);
+            mc[k4] = fmaxf(a, v[16 * k4 + 15]);
+          }
+          mrow = fmaxf(mrow, fmaxf(max3f(mc[0], mc[1], mc[2]), mc[3]));
+        }
+        const float mx = mrow * c2;
+        // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in P
+        // and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
+        const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
+        float alpha = 1.0f;
+        if (need) {
+          alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
+          l_run *= alpha;
+          m_run = mx;
+        }
+        if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+          // O is complete through PV(s-1): the s_full commit covers every earlier MMA
+#pragma unroll 1
+          for (int cc = 0; cc < D; cc += 32) {
+            float ov[32];
+            tmem_ld32(tO + cc, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+            tmem_st32(tO + cc, ov);
+          }
+        }
+        const float msub = m_run == -INFINITY ? 0.0f : m_run;
+        // p = 2^(s c2 - m) in pairs (FFMA2); 1 of every 4 pairs on the FMA pipe (rel. err 8e-5 << bf16
+        // rounding of P), the rest on MUFU.EX2.  P -> TMEM as packed bf16 over the S columns.
+        const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
+        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const int nchunk = two ? 4 : 2;
+        // pass 2: per 32-column chunk: reload, mask, p, row-sum, pack, store P over the S columns
+#pragma unroll 1
+        for (int ch = 0; ch < nchunk; ++ch) {
+          float v[32];
+          tmem_ld32(tS + ch * 32, v);
+          tmem_wait_ld();
+          const int lim = (ch < 2 ? la : lb) - (ch & 1) * 32;
+          if (lim < 31) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c > lim) v[c] = -INFINITY;
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
+            float2 pr;
+            if (e % 4 == 1) {
+              pr = exp2_poly2(x);
+            } else {
+              pr.x = ex2_approx(x.x);
+              pr.y = ex2_approx(x.y);
+            }
+            ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
+            pk[e] = pack_bf16x2(pr.x, pr.y);
+          }
+          tmem_st16(tS + ch * 16, pk);
+        }
+        l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_full + q);
+      }
+      // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
+      mbar_wait(o_full + q, my_it & 1);
+      tc_fence_after();
+      const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+#pragma unroll 1
+      for (int cc = 0; cc < D; cc += 32) {
+        float ov[32];
+        tmem_ld32(tO + cc, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + cc);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
+      }
+      if (valid && lse)
+        lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
+            l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+      tc_fence_before();
+      mbar_arrive(o_free + q);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int NQT, bool PAGED, bool DENSE>
+int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
+              void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st) {
+  using C = Cfg2<NQT>;
+  auto kern = k_attn2<NQT, PAGED, DENSE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = n_items < num_sms ? n_items : num_sms;
+  kern<<<grid, C::THREADS, C::SMEM_TOTAL, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
+                                                static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC);
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+// head_dim 128 only (two 32 KB K/V slots per ring stage do not fit next to Q at d = 256).
+int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st) {
+  const int hpq = BM / g.T;
+  const int nqt = g.m > hpq ? 2 : 1;
+  const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
+  const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
+  if (items == 0) return 0;
+  const int n = (int)items;
+#define BFLA_GO2(Q_, P_, X_) return launch2_t<Q_, P_, X_>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
+  if (nqt == 2) {
+    if (g.paged) { if (dense) BFLA_GO2(2, true, true); else BFLA_GO2(2, true, false); }
+    else { if (dense) BFLA_GO2(2, false, true); else BFLA_GO2(2, false, false); }
+  } else {
+    if (g.paged) { if (dense) BFLA_GO2(1, true, true); else BFLA_GO2(1, true, false); }
+    else { if (dense) BFLA_GO2(1, false, true); else BFLA_GO2(1, false, false); }
+  }
+#undef BFLA_GO2
+}
+
+}  // namespace bfla

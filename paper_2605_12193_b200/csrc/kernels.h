@@ -41,5 +41,8 @@ struct AttnMaps {
 size_t attn_smem_bytes(int D, int nqt);
 int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st);
+// head_dim 128: two kept tiles per step, P in TMEM (attention2.cu)
+int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st);
 
 }  // namespace bfla
