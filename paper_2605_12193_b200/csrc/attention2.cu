@@ -16,6 +16,8 @@
 // allocation, warps 4.. one softmax warpgroup per Q tile (thread = row = TMEM lane).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "attn_common.cuh"
 #include "common.cuh"
 #include "kernels.h"
@@ -49,7 +51,7 @@ struct Cfg2 {
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
-template <int NQT, bool PAGED, bool DENSE>
+template <int NQT, bool PAGED, bool DENSE, bool PINGPONG>
 __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
@@ -282,6 +284,21 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     const uint32_t tS = tmem + lane_addr + C::COL_S + q * 128;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
+    // ping-pong (NQT = 2): the two softmax warpgroups take turns (named barriers 1 + q), so each
+    // runs its exponentials at full issue rate while the tensor core works on the other Q tile.
+    const bool pingpong = PINGPONG && NQT == 2;
+    auto turn_wait = [&]() {
+      if (pingpong) asm volatile("bar.sync %0, 256;" ::"r"(1 + q) : "memory");
+    };
+    auto turn_pass = [&]() {
+      if (pingpong) asm volatile("bar.arrive %0, 256;" ::"r"(1 + (q ^ 1)) : "memory");
+    };
+    long long total_steps = 0;  // steps this warpgroup will run (both warpgroups run the same ones)
+    if (pingpong) {
+      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) total_steps += (row_count(decode_item(g, idx, NC)) + 1) / 2;
+      if (q == 1 && total_steps > 0) turn_pass();  // tile 0 goes first
+    }
+    long long done_steps = 0;
     uint32_t st = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
@@ -308,6 +325,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         const int ja = tile_at(lst, 2 * s), jb = two ? tile_at(lst, 2 * s + 1) : 0;
         mbar_wait(s_full + q, st & 1);
         tc_fence_after();
+        turn_wait();
         // pass 1: row max over the step's columns (TMEM read in two halves of 64 to bound registers)
         // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
         const int la = g.Nc + t - ja * BN, lb = two ? g.Nc + t - jb * BN : -1;
@@ -394,6 +412,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(p_full + q);
+        ++done_steps;
+        if (!(q == 1 && done_steps == total_steps)) turn_pass();  // tile 1's last step has no successor
       }
       // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
       mbar_wait(o_full + q, my_it & 1);
@@ -432,7 +452,11 @@ template <int NQT, bool PAGED, bool DENSE>
 int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
               void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st) {
   using C = Cfg2<NQT>;
-  auto kern = k_attn2<NQT, PAGED, DENSE>;
+  static const bool pp = [] {
+    const char* e = getenv("BFLA_PINGPONG");
+    return !(e && atoi(e) == 0);
+  }();
+  auto kern = pp ? k_attn2<NQT, PAGED, DENSE, true> : k_attn2<NQT, PAGED, DENSE, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;
