@@ -51,7 +51,7 @@ struct Cfg2 {
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
-template <int NQT, bool PAGED, bool DENSE, bool PINGPONG>
+template <int NQT, bool PAGED, bool DENSE, bool PINGPONG, int POLY>
 __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
           for (int e = 0; e < 16; ++e) {
             const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
             float2 pr;
-            if (e % 4 == 1) {
+            if (POLY > 0 && e % POLY == 1) {  // 1 of every POLY pairs on the FMA pipe
               pr = exp2_poly2(x);
             } else {
               pr.x = ex2_approx(x.x);
@@ -454,9 +454,10 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
   using C = Cfg2<NQT>;
   static const bool pp = [] {
     const char* e = getenv("BFLA_PINGPONG");
-    return !(e && atoi(e) == 0);
+    return e && atoi(e) == 1;  // off by default: one softmax warp per SMSP is latency bound
   }();
-  auto kern = pp ? k_attn2<NQT, PAGED, DENSE, true> : k_attn2<NQT, PAGED, DENSE, false>;
+  // 1 of every 4 exponential pairs on the FMA pipe: measured best of {0, 1/8, 1/4}
+  auto kern = pp ? k_attn2<NQT, PAGED, DENSE, true, 4> : k_attn2<NQT, PAGED, DENSE, false, 4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;
