@@ -279,7 +279,7 @@ def cpu_baseline(w, seconds_hint=20.0):
                              rho=w["rho"])
     t_mask = time.perf_counter() - t0
     N = w["N"]
-    stride = max(1, N // 512)
+    stride = max(1, N // 4096)
     rows = np.array([[p, t] for p in range(m) for t in range(0, N, stride)], np.int32)
     t0 = time.perf_counter()
     oracle.masked_attention(q, k, v, 1 / math.sqrt(w["d"]), r["labels"], 64, rows)
