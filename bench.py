@@ -211,6 +211,23 @@ def run_ours(args, w, rank, world, local_rank):
     de[1].record(st)
     torch.cuda.synchronize()
     dense_ms = de[0].elapsed_time(de[1]) / nd
+    # external sanity reference (not a target): torch SDPA (flash/cuDNN backend) on the same shapes
+    sdpa_ms = None
+    try:
+        import torch.nn.functional as F
+
+        if not w["paged"]:
+            for _ in range(2):
+                F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+            torch.cuda.synchronize()
+            de[0].record(st)
+            for _ in range(nd):
+                F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+            de[1].record(st)
+            torch.cuda.synchronize()
+            sdpa_ms = de[0].elapsed_time(de[1]) / nd
+    except Exception:
+        sdpa_ms = None
 
     # ---- e2e through the public API with host buffers (pinned H2D of Q/K/V, D2H of O) ----
     qh = q.cpu().pin_memory()
@@ -254,7 +271,7 @@ def run_ours(args, w, rank, world, local_rank):
     if os.path.exists(prof):
         tr = json.load(open(prof)).get(args.workload, {})
         traffic = tr.get("attention_bytes")
-    res = dict(ms_per_step=ms_per_step, s1=s1, s2=s2, at=at, dense_ms=dense_ms, kappa=kappa, stats=stats,
+    res = dict(ms_per_step=ms_per_step, s1=s1, s2=s2, at=at, dense_ms=dense_ms, sdpa_ms=sdpa_ms, kappa=kappa, stats=stats,
                launches=launches, clk=clk.summary(), e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, peaks=peaks,
                achieved_tf=achieved_tf, dense_tf=dense_tf, traffic=traffic, retained_flops=retained_flops)
     return res
@@ -355,6 +372,7 @@ def main():
                                      "groups_recomputed": r["stats"]["rows_recomputed"],
                                      "rows_exact_tie": r["stats"]["rows_exact_tie"]},
             "dense_ms": r["dense_ms"], "speedup_vs_dense": r["dense_ms"] / r["ms_per_step"],
+            "torch_sdpa_dense_ms": r["sdpa_ms"],
             "dense_roofline": {"bound": "tensor", "achieved": r["dense_tf"], "peak": peaks["bf16"],
                                "unit": "TFLOP/s", "frac": r["dense_tf"] / peaks["bf16"]},
             "roofline": {"bound": "tensor", "achieved": r["achieved_tf"], "peak": peaks["bf16"], "unit": "TFLOP/s",
