@@ -48,6 +48,26 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
+// Side stream + events for fork/join inside one call (created once per device, then read-only).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream* side_stream() {
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStream& ss = per_dev[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+  }
+  return &ss;
+}
+
 static int num_sms_current() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -251,7 +271,17 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       gk.kvs1 = (long long)g.Nkv * g.D;
       gk.kvs0 = (long long)g.Hkv * g.Nkv * g.D;
     }
-    launch_block_norms(gk, P->q, kc, qn, kn, st);
+    // norms (HBM-bound) run on a side stream concurrently with the tensor-core scores; joined before
+    // the certified selection that reads them
+    SideStream* ss = side_stream();
+    if (ss) {
+      cudaEventRecord(ss->fork, st);
+      cudaStreamWaitEvent(ss->s, ss->fork, 0);
+      launch_block_norms(gk, P->q, kc, qn, kn, ss->s);
+      cudaEventRecord(ss->join, ss->s);
+    } else {
+      launch_block_norms(gk, P->q, kc, qn, kn, st);
+    }
     CUtensorMap tmA, tmB;
     bfla_status s;
     {
@@ -268,6 +298,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     }
     if (launch_tc_scores(gk, tmA, tmB, S, st)) return fail(BFLA_ERR_CUDA, "tc scores launch failed");
     cudaMemsetAsync(nflag, 0, sizeof(int32_t), st);
+    if (ss) cudaStreamWaitEvent(st, ss->join, 0);
     const int sms = num_sms_current();
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
                   1, qn, kn, certify_tau(g), flagged, nflag, sms);

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
                                                            const int32_t* __restrict__ flagged,
                                                            const int32_t* __restrict__ n_flagged,
                                                            float* __restrict__ S) {
-  constexpr int KC = 128, JB = 16, NST = 4;
+  // k-chunk: 256 elements (two tokens at d = 128; rows are contiguous token runs on this path)
+  constexpr int KC = G <= 4 ? 256 : 128, JB = 16, NST = 4;
   constexpr int ROWS = G + JB * G, RB = KC * 2 + 16;  // row bytes padded by 16 (bank spread)
   constexpr int NDOT = JB * G * G, PER = (NDOT + 255) / 256;
   extern __shared__ __align__(16) unsigned char rsm[];
@@ -344,7 +345,8 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
   auto go = [&](auto kern, int G) {
-    const size_t smem = (size_t)4 * (G + 16 * G) * (128 * 2 + 16) + (size_t)16 * G * G * 4;
+    const int KC = G <= 4 ? 256 : 128;
+    const size_t smem = (size_t)4 * (G + 16 * G) * (KC * 2 + 16) + (size_t)16 * G * G * 4;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<2 * num_sms, 256, smem, st>>>(g, qq, kk, flagged, n_flagged, S);
   };
