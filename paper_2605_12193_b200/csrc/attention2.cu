@@ -326,13 +326,29 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         mbar_wait(s_full + q, st & 1);
         tc_fence_after();
         turn_wait();
-        // pass 1: row max over the step's columns (TMEM read in two halves of 64 to bound registers)
         // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
         const int la = g.Nc + t - ja * BN, lb = two ? g.Nc + t - jb * BN : -1;
-        float mrow = -INFINITY;
-#pragma unroll 1
-        for (int hf = 0; hf < (two ? 2 : 1); ++hf) {
-          float v[64];
+        // p = 2^(s c2 - m) in pairs (FFMA2); 1 of every 4 pairs on the FMA pipe (rel. err 8e-5 << bf16
+        // rounding of P), the rest on MUFU.EX2.  Results are packed bf16 pairs, stored after the step.
+        uint32_t pk[64];
+        float2 ls[4];
+        auto exps64 = [&](const float* v, int hf, float msub) {
+          const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
+            float2 pr;
+            if (POLY > 0 && e % POLY == 1) {
+              pr = exp2_poly2(x);
+            } else {
+              pr.x = ex2_approx(x.x);
+              pr.y = ex2_approx(x.y);
+            }
+            ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
+            pk[hf * 32 + e] = pack_bf16x2(pr.x, pr.y);
+          }
+        };
+        auto load64 = [&](float* v, int hf) {
           tmem_ld32(tS + hf * 64, v);
           tmem_ld32(tS + hf * 64 + 32, v + 32);
           tmem_wait_ld();
@@ -342,6 +358,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             for (int c = 0; c < BN; ++c)
               if (c > lim) v[c] = -INFINITY;
           }
+        };
+        auto max64 = [&](const float* v) {
           float mc[4];
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
@@ -350,17 +368,62 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             for (int c = 3; c < 15; c += 2) a = max3f(a, v[16 * k4 + c], v[16 * k4 + c + 1]);
             mc[k4] = fmaxf(a, v[16 * k4 + 15]);
           }
-          mrow = fmaxf(mrow, fmaxf(max3f(mc[0], mc[1], mc[2]), mc[3]));
-        }
-        const float mx = mrow * c2;
-        // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in P
-        // and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
-        const bool need = mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY);
+          return fmaxf(max3f(mc[0], mc[1], mc[2]), mc[3]);
+        };
+        // fast path (running max known): one TMEM pass against m_run, checking the max on the way;
+        // valid unless some row's max grew by more than 8 (then the lazy rule moves m_run)
+        bool done = false;
         float alpha = 1.0f;
-        if (need) {
-          alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
-          l_run *= alpha;
-          m_run = mx;
+        if (__all_sync(0xffffffffu, m_run != -INFINITY)) {
+          ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+          float mrow;
+          {
+            float v[64];
+            load64(v, 0);
+            mrow = max64(v);
+            exps64(v, 0, m_run);
+          }
+          if (two) {
+            float v[64];
+            load64(v, 1);
+            mrow = fmaxf(mrow, max64(v));
+            exps64(v, 1, m_run);
+          }
+          done = !__any_sync(0xffffffffu, mrow * c2 > m_run + 8.0f);
+        }
+        if (!done) {
+          // exact path: row max first (S is still intact in TMEM: no P has been stored yet)
+          float mrow;
+          {
+            float v[64];
+            load64(v, 0);
+            mrow = max64(v);
+          }
+          if (two) {
+            float v[64];
+            load64(v, 1);
+            mrow = fmaxf(mrow, max64(v));
+          }
+          const float mx = mrow * c2;
+          // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in P
+          // and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
+          if (mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY)) {
+            alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
+            l_run *= alpha;
+            m_run = mx;
+          }
+          const float msub = m_run == -INFINITY ? 0.0f : m_run;
+          ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+          {
+            float v[64];
+            load64(v, 0);
+            exps64(v, 0, msub);
+          }
+          if (two) {
+            float v[64];
+            load64(v, 1);
+            exps64(v, 1, msub);
+          }
         }
         if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
           // O is complete through PV(s-1): the s_full commit covers every earlier MMA
@@ -374,41 +437,14 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             tmem_st32(tO + cc, ov);
           }
         }
-        const float msub = m_run == -INFINITY ? 0.0f : m_run;
-        // p = 2^(s c2 - m) in pairs (FFMA2); 1 of every 4 pairs on the FMA pipe (rel. err 8e-5 << bf16
-        // rounding of P), the rest on MUFU.EX2.  P -> TMEM as packed bf16 over the S columns.
-        const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
-        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        const int nchunk = two ? 4 : 2;
-        // pass 2: per 32-column chunk: reload, mask, p, row-sum, pack, store P over the S columns
-#pragma unroll 1
-        for (int ch = 0; ch < nchunk; ++ch) {
-          float v[32];
-          tmem_ld32(tS + ch * 32, v);
-          tmem_wait_ld();
-          const int lim = (ch < 2 ? la : lb) - (ch & 1) * 32;
-          if (lim < 31) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (c > lim) v[c] = -INFINITY;
-          }
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
-            float2 pr;
-            if (POLY > 0 && e % POLY == 1) {  // 1 of every POLY pairs on the FMA pipe
-              pr = exp2_poly2(x);
-            } else {
-              pr.x = ex2_approx(x.x);
-              pr.y = ex2_approx(x.y);
-            }
-            ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
-            pk[e] = pack_bf16x2(pr.x, pr.y);
-          }
-          tmem_st16(tS + ch * 16, pk);
-        }
         l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+        // P -> TMEM over the S columns it came from (packed bf16 pairs)
+        tmem_st16(tS, pk);
+        tmem_st16(tS + 16, pk + 16);
+        if (two) {
+          tmem_st16(tS + 32, pk + 32);
+          tmem_st16(tS + 48, pk + 48);
+        }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(p_full + q);
