@@ -112,7 +112,11 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
   auto row_list = [&](const Item& it) -> const int32_t* {
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
   };
-  auto tile_at = [&](const int32_t* lst, int n) -> int { return DENSE ? n : __ldg(lst + n); };
+  // tiles are visited in DESCENDING j (diagonal / local band first): the largest scores usually sit
+  // near the diagonal, so the running max settles on the first step and the lazy-max fast path holds
+  auto tile_at_c = [&](const int32_t* lst, int cnt, int n) -> int {
+    return DENSE ? cnt - 1 - n : __ldg(lst + (cnt - 1 - n));
+  };
 
   // one 64-row tile j of item `it` into half `hf` of K (kvsel = 0) or V (kvsel = 1) slot `dst`
   auto load_tile = [&](int kvsel, unsigned char* dst, uint64_t* full, int hf, int j, const Item& it) {
@@ -143,8 +147,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     const bool two = 2 * s + 1 < cnt;
     mbar_arrive_expect_tx(full, (two ? 2 : 1) * BN * D * 2);
     unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::SLOT;
-    load_tile(kvsel, dst, full, 0, tile_at(lst, 2 * s), it);
-    if (two) load_tile(kvsel, dst, full, 1, tile_at(lst, 2 * s + 1), it);
+    load_tile(kvsel, dst, full, 0, tile_at_c(lst, cnt, 2 * s), it);
+    if (two) load_tile(kvsel, dst, full, 1, tile_at_c(lst, cnt, 2 * s + 1), it);
   };
 
   if (warp == 0) {
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       float m_run = -INFINITY, l_run = 0.0f;
       for (int s = 0; s < ns; ++s, ++st) {
         const bool two = 2 * s + 1 < cnt;
-        const int ja = tile_at(lst, 2 * s), jb = two ? tile_at(lst, 2 * s + 1) : 0;
+        const int ja = tile_at_c(lst, cnt, 2 * s), jb = two ? tile_at_c(lst, cnt, 2 * s + 1) : 0;
         mbar_wait(s_full + q, st & 1);
         tc_fence_after();
         turn_wait();
