@@ -31,6 +31,8 @@ constexpr int D = 128;
 constexpr int BM = 128;   // MMA M (rows of a Q tile)
 constexpr int BN = 64;    // mask tile T
 constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
+// lazy-rescale headroom (log2 units): p = 2^(x - m_run) <= 2^24; O <= 2^24 * N_kv * |V| << fp32 max
+constexpr float kLazy = 24.0f;
 
 template <int NQT>
 struct Cfg2 {
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             mrow = fmaxf(mrow, max64(v));
             exps64(v, 1, m_run);
           }
-          done = !__any_sync(0xffffffffu, mrow * c2 > m_run + 8.0f);
+          done = !__any_sync(0xffffffffu, mrow * c2 > m_run + kLazy);
         }
         if (!done) {
           // exact path: row max first (S is still intact in TMEM: no P has been stored yet)
@@ -409,9 +411,9 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             mrow = fmaxf(mrow, max64(v));
           }
           const float mx = mrow * c2;
-          // lazy rescale: raise the running max only when it grows by more than 8 (2^8 headroom in P
-          // and l); the decision is per row, the TMEM traffic below is warp-uniform (.sync.aligned)
-          if (mx > m_run + 8.0f || (m_run == -INFINITY && mx > -INFINITY)) {
+          // lazy rescale: raise the running max only when it grows by more than kLazy (P <= 2^kLazy:
+          // bf16 P, fp32 l and O stay far inside their range); TMEM traffic below is warp-uniform
+          if (mx > m_run + kLazy || (m_run == -INFINITY && mx > -INFINITY)) {
             alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
             l_run *= alpha;
             m_run = mx;
