@@ -182,7 +182,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
 
 // ---- workspace layout -------------------------------------------------------------------------
 struct WsLayout {
-  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, nflag, kgather, total;
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, flagthr, nflag, kgather, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Geom& g) {
@@ -209,6 +209,8 @@ static WsLayout ws_layout(const Geom& g) {
   L.kn = o;
   o += al((size_t)g.B * g.Hkv * g.Lkv * 4);
   L.flagged = o;
+  o += al((size_t)g.B * g.Hq * g.Lq * 4);
+  L.flagthr = o;
   o += al((size_t)g.B * g.Hq * g.Lq * 4);
   L.nflag = o;
   o += al(16);
@@ -260,6 +262,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     float* kn = reinterpret_cast<float*>(ws + L.kn);
     int32_t* flagged = reinterpret_cast<int32_t*>(ws + L.flagged);
     int32_t* nflag = reinterpret_cast<int32_t*>(ws + L.nflag);
+    float* fthr = reinterpret_cast<float*>(ws + L.flagthr);
     const void* kc = P->k;
     Geom gk = g;  // geometry of the K operand as the score kernels see it (gathered = contiguous)
     if (g.paged) {
@@ -301,8 +304,8 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);
     const int sms = num_sms_current();
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
-                  1, qn, kn, certify_tau(g), flagged, nflag, sms);
-    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, S, sms, st))
+                  1, qn, kn, certify_tau(g), flagged, nflag, sms, fthr);
+    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, fthr, S, sms, st))
       return fail(BFLA_ERR_CUDA, "recompute launch failed");
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
                   2, nullptr, nullptr, 0.f, flagged, nflag, sms);

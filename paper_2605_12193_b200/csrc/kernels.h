@@ -20,14 +20,15 @@ size_t select_smem_bytes(const Geom& g, int nwarps);
 void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
                    uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st, int mode = 0,
                    const float* qn = nullptr, const float* kn = nullptr, float tau = 0.f,
-                   int32_t* flagged = nullptr, int32_t* n_flagged = nullptr, int num_sms = 148);
+                   int32_t* flagged = nullptr, int32_t* n_flagged = nullptr, int num_sms = 148,
+                   float* flag_thr = nullptr);
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
 constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, cudaStream_t st);
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st);
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, float* S, int num_sms, cudaStream_t st);
+                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st);
 void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, void* kout, cudaStream_t st);
 // Stage 2 (Eq. 19-26)
 void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int n_local, int eta, double rho,

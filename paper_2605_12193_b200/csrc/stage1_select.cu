@@ -53,6 +53,7 @@ struct RowResult {
   int nsel;
   float P;
   bool tie, certified;
+  float M, dmax;  // fast row max and largest score-error bound (mode 1)
 };
 
 __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int nc, float c_alpha, int select,
@@ -111,7 +112,7 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     if (keep_all) continue;
     if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
   }
-  RowResult res{nsel, P, false, true};
+  RowResult res{nsel, P, false, true, M, 0.f};
   if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
@@ -146,6 +147,7 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
       }
     }
     res.certified = ok;
+    res.dmax = dmax;
   }
   return res;
 }
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
                                                    unsigned long long* __restrict__ stats, int mode,
                                                    const float* __restrict__ qn, const float* __restrict__ kn,
                                                    float tau, int32_t* __restrict__ flagged,
-                                                   int32_t* __restrict__ n_flagged) {
+                                                   int32_t* __restrict__ n_flagged, float* __restrict__ flag_thr) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -219,7 +221,13 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
         if (kept_mass && lane == 0) kept_mass[rowid] = res.P;
       } else {
         unc++;
-        if (lane == 0) flagged[atomicAdd(n_flagged, 1)] = (int32_t)rowid;
+        // blocks with S_f < thr have canonical logit < -127 (exp2_canon = 0 exactly): only the others
+        // need canonical scores (k_s1_recompute_rows skips the rest)
+        if (lane == 0) {
+          const int f = atomicAdd(n_flagged, 1);
+          flagged[f] = (int32_t)rowid;
+          flag_thr[f] = res.M - 2.0f * res.dmax - 127.0f / c_alpha;
+        }
       }
       __syncwarp();
     }
@@ -242,14 +250,15 @@ size_t select_smem_bytes(const Geom& g, int nwarps) {
 
 void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
                    uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st, int mode,
-                   const float* qn, const float* kn, float tau, int32_t* flagged, int32_t* n_flagged, int num_sms) {
+                   const float* qn, const float* kn, float tau, int32_t* flagged, int32_t* n_flagged, int num_sms,
+                   float* flag_thr) {
   const int nwarps = g.m < 4 ? g.m : 4;
   const size_t smem = select_smem_bytes(g, nwarps);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_s1_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int rows = g.B * g.Hkv * g.Lq;
   const int grid = mode == 2 ? num_sms : rows;
   k_s1_select<<<grid, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse, kept_mass, stats,
-                                               mode, qn, kn, tau, flagged, n_flagged);
+                                               mode, qn, kn, tau, flagged, n_flagged, flag_thr);
   count_launch();
 }
 

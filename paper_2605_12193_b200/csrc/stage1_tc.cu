@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
                                                            const __nv_bfloat16* __restrict__ k,
                                                            const int32_t* __restrict__ flagged,
                                                            const int32_t* __restrict__ n_flagged,
+                                                           const float* __restrict__ flag_thr,
                                                            float* __restrict__ S) {
   // k-chunk: 256 elements (two tokens at d = 128; rows are contiguous token runs on this path)
   constexpr int KC = G <= 4 ? 256 : 128, JB = 16, NST = 4;
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
   constexpr int NDOT = JB * G * G, PER = (NDOT + 255) / 256;
   extern __shared__ __align__(16) unsigned char rsm[];
   float* part = reinterpret_cast<float*>(rsm + NST * ROWS * RB);
+  __shared__ uint32_t live_bits;  // blocks of this chunk whose canonical logit can exceed -127
   const int nf = *n_flagged;
   const int chunks = (g.Lkv + JB - 1) / JB;
   const long long units = (long long)nf * chunks;
@@ -213,7 +215,18 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
     const int jmax = (int)(e_i / g.b);
     const int j0 = chunk * JB;
     if (j0 > jmax) continue;  // uniform over the CTA
-    __syncthreads();          // the previous unit's readers are done with the ring
+    __syncthreads();          // the previous unit's readers are done with the ring (and live_bits)
+    float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
+    if (threadIdx.x < 32) {
+      const float thr = flag_thr[unit / chunks];
+      const int j = j0 + threadIdx.x;
+      const bool live = threadIdx.x < JB && j <= jmax && srow[j] >= thr;
+      const uint32_t bal = __ballot_sync(0xffffffffu, live);
+      if (threadIdx.x == 0) live_bits = bal;
+    }
+    __syncthreads();
+    const uint32_t live = live_bits;
+    if (!live) continue;  // every block of the chunk has an exactly-zero canonical probability
     auto issue = [&](int kc) {
       unsigned char* buf = rsm + (kc % NST) * ROWS * RB;
       const int x0 = kc * KC, tk = x0 / g.D, c0 = x0 % g.D;
@@ -228,7 +241,7 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
         } else {
           const int bi = rr - G, jl = bi / G, v = bi % G;
           const int s = (j0 + jl) * g.b + v * g.g + tk;
-          ok = j0 + jl <= jmax && s < g.Nkv;
+          ok = ((live >> jl) & 1u) && s < g.Nkv;
           if (ok) src = k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2 + c0 + piece * 8;
         }
         cp_async16(buf + rr * RB + piece * 16, src, ok);  // zero-filled when !ok (padding)
@@ -251,7 +264,7 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
 #pragma unroll
       for (int e = 0; e < PER; ++e) {
         const int di = threadIdx.x + e * 256;
-        if (di < NDOT) {
+        if (di < NDOT && ((live >> (di / (G * G))) & 1u)) {
           const int jl = di / (G * G), u = (di / G) % G, v = di % G;
           const uint2* xa = reinterpret_cast<const uint2*>(buf + u * RB);
           const uint2* yb = reinterpret_cast<const uint2*>(buf + (G + jl * G + v) * RB);
@@ -278,14 +291,14 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
     __syncthreads();
     if (threadIdx.x < JB) {
       const int jl = threadIdx.x, j = j0 + jl;
-      if (j <= jmax) {
+      if ((live >> jl) & 1u) {
         float mx = -INFINITY;
         for (int u = 0; u < G; ++u) {
           if (i * g.b + u * g.g >= g.Nq) continue;  // padding-only query group (R3)
           for (int v = 0; v < G; ++v)
             if (j * g.b + v * g.g < g.Nkv) mx = fmaxf(mx, part[(jl * G + u) * G + v]);
         }
-        S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = mx;
+        srow[j] = mx;
       }
     }
   }
@@ -340,7 +353,7 @@ void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, 
 }
 
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, float* S, int num_sms, cudaStream_t st) {
+                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st) {
   (void)pt;
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
@@ -348,7 +361,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
     const int KC = G <= 4 ? 256 : 128;
     const size_t smem = (size_t)4 * (G + 16 * G) * (KC * 2 + 16) + (size_t)16 * G * G * 4;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<2 * num_sms, 256, smem, st>>>(g, qq, kk, flagged, n_flagged, S);
+    kern<<<2 * num_sms, 256, smem, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
   };
   switch (g.G) {
     case 1: go(k_s1_recompute_rows<1>, 1); break;
