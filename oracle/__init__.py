@@ -245,3 +245,57 @@ def tile_lists(labels: np.ndarray):
     """Kept KV tiles per (h, i), ascending j — the kernel's work lists (Eq. 26 -> Eq. 27)."""
     Hkv, Tq, _ = labels.shape
     return [[np.nonzero(labels[h, i])[0].astype(np.int32) for i in range(Tq)] for h in range(Hkv)]
+
+
+# ---------------------------------------------------------------- Appendix bound, Eq. 28-33 (analysis)
+def appendix_bound(q, k, v, labels, T: int, scale: float):
+    """The paper's appendix bound (Remark 1, Eq. boundv0), one query head at a time, fp64.
+
+    With Z_s the causal indicator, Z = Z_s masked by the tile mask (Remark 1), D_s / D the row sums of
+    exp(scale QK^T) (.) Z_s / Z, A = D_s^-1 exp(...) (.) Z_s, A_2 = D^-1 exp(...) (.) Z:
+        alpha = ||D^-1 D_s - I||_F ||Z||_F + ||Z - Z_s||_F,   ||O - O_s||_F <= alpha ||A||_F ||V||_F.
+    Returns a list of dicts (lhs, rhs, alpha) per query head.  Desk scale only (materialises N x N).
+    """
+    q, k, v = (np.asarray(t, np.float64) for t in (q, k, v))
+    Hq, Nq, C = q.shape
+    Hkv, Nkv, _ = k.shape
+    m, n_c = Hq // Hkv, Nkv - Nq
+    t = np.arange(Nq)[:, None]
+    s = np.arange(Nkv)[None, :]
+    Zs = (s <= n_c + t).astype(np.float64)
+    out = []
+    for p in range(Hq):
+        h = p // m
+        E = np.exp(scale * (q[p] @ k[h].T) - (scale * (q[p] @ k[h].T)).max(1, keepdims=True))
+        Z = Zs * (np.asarray(labels)[h][t // T, s // T] > 0)
+        Ds, Dm = (E * Zs).sum(1), (E * Z).sum(1)
+        A = (E * Zs) / Ds[:, None]
+        A2 = (E * Z) / Dm[:, None]
+        O, Os = A2 @ v[h], A @ v[h]
+        alpha = np.linalg.norm(Ds / Dm - 1.0) * np.linalg.norm(Z) + np.linalg.norm(Z - Zs)
+        out.append(dict(lhs=float(np.linalg.norm(O - Os)), rhs=float(alpha * np.linalg.norm(A) * np.linalg.norm(v[h])),
+                        alpha=float(alpha)))
+    return out
+
+
+def mac_counts(labels, n_q: int, n_kv: int, C: int, h_q: int, b: int, g: int, T: int) -> dict:
+    """Multiply-accumulate accounting of Eq. 28-33 for one request (desk check of the cost model).
+
+    stage1: sum over causal block pairs of G^2 g C per query head (Eq. 30 counted exactly);
+    stage2_tiles: sum over kept tiles of 2 C * rows * cols per query head (QK^T + PV, Eq. 29 with
+    partial tiles counted by their in-range tokens); dense_tiles: the same over every causal tile;
+    kappa = kept / causal tiles (R20).
+    """
+    labels = np.asarray(labels)
+    Hkv, Tq, Tkv = labels.shape
+    m = h_q // Hkv
+    Lq, Lkv, G = cdiv(n_q, b), cdiv(n_kv, b), b // g
+    pairs = sum(1 for i in range(Lq) for j in range(Lkv) if causal(i, j, b, n_q, n_kv))
+    rows = np.array([min(T, n_q - i * T) for i in range(Tq)])
+    cols = np.array([min(T, n_kv - j * T) for j in range(Tkv)])
+    caus = np.array([[causal(i, j, T, n_q, n_kv) for j in range(Tkv)] for i in range(Tq)])
+    w = rows[:, None] * cols[None, :]
+    kept = sum(int(((labels[h] > 0) * w).sum()) for h in range(Hkv))
+    dense = int((caus * w).sum()) * Hkv
+    return dict(stage1=h_q * pairs * G * G * g * C, stage2=2 * C * m * kept, dense=2 * C * m * dense,
+                kappa=float((labels > 0).sum() / (caus.sum() * Hkv)), causal_pairs=pairs)
