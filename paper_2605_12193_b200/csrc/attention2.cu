@@ -120,42 +120,50 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     return DENSE ? cnt - 1 - n : __ldg(lst + (cnt - 1 - n));
   };
 
-  // one 64-row tile j of item `it` into half `hf` of K (kvsel = 0) or V (kvsel = 1) slot `dst`
-  auto load_tile = [&](int kvsel, unsigned char* dst, uint64_t* full, int hf, int j, const Item& it) {
+  // One ring step of K (kvsel = 0) or V (kvsel = 1), issued by a whole warp: lanes fetch the list
+  // entries and page-table entries concurrently (no chain of dependent global loads on one thread)
+  // and each lane issues its own TMA boxes.  Tile a fills rows 0-63 of the slot, tile b rows 64-127.
+  auto load_step = [&](int kvsel, uint32_t ks, const int32_t* lst, int cnt, int s, const Item& it) {
+    const int ns_ = kvsel ? C::VS : C::KS;
+    const int st = ks % ns_;
+    uint64_t* full = (kvsel ? v_full : k_full) + st;
+    mbar_wait((kvsel ? v_empty : k_empty) + st, ((ks / ns_) & 1) ^ 1);
+    const bool two = 2 * s + 1 < cnt;
+    // lane 0 / 1: list entries of tiles a / b (descending j, see tile_at_c)
+    int jl = 0;
+    if (lane < (two ? 2 : 1)) jl = tile_at_c(lst, cnt, 2 * s + lane);
+    const int ja = __shfl_sync(0xffffffffu, jl, 0), jb = __shfl_sync(0xffffffffu, jl, 1);
+    if (lane == 0) mbar_arrive_expect_tx(full, (two ? 2 : 1) * BN * D * 2);
+    __syncwarp();
+    unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::SLOT;
     const CUtensorMap* map = kvsel ? &tmV : &tmK;
     if (!PAGED) {
-      for (int cc = 0; cc < D / 64; ++cc)
-        tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF, map, full, cc * 64, j * BN, it.h, it.r);
+      // lane = (tile, d-chunk)
+      const int ntile = two ? 2 : 1;
+      if (lane < ntile * (D / 64)) {
+        const int hf = lane / (D / 64), cc = lane % (D / 64);
+        tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF, map, full, cc * 64, (hf ? jb : ja) * BN, it.h, it.r);
+      }
     } else {
-      // vLLM pages: BN/ps page boxes of (64 columns x ps rows); a page past the request's last
-      // logical page (ragged tail) is replaced by its first page (finite data; those keys are
-      // masked by causality and get P = 0).
-      const int ps = g.page_size;
-      const int npl = (g.Nkv + ps - 1) / ps;
-      const int32_t* table = page_table + (long long)it.r * g.max_pages;
-      for (int pc = 0; pc < BN / ps; ++pc) {
-        const int lp = j * BN / ps + pc;
-        const int phys = __ldg(table + (lp < npl ? lp : 0));
+      // lane = (tile, page of the tile): BN / page_size page boxes of (64 columns x ps rows) per
+      // d-chunk; a page past the request's last logical page (ragged tail) is replaced by its first
+      // page (finite data; those keys are masked by causality and get P = 0)
+      const int ps = g.page_size, ppt = BN / ps;
+      const int ntile = two ? 2 : 1;
+      if (lane < ntile * ppt) {
+        const int hf = lane / ppt, pc = lane % ppt;
+        const int npl = (g.Nkv + ps - 1) / ps;
+        const int lp = (hf ? jb : ja) * ppt + pc;
+        const int phys = __ldg(page_table + (long long)it.r * g.max_pages + (lp < npl ? lp : 0));
         for (int cc = 0; cc < D / 64; ++cc)
           tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
       }
     }
   };
-  auto load_step = [&](int kvsel, uint32_t ks, const int32_t* lst, int cnt, int s, const Item& it) {
-    const int nst = kvsel ? C::VS : C::KS;
-    const int st = ks % nst;
-    uint64_t* full = (kvsel ? v_full : k_full) + st;
-    mbar_wait((kvsel ? v_empty : k_empty) + st, ((ks / nst) & 1) ^ 1);
-    const bool two = 2 * s + 1 < cnt;
-    mbar_arrive_expect_tx(full, (two ? 2 : 1) * BN * D * 2);
-    unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::SLOT;
-    load_tile(kvsel, dst, full, 0, tile_at_c(lst, cnt, 2 * s), it);
-    if (two) load_tile(kvsel, dst, full, 1, tile_at_c(lst, cnt, 2 * s + 1), it);
-  };
 
   if (warp == 0) {
     // ================================ TMA producer (Q, K) ================================
-    if (lane == 0) {
+    {
       uint32_t ks = 0, nit = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
         const Item it = decode_item(g, idx, NC);
@@ -164,21 +172,22 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const uint32_t my_it = nit++;
         mbar_wait(q_empty, (my_it & 1) ^ 1);
-        int nq_boxes = 0;
-        for (int q = 0; q < NQT; ++q)
-          for (int s = 0; s < hpq; ++s)
-            if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
-        mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
-        for (int q = 0; q < NQT; ++q)
-          for (int s = 0; s < hpq; ++s) {
-            const int pl = it.c * heads_in_chunk + q * hpq + s;
-            if (pl >= g.m) continue;
-            const int p = it.h * g.m + pl;
-            for (int cc = 0; cc < D / 64; ++cc)
-              tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
-                          cc * 64, it.i * g.T, p, it.r);
-          }
-        if (idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read from HBM once)
+        if (lane == 0) {
+          int nq_boxes = 0;
+          for (int q = 0; q < NQT; ++q)
+            for (int s = 0; s < hpq; ++s)
+              if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
+          mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
+        }
+        __syncwarp();
+        {  // lane = (Q tile, head slot, d-chunk)
+          const int q = lane / (hpq * (D / 64)), s = (lane / (D / 64)) % hpq, cc = lane % (D / 64);
+          const int pl = it.c * heads_in_chunk + q * hpq + s;
+          if (q < NQT && pl < g.m)
+            tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
+                        cc * 64, it.i * g.T, it.h * g.m + pl, it.r);
+        }
+        if (lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read once)
           const Item nx = decode_item(g, idx + gridDim.x, NC);
           for (int q = 0; q < NQT; ++q)
             for (int s = 0; s < hpq; ++s) {
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     }
   } else if (warp == 3) {
     // ================================ TMA producer (V) ================================
-    if (lane == 0) {
+    {
       uint32_t ks = 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
         const Item it = decode_item(g, idx, NC);
