@@ -20,6 +20,9 @@ CASES = {
     # bench.py default: Llama-3.1-8B layer, 32K, strong operating point
     "llama8b-32k": dict(Hq=32, Hkv=8, d=128, N=32768, b=256, g=64, gamma=0.99, eta=16, rho=0.0, paged=0,
                         theta=5e5, seed=303),
+    # Llama-3.1-8B layer at 128K (BASELINE.json configs[2], single-GPU slice of the sharded run)
+    "llama8b-128k": dict(Hq=32, Hkv=8, d=128, N=131072, b=256, g=64, gamma=0.99, eta=16, rho=0.0, paged=0,
+                         theta=5e5, seed=303),
     # Qwen3-32B-like, 64K, vLLM pages of 16, all rescues (BASELINE.json configs[3])
     "qwen32b-64k-paged": dict(Hq=64, Hkv=8, d=128, N=65536, b=256, g=64, gamma=0.99, eta=16, rho=0.1, paged=16,
                               theta=1e6, seed=404),
@@ -61,7 +64,7 @@ def test_fullsize(name):
     kappa = st["kept_tiles"] / st["causal_tiles"]
     # O / LSE on sampled query tiles (all heads)
     Tq = N // 64
-    stride = 64
+    stride = 64 if N <= 65536 else 256
     tiles = sorted(set(list(range(0, Tq, stride)) + [Tq - 1]))
     rows = np.array([[p, i * 64 + r] for p in range(Hq) for i in tiles for r in range(64)], np.int32)
     O_ref, lse_ref = oracle.masked_attention(qf, kf, vf, 1 / math.sqrt(d), ref["labels"], 64, rows)
