@@ -84,6 +84,14 @@ typedef struct {
     int32_t page_size, num_pages, max_pages_per_seq;
     const int32_t* page_table; /* paged only: device int32 [batch][max_pages_per_seq], logical page
                                   n of request r lives at physical page page_table[r][n]           */
+    const int32_t* seqlens;    /* optional device int32 [batch][2] = (n_q_r, n_kv_r): variable-length
+                                  batch (requests of different lengths / chunk offsets).  Must satisfy
+                                  1 <= n_q_r <= n_kv_r, n_q_r <= n_q, n_kv_r <= n_kv (not checked: device
+                                  memory).  n_q / n_kv are then the padded extents of every buffer;
+                                  request r's queries are rows 0..n_q_r-1 of its Q/O slice, its keys
+                                  rows 0..n_kv_r-1 (or its first n_kv_r paged tokens); other O/LSE rows
+                                  are not written.  Stage-1 scores use the canonical path.  NULL =
+                                  every request has (n_q, n_kv).                                    */
 } bfla_problem;
 
 /* Method knobs.  Defaults of the paper's strong operating point:
@@ -136,7 +144,8 @@ typedef struct {
 
 /* Bytes of device scratch the entry points need for (problem, config). */
 size_t bfla_workspace_size(const bfla_problem* problem, const bfla_config* config);
-/* Entries tile_list must hold: batch * h_kv * (causal tiles per (r,h)). */
+/* Entries tile_list must hold: batch * h_kv * (causal tiles per (r,h)); with seqlens, batch * h_kv *
+   ceil(n_q/T) * ceil(n_kv/T). */
 int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* config);
 
 /* Stage 1 (Eq. 4-18 + GQA OR): pooling, block scores (Eq. 9-10), causal mask (Eq. 11-14),

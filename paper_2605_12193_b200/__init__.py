@@ -65,10 +65,12 @@ def _ptr(t: Optional[torch.Tensor]):
 
 def make_problem(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
                  lse: Optional[torch.Tensor] = None, *, softmax_scale: float = 0.0, head_offset: int = 0,
-                 page_table: Optional[torch.Tensor] = None, n_kv: Optional[int] = None) -> Problem:
+                 page_table: Optional[torch.Tensor] = None, n_kv: Optional[int] = None,
+                 seqlens: Optional[torch.Tensor] = None) -> Problem:
     """q, o: [B, Hq, Nq, d] bf16 (strided views allowed, d contiguous).
     Contiguous K/V: k, v [B, Hkv, Nkv, d].  Paged (vLLM): k, v [num_pages, page_size, Hkv, d] and
-    page_table int32 [B, max_pages]; n_kv must then be given."""
+    page_table int32 [B, max_pages]; n_kv must then be given.  seqlens (optional, int32 [B, 2] on the
+    device): per-request (n_q_r, n_kv_r) of a variable-length batch padded to the tensor extents."""
     B, Hq, Nq, d = q.shape
     for t in (q, k, v, o):
         if t.dtype != torch.bfloat16 or not t.is_cuda or t.stride(-1) != 1:
@@ -103,6 +105,12 @@ def make_problem(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Ten
         pt = page_table.to(torch.int32).contiguous()
         p.page_table = _ptr(pt)
         keep.append(pt)
+    if seqlens is not None:
+        sl = seqlens.to(device=q.device, dtype=torch.int32).contiguous()
+        if sl.shape != (B, 2):
+            raise ValueError("seqlens must be [batch, 2] = (n_q_r, n_kv_r)")
+        p.seqlens = _ptr(sl)
+        keep.append(sl)
     return Problem(p, tuple(keep))
 
 

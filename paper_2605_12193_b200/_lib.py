@@ -29,7 +29,8 @@ class bfla_problem(ctypes.Structure):
                 ("n_q", i32), ("n_kv", i32), ("softmax_scale", f32), ("head_offset", i32),
                 ("q", vp), ("q_stride", i64 * 3), ("o", vp), ("o_stride", i64 * 3), ("lse", vp),
                 ("kv_layout", i32), ("k", vp), ("v", vp), ("kv_stride", i64 * 3),
-                ("page_size", i32), ("num_pages", i32), ("max_pages_per_seq", i32), ("page_table", vp)]
+                ("page_size", i32), ("num_pages", i32), ("max_pages_per_seq", i32), ("page_table", vp),
+                ("seqlens", vp)]
 
 
 class bfla_config(ctypes.Structure):

@@ -176,7 +176,10 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
   g->Tq = (int)cdiv(g->Nq, T);
   g->Tkv = (int)cdiv(g->Nkv, T);
   g->Tw = (int)cdiv(g->Tkv, 32);
-  g->causal_per_head = causal_row_offset(*g, g->Tq);
+  g->lens = P->seqlens;
+  // list capacity per (r, h): the closed-form causal count (uniform batch) or the full tile rectangle
+  // (varlen: every request's causal set fits inside it)
+  g->causal_per_head = g->lens ? (long long)g->Tq * g->Tkv : causal_row_offset(*g, g->Tq);
   return BFLA_OK;
 }
 
@@ -240,6 +243,7 @@ static float certify_tau(const Geom& g) {
 
 static bool tc_eligible(const Geom& g, const bfla_problem* P, const bfla_config* cfg, const bfla_mask* mask) {
   if (cfg->pool != BFLA_POOL_FLATTEN || cfg->scores_path != BFLA_SCORES_AUTO || mask->kept_mass) return false;
+  if (g.lens) return false;  // varlen: a request's partial group would read padding (canonical path zero-fills)
   if (g.Nq % g.g || g.Nkv % g.g) return false;       // a TMA group row must not straddle the tail
   if (g.qs2 != g.D) return false;                    // group rows = contiguous token runs
   if (!g.paged && g.kvs2 != g.D) return false;

@@ -117,11 +117,13 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
   const int heads_in_chunk = NQT * hpq;
 
   auto row_count = [&](const Item& it) -> int {
-    if (DENSE) return (int)causal_row_count(g, it.i);
+    const Req R = req_of(g, it.r);
+    if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
+    if (DENSE) return (int)req_row_count(R, g.T, it.i);
     return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
-    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
+    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
   };
 
   // one K (kvsel = 0) or V (kvsel = 1) tile j of item `it` into ring slot kv % stages
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       // request's last logical page (ragged tail) is replaced by its first page (finite data; those
       // keys are masked by causality and get P = 0).
       const int ps = g.page_size;
-      const int npl = (g.Nkv + ps - 1) / ps;
+      const int npl = (req_of(g, it.r).Nkv + ps - 1) / ps;
       const int32_t* table = page_table + (long long)it.r * g.max_pages;
       for (int pc = 0; pc < BN / ps; ++pc) {
         const int lp = j * BN / ps + pc;
@@ -316,7 +318,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
-      const bool valid = slot < hpq && pl < g.m && t < g.Nq;
+      const Req Rq = req_of(g, it.r);  // this request's logical dims (varlen)
+      const bool valid = slot < hpq && pl < g.m && t < Rq.Nq;
       const int p = it.h * g.m + pl;
       __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2 + half * DH;
       if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         for (int c0 = 0; c0 < NCOL; c0 += 32) tmem_ld32(tS0 + (tc & 1) * BN + c0, s + c0);
         tmem_wait_ld();
         // token-exact causality inside the tile (Eq. 27): key j*64 + NCOL half + c visible iff <= N_c + t
-        const int lim = g.Nc + t - j * BN - half * NCOL;
+        const int lim = Rq.Nc + t - j * BN - half * NCOL;
         if (lim < NCOL - 1) {
 #pragma unroll
           for (int c = 0; c < NCOL; ++c)

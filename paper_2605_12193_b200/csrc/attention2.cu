@@ -108,11 +108,13 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
   const int heads_in_chunk = NQT * hpq;
 
   auto row_count = [&](const Item& it) -> int {
-    if (DENSE) return (int)causal_row_count(g, it.i);
+    const Req R = req_of(g, it.r);
+    if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
+    if (DENSE) return (int)req_row_count(R, g.T, it.i);
     return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
-    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + causal_row_offset(g, it.i);
+    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
   };
   // tiles are visited in DESCENDING j (diagonal / local band first): the largest scores usually sit
   // near the diagonal, so the running max settles on the first step and the lazy-max fast path holds
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       const int ntile = two ? 2 : 1;
       if (lane < ntile * ppt) {
         const int hf = lane / ppt, pc = lane % ppt;
-        const int npl = (g.Nkv + ps - 1) / ps;
+        const int npl = (req_of(g, it.r).Nkv + ps - 1) / ps;
         const int lp = (hf ? jb : ja) * ppt + pc;
         const int phys = __ldg(page_table + (long long)it.r * g.max_pages + (lp < npl ? lp : 0));
         for (int cc = 0; cc < D / 64; ++cc)
@@ -321,7 +323,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
-      const bool valid = slot < hpq && pl < g.m && t < g.Nq;
+      const Req Rq = req_of(g, it.r);  // this request's logical dims (varlen)
+      const bool valid = slot < hpq && pl < g.m && t < Rq.Nq;
       const int p = it.h * g.m + pl;
       __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2;
       if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         tc_fence_after();
         turn_wait();
         // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
-        const int la = g.Nc + t - ja * BN, lb = two ? g.Nc + t - jb * BN : -1;
+        const int la = Rq.Nc + t - ja * BN, lb = two ? Rq.Nc + t - jb * BN : -1;
         // p = 2^(s c2 - m) in pairs (FFMA2); 1 of every 4 pairs on the FMA pipe (rel. err 8e-5 << bf16
         // rounding of P), the rest on MUFU.EX2.  Results are packed bf16 pairs, stored after the step.
         uint32_t pk[64];

@@ -23,7 +23,43 @@ struct Geom {
   long long qs0, qs1, qs2, os0, os1, os2, kvs0, kvs1, kvs2;
   int paged, page_size, num_pages, max_pages;
   float scale;                 // softmax scale (Eq. 27)
+  // varlen batches (§8 f1): optional device int32 [B][2] = (n_q_r, n_kv_r), each <= (Nq, Nkv).  The
+  // fields above are then the padded LAYOUT of every buffer; Req below holds request r's logical dims.
+  const int32_t* lens;
 };
+
+// Logical dimensions of request r (Eq. 4, 11, 19 with that request's N_q, N_kv).
+struct Req {
+  int Nq, Nkv, Nc, Lq, Lkv, Tq, Tkv;
+};
+__host__ __device__ inline Req make_req(int Nq, int Nkv, int b, int T) {
+  Req q;
+  q.Nq = Nq;
+  q.Nkv = Nkv;
+  q.Nc = Nkv - Nq;
+  q.Lq = (Nq + b - 1) / b;
+  q.Lkv = (Nkv + b - 1) / b;
+  q.Tq = (Nq + T - 1) / T;
+  q.Tkv = (Nkv + T - 1) / T;
+  return q;
+}
+__device__ inline Req req_of(const Geom& g, int r) {
+  if (!g.lens) return make_req(g.Nq, g.Nkv, g.b, g.T);
+  return make_req(__ldg(g.lens + 2 * r), __ldg(g.lens + 2 * r + 1), g.b, g.T);
+}
+// causal tiles of row i and their prefix for one request (Eq. 11-13 at block size T)
+__host__ __device__ inline long long req_row_count(const Req& q, int T, int i) {
+  long long a = (q.Nc + T - 1) / T + 1;
+  long long n = i + a;
+  return n < q.Tkv ? n : q.Tkv;
+}
+__host__ __device__ inline long long req_row_offset(const Req& q, int T, int i) {
+  long long a = (q.Nc + T - 1) / T + 1;
+  long long i0 = q.Tkv - a;
+  if (i0 < 0) i0 = 0;
+  if (i <= i0) return (long long)i * a + (long long)i * (i - 1) / 2;
+  return i0 * a + i0 * (i0 - 1) / 2 + (long long)(i - i0) * q.Tkv;
+}
 
 // Closed form of the causal-tile prefix (Eq. 11-13 at block size T): row i has
 // n(i) = min(Tkv, i + a) causal tiles with a = ceil(Nc/T) + 1; offset(i) = sum_{i'<i} n(i').

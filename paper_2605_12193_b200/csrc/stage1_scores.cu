@@ -54,11 +54,12 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
   const int i0 = blockIdx.y * BI, j0 = blockIdx.x * BJ;
   const int rp = blockIdx.z;
   const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
+  const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
   // causal skip (Eq. 11-13): the tile's smallest j against the largest i's frontier
   {
-    long long e_last = (long long)g.Nc + (long long)(i0 + BI) * g.b - 1;
-    if (e_last > g.Nkv - 1) e_last = g.Nkv - 1;
-    if ((long long)j0 * g.b > e_last) return;
+    long long e_last = (long long)R.Nc + (long long)(i0 + BI) * g.b - 1;
+    if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
+    if ((long long)j0 * g.b > e_last || i0 >= R.Lq) return;
   }
   const int gC = g.g * g.D;
   const int nit = gC / KC;
@@ -80,11 +81,11 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
         const int u = row >> 4, loc = row & 15;
         const int ib = i0 + loc, jb = j0 + loc;
         const int tq = ib * g.b + u * g.g + tk;
-        if (ib < g.Lq && tq < g.Nq)
+        if (ib < R.Lq && tq < R.Nq)
           ra[e] = __ldg(reinterpret_cast<const uint4*>(q + (long long)r * g.qs0 + (long long)p * g.qs1 +
                                                        (long long)tq * g.qs2 + c0 + piece * 8));
         const int sk = jb * g.b + u * g.g + tk;
-        if (jb < g.Lkv && sk < g.Nkv)
+        if (jb < R.Lkv && sk < R.Nkv)
           rb[e] = __ldg(reinterpret_cast<const uint4*>(k_token(g, k, pt, r, h, sk) + c0 + piece * 8));
       }
     }
@@ -142,17 +143,17 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
     __syncthreads();
   }
   const int i = i0 + ti, j = j0 + tj;
-  if (i >= g.Lq || j >= g.Lkv) return;
-  long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-  if (e_i > g.Nkv - 1) e_i = g.Nkv - 1;
+  if (i >= R.Lq || j >= R.Lkv) return;
+  long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+  if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
   if ((long long)j * g.b > e_i) return;  // non-causal: never read (Eq. 14 is applied by the selector)
   float best = -INFINITY;
 #pragma unroll
   for (int u = 0; u < G; ++u) {
-    if (i * g.b + u * g.g >= g.Nq) continue;  // padding-only query group (R3)
+    if (i * g.b + u * g.g >= R.Nq) continue;  // padding-only query group (R3)
 #pragma unroll
     for (int v = 0; v < G; ++v) {
-      if (j * g.b + v * g.g >= g.Nkv) continue;  // padding-only key group
+      if (j * g.b + v * g.g >= R.Nkv) continue;  // padding-only key group
       best = fmaxf(best, acc[u][v]);
     }
   }
@@ -173,9 +174,12 @@ __global__ void __launch_bounds__(256) k_s1_mean_pool(Geom g, const __nv_bfloat1
   if (unit >= nq_units + nk_units) return;
   const bool isq = unit < nq_units;
   const long long u = isq ? unit : unit - nq_units;
-  const int L = isq ? g.Lq : g.Lkv, H = isq ? g.Hq : g.Hkv, N = isq ? g.Nq : g.Nkv;
+  const int L = isq ? g.Lq : g.Lkv, H = isq ? g.Hq : g.Hkv;
   const int blk = (int)(u % L), hh = (int)((u / L) % H), r = (int)(u / ((long long)L * H));
+  const Req R = req_of(g, r);
+  const int N = isq ? R.Nq : R.Nkv;
   const int t0 = blk * g.b, t1 = min(N, (blk + 1) * g.b);
+  if (t0 >= t1) return;  // padding block of a shorter request (never read)
   float acc[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
@@ -208,8 +212,10 @@ __global__ void __launch_bounds__(256) k_s1_mean_scores(Geom g, const float* __r
   const int i = (int)(row % g.Lq);
   const int p = (int)((row / g.Lq) % g.Hq);
   const int r = (int)(row / ((long long)g.Lq * g.Hq));
-  long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-  if (e_i > g.Nkv - 1) e_i = g.Nkv - 1;
+  const Req R = req_of(g, r);
+  if (i >= R.Lq) return;
+  long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+  if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
   if ((long long)j * g.b > e_i) return;
   const float* a = qbar + row * g.D;
   const float* bb = kbar + (((long long)r * g.Hkv + p / g.m) * g.Lkv + j) * g.D;

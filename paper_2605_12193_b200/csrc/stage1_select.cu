@@ -187,8 +187,9 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
     for (int f = blockIdx.x * nwarps + warp; f < nf; f += gridDim.x * nwarps) {
       const int row = flagged[f];
       const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq), h = p / g.m;
-      const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-      const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;
+      const Req R = req_of(g, r);
+      const long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+      const int nc = (int)((e_i < R.Nkv - 1 ? e_i : (long long)R.Nkv - 1) / g.b) + 1;
       const float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
       const RowResult res = select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, false, 0.f, nullptr, 0.f);
       or_kept(keys, nc, coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw);
@@ -203,9 +204,10 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
     const int r = blockIdx.x / (g.Lq * g.Hkv);
     for (int w = threadIdx.x; w < g.Lw; w += blockDim.x) row_bits[w] = 0u;
     __syncthreads();
-    const long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-    const int nc = (int)((e_i < g.Nkv - 1 ? e_i : (long long)g.Nkv - 1) / g.b) + 1;  // causal blocks
-    for (int pl = warp; pl < g.m; pl += nwarps) {
+    const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
+    const long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+    const int nc = (int)((e_i < R.Nkv - 1 ? e_i : (long long)R.Nkv - 1) / g.b) + 1;  // causal blocks
+    for (int pl = warp; pl < (i < R.Lq ? g.m : 0); pl += nwarps) {  // padding rows stay empty
       const int p = h * g.m + pl;
       const long long rowid = ((long long)r * g.Hq + p) * g.Lq + i;
       const float* s = S + rowid * g.Lkv;

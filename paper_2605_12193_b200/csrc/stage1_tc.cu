@@ -38,8 +38,10 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
   const long long nq = (long long)g.B * g.Hq * g.Lq;
   const bool isq = u < nq;
   const long long w = isq ? u : u - nq;
-  const int L = isq ? g.Lq : g.Lkv, H = isq ? g.Hq : g.Hkv, N = isq ? g.Nq : g.Nkv;
+  const int L = isq ? g.Lq : g.Lkv, H = isq ? g.Hq : g.Hkv;
   const int blk = (int)(w % L), hh = (int)((w / L) % H), r = (int)(w / ((long long)L * H));
+  const Req R = req_of(g, r);
+  const int N = isq ? R.Nq : R.Nkv;
   const int vec_per_tok = g.D / 8;
   float best = 0.f;
   for (int grp = warp; grp < g.G; grp += 8) {
@@ -96,10 +98,11 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   const int rp = t / n_mt;  // r * Hq + p
   const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
   const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
+  const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
   {  // causal skip (Eq. 11-13): smallest j of the N tile vs the largest i of the M tile
-    long long e_last = (long long)g.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
-    if (e_last > g.Nkv - 1) e_last = g.Nkv - 1;
-    if ((long long)nt * BK * g.b > e_last) return;
+    long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
+    if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
+    if ((long long)nt * BK * g.b > e_last || mt * BQ >= R.Lq) return;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -145,9 +148,9 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     tc_fence_after();
     const int grow = mt * TM + row;           // global query group of head p
     const int ib = grow / g.G, u = grow % g.G;
-    const bool uvalid = (long long)grow * g.g < g.Nq;  // padding-only groups never take the max (R3)
-    long long e_i = (long long)g.Nc + (long long)(ib + 1) * g.b - 1;
-    if (e_i > g.Nkv - 1) e_i = g.Nkv - 1;
+    const bool uvalid = (long long)grow * g.g < R.Nq;  // padding-only groups never take the max (R3)
+    long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
+    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
     for (int c0 = 0; c0 < TN; c0 += 32) {
       float v[32];
@@ -157,11 +160,11 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
         const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
         float mx = -INFINITY;
         for (int vv = 0; vv < g.G; ++vv)
-          if ((long long)(gcol + vv) * g.g < g.Nkv) mx = fmaxf(mx, v[jb0 + vv]);
+          if ((long long)(gcol + vv) * g.g < R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);
         if (!uvalid) mx = -INFINITY;
         for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const int jb = gcol / g.G;
-        if (u == 0 && ib < g.Lq && jb < g.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
+        if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
       }
     }
   }
@@ -210,8 +213,9 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
     const int row = flagged[unit / chunks];  // (r * Hq + p) * Lq + i
     const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
     const int h = p / g.m;
-    long long e_i = (long long)g.Nc + (long long)(i + 1) * g.b - 1;
-    if (e_i > g.Nkv - 1) e_i = g.Nkv - 1;
+    const Req R = req_of(g, r);
+    long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     const int jmax = (int)(e_i / g.b);
     const int j0 = chunk * JB;
     if (j0 > jmax) continue;  // uniform over the CTA
@@ -236,12 +240,12 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
         bool ok = false;
         if (rr < G) {
           const int t = i * g.b + rr * g.g + tk;
-          ok = t < g.Nq;
+          ok = t < R.Nq;
           if (ok) src = q + (long long)r * g.qs0 + (long long)p * g.qs1 + (long long)t * g.qs2 + c0 + piece * 8;
         } else {
           const int bi = rr - G, jl = bi / G, v = bi % G;
           const int s = (j0 + jl) * g.b + v * g.g + tk;
-          ok = ((live >> jl) & 1u) && s < g.Nkv;
+          ok = ((live >> jl) & 1u) && s < R.Nkv;
           if (ok) src = k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2 + c0 + piece * 8;
         }
         cp_async16(buf + rr * RB + piece * 16, src, ok);  // zero-filled when !ok (padding)
@@ -294,9 +298,9 @@ __global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bf
       if ((live >> jl) & 1u) {
         float mx = -INFINITY;
         for (int u = 0; u < G; ++u) {
-          if (i * g.b + u * g.g >= g.Nq) continue;  // padding-only query group (R3)
+          if (i * g.b + u * g.g >= R.Nq) continue;  // padding-only query group (R3)
           for (int v = 0; v < G; ++v)
-            if (j * g.b + v * g.g < g.Nkv) mx = fmaxf(mx, part[(jl * G + u) * G + v]);
+            if (j * g.b + v * g.g < R.Nkv) mx = fmaxf(mx, part[(jl * G + u) * G + v]);
         }
         srow[j] = mx;
       }
@@ -318,6 +322,7 @@ __global__ void __launch_bounds__(256) k_paged_gather(Geom g, const uint4* __res
   rest /= g.Nkv;
   const int h = (int)(rest % g.Hkv);
   const int r = (int)(rest / g.Hkv);
+  if (g.lens && s >= __ldg(g.lens + 2 * r + 1)) return;  // past this request's KV (no page mapped)
   const long long page = pt[(long long)r * g.max_pages + s / g.page_size];
   out[idx] = __ldg(kc + ((page * g.page_size + s % g.page_size) * g.Hkv + h) * per_tok + c);
 }

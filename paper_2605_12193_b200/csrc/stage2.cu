@@ -34,15 +34,23 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
   const int i = (int)(row % g.Tq);
   const int h = (int)((row / g.Tq) % g.Hkv);
   const int r = (int)(row / ((long long)g.Tq * g.Hkv));
+  const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
+  if (i >= R.Tq) {             // padding row of a shorter request: empty
+    for (int w = lane; w < g.Tw; w += 32) tile_bits[row * g.Tw + w] = 0u;
+    if (label)
+      for (int j = lane; j < g.Tkv; j += 32) label[row * g.Tkv + j] = 0;
+    if (lane == 0) count[row] = 0;
+    return;
+  }
   // Eq. 11-13 at tile size T: causal iff jT <= min(N_c + (i+1)T - 1, N_kv - 1)
-  const long long fr = (long long)g.Nc + (long long)(i + 1) * g.T - 1;
-  const int jmax = (int)((fr < g.Nkv - 1 ? fr : (long long)g.Nkv - 1) / g.T);
+  const long long fr = (long long)R.Nc + (long long)(i + 1) * g.T - 1;
+  const int jmax = (int)((fr < R.Nkv - 1 ? fr : (long long)R.Nkv - 1) / g.T);
   // R11: band = [max(0, d_i - n_local), d_i], d_i = min(floor(fr / T), Tkv - 1)
   int d_i = (int)(fr / g.T);
-  if (d_i > g.Tkv - 1) d_i = g.Tkv - 1;
+  if (d_i > R.Tkv - 1) d_i = R.Tkv - 1;
   const int band_lo = d_i - n_local > 0 ? d_i - n_local : 0;
   const uint32_t* crow = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i / g.rb) * g.Lw;
-  int32_t* lrow = list + (long long)(r * g.Hkv + h) * g.causal_per_head + causal_row_offset(g, i);
+  int32_t* lrow = list + (long long)(r * g.Hkv + h) * g.causal_per_head + req_row_offset(R, g.T, i);
   const uint64_t hglob = (uint64_t)(g.head_offset + h);
   int nk = 0;
   unsigned cnt[6] = {0, 0, 0, 0, 0, 0};

@@ -217,3 +217,84 @@ def test_strided_views_and_batch():
     bf.bfla_prefill(P, cfg, None, bf.alloc_workspace(P, cfg))
     ref = run_gpu(prob, cfg)
     assert torch.equal(ot.contiguous(), ref["o"])
+
+
+def _varlen_case(seed, lens, Hq=4, Hkv=2, d=128):
+    """Padded varlen batch: request r uses q[r, :, :n_q_r], k/v[r, :, :n_kv_r]; the padding holds
+    large garbage that must not reach any result."""
+    B = len(lens)
+    Nq, Nkv = max(a for a, _ in lens), max(b for _, b in lens)
+    prob = workloads.gaussian(seed, B, Hq, Hkv, Nq, Nkv, d, sigma=0.8)
+    q, k, v = prob.q.clone(), prob.k.clone(), prob.v.clone()
+    for r, (nq, nkv) in enumerate(lens):
+        q[r, :, nq:] = 1e4
+        k[r, :, nkv:] = -1e4
+        v[r, :, nkv:] = 1e4
+    return workloads.Problem(q, k, v), torch.tensor(lens, dtype=torch.int32)
+
+
+@pytest.mark.parametrize("paged", [0, 16])
+def test_varlen_batch(paged):
+    lens = [(700, 1500), (300, 300), (129, 1000), (64, 64)]
+    prob, sl = _varlen_case(81, lens)
+    cfg = bf.Config(b=128, g=64, gamma=0.95, eta=4, rho=0.2, seed=3)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    B, Hq, Nq, d = q.shape
+    Nkv = k.shape[2]
+    o = torch.zeros_like(q)
+    l = torch.zeros(B, Hq, Nq, dtype=torch.float32, device="cuda")
+    if paged:
+        kc, vc, pt = workloads.paged(k, v, paged, seed=5, extra_pages=2)
+        P = bf.make_problem(q, kc, vc, o, l, page_table=pt, n_kv=Nkv, seqlens=sl)
+    else:
+        P = bf.make_problem(q, k, v, o, l, seqlens=sl)
+    ws = bf.alloc_workspace(P, cfg)
+    m = bf.alloc_mask(P, cfg, labels=True)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    torch.cuda.synchronize()
+    coarse, labels = m.coarse_dense().cpu().numpy(), m.tile_label.cpu().numpy()
+    counts, lists = m.tile_count.cpu().numpy(), m.tile_list.cpu().numpy()
+    Tq_max, Tkv_max = labels.shape[2], labels.shape[3]
+    for r, (nq, nkv) in enumerate(lens):
+        qf, kf, vf = (f32(t[r])[:, :n] for t, n in ((prob.q, nq), (prob.k, nkv), (prob.v, nkv)))
+        ref = oracle.mask_pipeline(qf, kf, b=128, g=64, T=64, gamma=0.95, eta=4, rho=0.2, seed=3)
+        Lq, Lkv = ref["coarse"].shape[1:]
+        assert np.array_equal(coarse[r, :, :Lq, :Lkv], ref["coarse"]), r
+        assert not coarse[r, :, Lq:].any() and not coarse[r, :, :, Lkv:].any()
+        Tq, Tkv = ref["labels"].shape[1:]
+        assert np.array_equal(labels[r, :, :Tq, :Tkv], ref["labels"]), r
+        assert not labels[r, :, Tq:].any() and not labels[r, :, :, Tkv:].any()
+        # lists: row (r, h, i) at (r*Hkv + h) * Tq_max*Tkv_max + causal prefix of request r
+        rc = np.array([sum(oracle.causal(i, j, 64, nq, nkv) for j in range(Tkv)) for i in range(Tq)])
+        offs = np.concatenate([[0], np.cumsum(rc)])
+        for h in range(2):
+            for i in range(Tq):
+                want = np.nonzero(ref["labels"][h, i])[0]
+                base = (r * 2 + h) * Tq_max * Tkv_max + offs[i]
+                assert counts[r, h, i] == len(want)
+                assert np.array_equal(lists[base:base + len(want)], want)
+            assert not counts[r, h, Tq:].any()
+        O_ref, lse_ref = oracle.masked_attention(qf, kf, vf, 128 ** -0.5, ref["labels"], 64)
+        compare_o(o[r, :, :nq], O_ref, f"varlen r={r}")
+        assert np.abs(l[r, :, :nq].cpu().numpy() - lse_ref).max() <= 1e-3
+        assert not o[r, :, nq:].float().abs().sum().item()  # padding rows untouched (zeros)
+
+
+def test_varlen_dense_and_single_call():
+    lens = [(500, 900), (256, 256), (77, 333)]
+    prob, sl = _varlen_case(82, lens, Hq=8, Hkv=2)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o = torch.zeros_like(q)
+    bf.bfla_prefill(bf.make_problem(q, k, v, o, seqlens=sl), None, None, None)  # dense causal
+    cfg = bf.Config(b=128, g=64, gamma=1.0)  # keep-all through the whole sparse path
+    o2 = torch.zeros_like(q)
+    P2 = bf.make_problem(q, k, v, o2, seqlens=sl)
+    bf.bfla_prefill(P2, cfg, None, bf.alloc_workspace(P2, cfg))
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2)
+    for r, (nq, nkv) in enumerate(lens):
+        qf, kf, vf = (f32(t[r])[:, :n] for t, n in ((prob.q, nq), (prob.k, nkv), (prob.v, nkv)))
+        O_ref, _ = oracle.masked_attention(qf, kf, vf, 128 ** -0.5)
+        compare_o(o[r, :, :nq], O_ref, f"varlen dense r={r}")
