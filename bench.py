@@ -277,36 +277,47 @@ def run_ours(args, w, rank, world, local_rank):
     return res
 
 
-def cpu_baseline(w, seconds_hint=20.0):
-    """Time the oracle (as it stands) on the host: the whole layer's Stage 1 + Stage 2 mask (all KV
-    heads, canonical fp32) plus fp64 masked attention on every 8th query row of every head;
-    the attention part is extrapolated to all rows."""
+def cpu_baseline(w, small: bool = False, prob=None):
+    """Time the oracle (as it stands) on the host.  Default sample: the whole layer's Stage 1 + Stage 2
+    mask (all KV heads, canonical fp32) plus fp64 masked attention on every 8th query row of every
+    head (attention extrapolated x8).  small=True (one --impl reference step): one KV head group's
+    mask and every 64th row of its heads, extrapolated to the layer."""
     import numpy as np
 
     import oracle
     import workloads
 
-    prob = workloads.structured(303, 1, w["Hq"], w["Hkv"], w["N"], w["N"], w["d"], block=w["b"], theta=w["theta"])
-    q = prob.q[0].float().numpy()
-    k = prob.k[0].float().numpy()
-    v = prob.v[0].float().numpy()
+    if prob is None:
+        prob = workloads.structured(303, 1, w["Hq"], w["Hkv"], w["N"], w["N"], w["d"], block=w["b"],
+                                    theta=w["theta"])
+    m = w["Hq"] // w["Hkv"]
+    if small:
+        q, k, v = (t[0, :n].float().numpy() for t, n in ((prob.q, m), (prob.k, 1), (prob.v, 1)))
+    else:
+        q = prob.q[0].float().numpy()
+        k = prob.k[0].float().numpy()
+        v = prob.v[0].float().numpy()
     oracle.build()
     t0 = time.perf_counter()
     r = oracle.mask_pipeline(q, k, b=w["b"], g=w["g"], T=64, gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"],
                              rho=w["rho"])
     t_mask = time.perf_counter() - t0
-    N, Hq = w["N"], w["Hq"]
-    stride = 8
+    N, Hq = w["N"], q.shape[0]
+    stride = 64 if small else 8
     rows = np.array([[p, t] for p in range(Hq) for t in range(0, N, stride)], np.int32)
     t0 = time.perf_counter()
     oracle.masked_attention(q, k, v, 1 / math.sqrt(w["d"]), r["labels"], 64, rows)
     t_attn = time.perf_counter() - t0
-    layer_ms = (t_mask + t_attn * stride) * 1e3
+    heads = w["Hkv"] if small else 1
+    layer_ms = (t_mask + t_attn * stride) * heads * 1e3
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    return dict(value=layer_ms, unit=UNIT, cores=cores, kind="oracle",
-                sample=f"whole-layer Stage1+Stage2 mask, all {w['Hkv']} KV heads ({t_mask:.2f}s) + fp64 masked "
-                       f"attention on every {stride}th query row of all {Hq} heads ({len(rows)} rows, {t_attn:.2f}s); "
-                       f"attention extrapolated x{stride}")
+    what = (f"1 of {w['Hkv']} KV head groups: Stage1+Stage2 mask ({t_mask:.2f}s) + fp64 masked attention on every "
+            f"{stride}th row of its {Hq} heads ({len(rows)} rows, {t_attn:.2f}s); extrapolated x{heads} groups, "
+            f"x{stride} rows") if small else (
+            f"whole-layer Stage1+Stage2 mask, all {w['Hkv']} KV heads ({t_mask:.2f}s) + fp64 masked attention on "
+            f"every {stride}th query row of all {Hq} heads ({len(rows)} rows, {t_attn:.2f}s); attention "
+            f"extrapolated x{stride}")
+    return dict(value=layer_ms, unit=UNIT, cores=cores, kind="oracle", sample=what)
 
 
 def main():
@@ -336,10 +347,16 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        import workloads
+
+        prob = workloads.structured(303, 1, w["Hq"], w["Hkv"], w["N"], w["N"], w["d"], block=w["b"],
+                                    theta=w["theta"])
+        for _ in range(args.warmup):
+            cpu_baseline(w, small=True, prob=prob)
         vals = []
         cb = None
         for _ in range(max(1, args.steps)):
-            cb = cpu_baseline(w)
+            cb = cpu_baseline(w, small=True, prob=prob)
             vals.append(cb["value"])
         v = statistics.median(vals)
         cb["value"] = v
