@@ -303,7 +303,7 @@ def cpu_baseline(w, small: bool = False, prob=None):
                              rho=w["rho"])
     t_mask = time.perf_counter() - t0
     N, Hq = w["N"], q.shape[0]
-    stride = 64 if small else 8
+    stride = 64 if small else 2
     rows = np.array([[p, t] for p in range(Hq) for t in range(0, N, stride)], np.int32)
     t0 = time.perf_counter()
     oracle.masked_attention(q, k, v, 1 / math.sqrt(w["d"]), r["labels"], 64, rows)

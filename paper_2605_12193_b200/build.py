@@ -64,5 +64,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_trace() -> str:
+    """libbfla_trace.so: the same library with the attention timeline instrumentation compiled in
+    (-DBFLA_TRACE; tools/attn_trace.py).  Never loaded by the product path or the tests."""
+    build()
+    out = os.path.join(HERE, "libbfla_trace.so")
+    obj = os.path.join(BUILD, "attention2_trace.o")
+    src = os.path.join(CSRC, "attention2.cu")
+    subprocess.check_call([nvcc(), *ARCH, *COMMON, "-DBFLA_TRACE", "-c", src, "-o", obj])
+    objs = [os.path.join(BUILD, u.replace(".cu", ".o")) for u in UNITS if u != "attention2.cu"]
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", out, *objs, obj])
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--trace" in sys.argv:
+        print(build_trace())
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

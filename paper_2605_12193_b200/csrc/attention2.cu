@@ -13,7 +13,11 @@
 // while one softmax warpgroup works, the tensor core runs the other tile's PV and next S.
 //
 // Roles: warp 0 TMA Q + K, warp 3 TMA V, warp 1 MMA issue (converged, elect.sync), warp 2 TMEM
-// allocation, warps 4.. one softmax warpgroup per Q tile (thread = row = TMEM lane).
+// allocation, warps 4.. one softmax warpgroup per Q tile (thread = row = TMEM lane).  setmaxnreg
+// moves registers from the first warpgroup (88) to the softmax warpgroups (208), which read the
+// whole 128-column S row of a step with one TMEM round trip, take the row max first, apply the lazy
+// rescale rule and only then compute the exponentials (MAXFIRST; BFLA_MAXFIRST=0 selects the older
+// single-pass-with-redo variant).  Timeline instrumentation: -DBFLA_TRACE (tools/attn_trace.py).
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -23,6 +27,27 @@
 #include "kernels.h"
 
 namespace bfla {
+
+#ifdef BFLA_TRACE
+// Timeline instrumentation (trace build only: libbfla_trace.so, tools/attn_trace.py).  CTAs below
+// kTraceCtas record (code, clock64) events per warp role into g_trace[cta][role][kTraceN].
+__device__ unsigned long long* g_trace = nullptr;
+constexpr int kTraceCtas = 4, kTraceRoles = 5, kTraceN = 8192;
+extern "C" int bfla_debug_set_trace(void* buf) {
+  return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
+}
+#define TRACE(role, code)                                                                              \
+  do {                                                                                                 \
+    if (g_trace && blockIdx.x < kTraceCtas && (threadIdx.x & 31) == 0 && tr_n[role] < kTraceN) {       \
+      g_trace[((size_t)blockIdx.x * kTraceRoles + (role)) * kTraceN + tr_n[role]++] =                  \
+          ((unsigned long long)(code) << 56) | ((unsigned long long)clock64() & 0xFFFFFFFFFFFFFFull);  \
+    }                                                                                                  \
+  } while (0)
+#else
+#define TRACE(role, code) \
+  do {                    \
+  } while (0)
+#endif
 
 namespace {
 using namespace attn;
@@ -53,12 +78,12 @@ struct Cfg2 {
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
-template <int NQT, bool PAGED, bool DENSE, bool PINGPONG, int POLY>
+template <int NQT, bool PAGED, bool DENSE, bool MAXFIRST, int POLY>
 __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
             const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
-            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
+            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC, int opts) {
   using C = Cfg2<NQT>;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
@@ -106,6 +131,12 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int heads_in_chunk = NQT * hpq;
+  // registers (NQT = 2, MAXFIRST): the producer / MMA warpgroup needs few, the softmax warpgroups
+  // hold a whole S row (128 fp32) plus its packed P: 128 x 56 + 256 x 224 = 384 x 168 (the launch
+  // allocation).  Each setmaxnreg dominates its role's code.
+#ifdef BFLA_TRACE
+  int tr_n[kTraceRoles] = {0, 0, 0, 0, 0};
+#endif
 
   auto row_count = [&](const Item& it) -> int {
     const Req R = req_of(g, it.r);
@@ -163,6 +194,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     }
   };
 
+  if (warp < 4) {
+    if (NQT == 2 && MAXFIRST) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   if (warp == 0) {
     // ================================ TMA producer (Q, K) ================================
     {
@@ -174,6 +207,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const uint32_t my_it = nit++;
         mbar_wait(q_empty, (my_it & 1) ^ 1);
+        TRACE(1, 14);
         if (lane == 0) {
           int nq_boxes = 0;
           for (int q = 0; q < NQT; ++q)
@@ -189,7 +223,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
                         cc * 64, it.i * g.T, it.h * g.m + pl, it.r);
         }
-        if (lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read once)
+        TRACE(1, 23);
+        if (!(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read once)
           const Item nx = decode_item(g, idx + gridDim.x, NC);
           for (int q = 0; q < NQT; ++q)
             for (int s = 0; s < hpq; ++s) {
@@ -198,8 +233,12 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
               for (int cc = 0; cc < D / 64; ++cc) tma_prefetch_4d(&tmQ, cc * 64, nx.i * g.T, nx.h * g.m + pl, nx.r);
             }
         }
+        TRACE(1, 22);
         const int ns = (cnt + 1) / 2;
-        for (int s = 0; s < ns; ++s, ++ks) load_step(0, ks, lst, cnt, s, it);
+        for (int s = 0; s < ns; ++s, ++ks) {
+          load_step(0, ks, lst, cnt, s, it);
+          TRACE(1, 6);
+        }
       }
     }
   } else if (warp == 3) {
@@ -212,7 +251,10 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const int ns = (cnt + 1) / 2;
-        for (int s = 0; s < ns; ++s, ++ks) load_step(1, ks, lst, cnt, s, it);
+        for (int s = 0; s < ns; ++s, ++ks) {
+          load_step(1, ks, lst, cnt, s, it);
+          TRACE(2, 7);
+        }
       }
     }
   } else if (warp == 1) {
@@ -249,15 +291,19 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
       const int ns = (cnt + 1) / 2;
+      TRACE(0, 24);
       mbar_wait(q_full, my_it & 1);
+      TRACE(0, 15);
       tc_fence_after();
       for (int s = 0; s < ns; ++s) {
         const uint32_t ksn = ks0 + s, kst = ksn % C::KS;
         mbar_wait(k_full + kst, (ksn / C::KS) & 1);
+        TRACE(0, 1);
         uint32_t vst = 0;
         if (s > 0) {
           vst = (ksn - 1) % C::VS;
           mbar_wait(v_full + vst, ((ksn - 1) / C::VS) & 1);
+          TRACE(0, 2);
         }
         tc_fence_after();
         const int nt = 2 * s + 1 < cnt ? 2 : 1;
@@ -265,11 +311,13 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         for (int q = 0; q < NQT; ++q) {
           if (s > 0) {  // O_q += P_q(s-1) [V]
             mbar_wait(p_full + q, (st0 + s - 1) & 1);
+            TRACE(0, 3 + 16 * q);
             if (s == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
             tc_fence_after();
             issue_PV(q, vst, 2, s > 1);  // every step but the last holds two tiles
           }
           issue_S(q, kst, nt);
+          TRACE(0, 4 + 16 * q);
         }
         umma_commit_warp(k_empty + kst);
         if (s > 0) umma_commit_warp(v_empty + vst);
@@ -283,6 +331,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < NQT; ++q) {
         mbar_wait(p_full + q, (st0 + ns - 1) & 1);
+        TRACE(0, 5 + 16 * q);
         if (ns == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
         tc_fence_after();
         issue_PV(q, vst, ntl, ns > 1);
@@ -292,7 +341,9 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       ks0 += ns;
       st0 += ns;
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    if (NQT == 2 && MAXFIRST) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     // ================================ softmax / epilogue ================================
     const int q = (warp - 4) >> 2;
     const int lg = warp & 3;         // TMEM lane group of this warp
@@ -301,21 +352,6 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     const uint32_t tS = tmem + lane_addr + C::COL_S + q * 128;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
-    // ping-pong (NQT = 2): the two softmax warpgroups take turns (named barriers 1 + q), so each
-    // runs its exponentials at full issue rate while the tensor core works on the other Q tile.
-    const bool pingpong = PINGPONG && NQT == 2;
-    auto turn_wait = [&]() {
-      if (pingpong) asm volatile("bar.sync %0, 256;" ::"r"(1 + q) : "memory");
-    };
-    auto turn_pass = [&]() {
-      if (pingpong) asm volatile("bar.arrive %0, 256;" ::"r"(1 + (q ^ 1)) : "memory");
-    };
-    long long total_steps = 0;  // steps this warpgroup will run (both warpgroups run the same ones)
-    if (pingpong) {
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) total_steps += (row_count(decode_item(g, idx, NC)) + 1) / 2;
-      if (q == 1 && total_steps > 0) turn_pass();  // tile 0 goes first
-    }
-    long long done_steps = 0;
     uint32_t st = 0, nit = 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
@@ -342,8 +378,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         const bool two = 2 * s + 1 < cnt;
         const int ja = tile_at_c(lst, cnt, 2 * s), jb = two ? tile_at_c(lst, cnt, 2 * s + 1) : 0;
         mbar_wait(s_full + q, st & 1);
+        if (lg == 0) TRACE(3 + q, 8);
         tc_fence_after();
-        turn_wait();
         // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
         const int la = Rq.Nc + t - ja * BN, lb = two ? Rq.Nc + t - jb * BN : -1;
         // p = 2^(s c2 - m) in pairs (FFMA2); 1 of every 4 pairs on the FMA pipe (rel. err 8e-5 << bf16
@@ -356,7 +392,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
           for (int e = 0; e < 32; ++e) {
             const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
             float2 pr;
-            if (POLY > 0 && e % POLY == 1) {
+            if ((POLY >> (e % 8)) & 1) {  // POLY: bit mask over e mod 8 of the pairs on the FMA pipe
               pr = exp2_poly2(x);
             } else {
               pr.x = ex2_approx(x.x);
@@ -388,43 +424,35 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
           }
           return fmaxf(max3f(mc[0], mc[1], mc[2]), mc[3]);
         };
-        // fast path (running max known): one TMEM pass against m_run, checking the max on the way;
-        // valid unless some row's max grew by more than 8 (then the lazy rule moves m_run)
-        bool done = false;
-        float alpha = 1.0f;
-        if (__all_sync(0xffffffffu, m_run != -INFINITY)) {
-          ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
-          float mrow;
-          {
-            float v[64];
-            load64(v, 0);
-            mrow = max64(v);
-            exps64(v, 0, m_run);
-          }
+        if (MAXFIRST) {
+          // whole S row in registers with ONE TMEM round trip (setmaxnreg gives the softmax
+          // warpgroups 224 registers); row max first, then the lazy rule, then exponentials.  P of
+          // the first tile goes to TMEM while the second tile's exponentials run.
+          float v[128];
+          tmem_ld32(tS, v);
+          tmem_ld32(tS + 32, v + 32);
           if (two) {
-            float v[64];
-            load64(v, 1);
-            mrow = fmaxf(mrow, max64(v));
-            exps64(v, 1, m_run);
+            tmem_ld32(tS + 64, v + 64);
+            tmem_ld32(tS + 96, v + 96);
           }
-          done = !__any_sync(0xffffffffu, mrow * c2 > m_run + kLazy);
-        }
-        if (!done) {
-          // exact path: row max first (S is still intact in TMEM: no P has been stored yet)
-          float mrow;
-          {
-            float v[64];
-            load64(v, 0);
-            mrow = max64(v);
+          tmem_wait_ld();
+          if (lg == 0) TRACE(3 + q, 16);
+          if (la < BN - 1) {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (c > la) v[c] = -INFINITY;
           }
-          if (two) {
-            float v[64];
-            load64(v, 1);
-            mrow = fmaxf(mrow, max64(v));
+          if (two && lb < BN - 1) {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (c > lb) v[BN + c] = -INFINITY;
           }
+          float mrow = max64(v);
+          if (two) mrow = fmaxf(mrow, max64(v + BN));
           const float mx = mrow * c2;
+          float alpha = 1.0f;
           // lazy rescale: raise the running max only when it grows by more than kLazy (P <= 2^kLazy:
-          // bf16 P, fp32 l and O stay far inside their range); TMEM traffic below is warp-uniform
+          // bf16 P, fp32 l and O stay far inside their range)
           if (mx > m_run + kLazy || (m_run == -INFINITY && mx > -INFINITY)) {
             alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
             l_run *= alpha;
@@ -432,45 +460,118 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
           }
           const float msub = m_run == -INFINITY ? 0.0f : m_run;
           ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
-          {
-            float v[64];
-            load64(v, 0);
-            exps64(v, 0, msub);
-          }
+          exps64(v, 0, msub);
+          tmem_st16(tS, pk);
+          tmem_st16(tS + 16, pk + 16);
+          if (lg == 0) TRACE(3 + q, 17);
           if (two) {
-            float v[64];
-            load64(v, 1);
-            exps64(v, 1, msub);
+            exps64(v + BN, 1, msub);
+            tmem_st16(tS + 32, pk + 32);
+            tmem_st16(tS + 48, pk + 48);
           }
-        }
-        if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-          // O is complete through PV(s-1): the s_full commit covers every earlier MMA
+          if (lg == 0) TRACE(3 + q, 9);
+          if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+            // O is complete through PV(s-1): the s_full commit covers every earlier MMA
 #pragma unroll 1
-          for (int cc = 0; cc < D; cc += 32) {
-            float ov[32];
-            tmem_ld32(tO + cc, ov);
-            tmem_wait_ld();
+            for (int cc = 0; cc < D; cc += 32) {
+              float ov[32];
+              tmem_ld32(tO + cc, ov);
+              tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
-            tmem_st32(tO + cc, ov);
+              for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+              tmem_st32(tO + cc, ov);
+            }
           }
-        }
-        l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
-        // P -> TMEM over the S columns it came from (packed bf16 pairs)
-        tmem_st16(tS, pk);
-        tmem_st16(tS + 16, pk + 16);
-        if (two) {
-          tmem_st16(tS + 32, pk + 32);
-          tmem_st16(tS + 48, pk + 48);
+          l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+        } else {
+          // fast path (running max known): one TMEM pass against m_run, checking the max on the way;
+          // valid unless some row's max grew by more than 8 (then the lazy rule moves m_run)
+          bool done = false;
+          float alpha = 1.0f;
+          if (__all_sync(0xffffffffu, m_run != -INFINITY)) {
+            ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+            float mrow;
+            {
+              float v[64];
+              load64(v, 0);
+              if (lg == 0) TRACE(3 + q, 16);
+              mrow = max64(v);
+              exps64(v, 0, m_run);
+              if (lg == 0) TRACE(3 + q, 17);
+            }
+            if (two) {
+              float v[64];
+              load64(v, 1);
+              if (lg == 0) TRACE(3 + q, 18);
+              mrow = fmaxf(mrow, max64(v));
+              exps64(v, 1, m_run);
+            }
+            done = !__any_sync(0xffffffffu, mrow * c2 > m_run + kLazy);
+            if (lg == 0) TRACE(3 + q, 9);
+          }
+          if (!done) {
+            // exact path: row max first (S is still intact in TMEM: no P has been stored yet)
+            float mrow;
+            {
+              float v[64];
+              load64(v, 0);
+              mrow = max64(v);
+            }
+            if (two) {
+              float v[64];
+              load64(v, 1);
+              mrow = fmaxf(mrow, max64(v));
+            }
+            const float mx = mrow * c2;
+            // lazy rescale: raise the running max only when it grows by more than kLazy (P <= 2^kLazy:
+            // bf16 P, fp32 l and O stay far inside their range); TMEM traffic below is warp-uniform
+            if (mx > m_run + kLazy || (m_run == -INFINITY && mx > -INFINITY)) {
+              alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
+              l_run *= alpha;
+              m_run = mx;
+            }
+            const float msub = m_run == -INFINITY ? 0.0f : m_run;
+            ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+            {
+              float v[64];
+              load64(v, 0);
+              exps64(v, 0, msub);
+            }
+            if (two) {
+              float v[64];
+              load64(v, 1);
+              exps64(v, 1, msub);
+            }
+          }
+          if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+            // O is complete through PV(s-1): the s_full commit covers every earlier MMA
+  #pragma unroll 1
+            for (int cc = 0; cc < D; cc += 32) {
+              float ov[32];
+              tmem_ld32(tO + cc, ov);
+              tmem_wait_ld();
+  #pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+              tmem_st32(tO + cc, ov);
+            }
+          }
+          l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+          // P -> TMEM over the S columns it came from (packed bf16 pairs)
+          tmem_st16(tS, pk);
+          tmem_st16(tS + 16, pk + 16);
+          if (two) {
+            tmem_st16(tS + 32, pk + 32);
+            tmem_st16(tS + 48, pk + 48);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(p_full + q);
-        ++done_steps;
-        if (!(q == 1 && done_steps == total_steps)) turn_pass();  // tile 1's last step has no successor
+        if (lg == 0) TRACE(3 + q, 10);
       }
       // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
       mbar_wait(o_full + q, my_it & 1);
+      if (lg == 0) TRACE(3 + q, 12);
       tc_fence_after();
       const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
 #pragma unroll 1
@@ -492,6 +593,7 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
       tc_fence_before();
       mbar_arrive(o_free + q);
+      if (lg == 0) TRACE(3 + q, 13);
     }
   }
   tc_fence_before();
@@ -506,17 +608,21 @@ template <int NQT, bool PAGED, bool DENSE>
 int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
               void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st) {
   using C = Cfg2<NQT>;
-  static const bool pp = [] {
-    const char* e = getenv("BFLA_PINGPONG");
-    return e && atoi(e) == 1;  // off by default: one softmax warp per SMSP is latency bound
+  static const bool mf = [] {
+    const char* e = getenv("BFLA_MAXFIRST");
+    return !(e && atoi(e) == 0);
   }();
-  // 1 of every 4 exponential pairs on the FMA pipe: measured best of {0, 1/8, 1/4}
-  auto kern = pp ? k_attn2<NQT, PAGED, DENSE, true, 4> : k_attn2<NQT, PAGED, DENSE, false, 4>;
+  // pairs e with e mod 8 in {1, 5} (1 in 4) on the FMA pipe: measured best of 0, 1/8, 1/4, 3/8, 1/2
+  auto kern = mf ? k_attn2<NQT, PAGED, DENSE, true, 0x22> : k_attn2<NQT, PAGED, DENSE, false, 0x22>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
+  static const int opts = [] {
+    const char* e = getenv("BFLA_ATTN_OPTS");  // experiment switches (bit 0: no Q prefetch)
+    return e ? atoi(e) : 0;
+  }();
   const int grid = n_items < num_sms ? n_items : num_sms;
   kern<<<grid, C::THREADS, C::SMEM_TOTAL, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
-                                                static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC);
+                                                static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts);
   count_launch();
   return (int)cudaGetLastError();
 }
