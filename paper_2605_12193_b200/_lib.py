@@ -14,6 +14,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbfla.so")
 if os.environ.get("BFLA_TRACE_LIB") == "1":  # timeline-instrumented build (tools/attn_trace.py only)
     LIB_PATH = os.path.join(_HERE, "libbfla_trace.so")
+if os.environ.get("BFLA_LIB_VARIANT"):  # A/B experiments: libbfla_<variant>.so built by tools/ab_build.py
+    LIB_PATH = os.path.join(_HERE, f"libbfla_{os.environ['BFLA_LIB_VARIANT']}.so")
 
 BFLA_OK = 0
 STATUS = {0: "BFLA_OK", 1: "BFLA_ERR_INVALID_ARGUMENT", 2: "BFLA_ERR_UNSUPPORTED", 3: "BFLA_ERR_MISALIGNED",

@@ -90,6 +90,18 @@ static bfla_status encode_4d(CUtensorMap* map, const void* base, const uint64_t 
   return BFLA_OK;
 }
 
+static bool encode_4d_quiet(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
+                            const uint32_t box[4]) {
+  EncodeTiledFn fn = get_encode();
+  if (!fn) return false;
+  cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t s[3] = {strides_b[0], strides_b[1], strides_b[2]};
+  cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), d, s, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---- validation -> geometry -----------------------------------------------------------------
 static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom* g) {
   if (!P) return fail(BFLA_ERR_INVALID_ARGUMENT, "problem is NULL");
@@ -341,6 +353,16 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     const uint64_t str[3] = {(uint64_t)g.qs2 * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
     const uint32_t box[4] = {64, (uint32_t)g.T, 1, 1};
     if ((s = encode_4d(&maps.q, P->q, dims, str, box)) != BFLA_OK) return s;
+    // O through TMA stores when its layout allows (16-byte aligned base and strides) and rows are not
+    // varlen padding (those must stay untouched); otherwise the kernel stores rows directly
+    const uint64_t ostr[3] = {(uint64_t)g.os2 * 2, (uint64_t)g.os1 * 2, (uint64_t)g.os0 * 2};
+    const bool oal = ((uintptr_t)P->o % 16 == 0) && ostr[0] % 16 == 0 && ostr[1] % 16 == 0 && ostr[2] % 16 == 0;
+    static const bool no_otma = [] {
+      const char* e = getenv("BFLA_OTMA");
+      return e && atoi(e) == 0;
+    }();
+    maps.o_ok = 0;
+    if (oal && !g.lens && !no_otma && encode_4d_quiet(&maps.o, P->o, dims, ostr, box)) maps.o_ok = 1;
   }
   if (!g.paged) {
     const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv, (uint64_t)g.B};

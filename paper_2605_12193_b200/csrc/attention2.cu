@@ -14,7 +14,7 @@
 //
 // Roles: warp 0 TMA Q + K, warp 3 TMA V, warp 1 MMA issue (converged, elect.sync), warp 2 TMEM
 // allocation, warps 4.. one softmax warpgroup per Q tile (thread = row = TMEM lane).  setmaxnreg
-// moves registers from the first warpgroup (88) to the softmax warpgroups (208), which read the
+// moves registers from the first warpgroup (96) to the softmax warpgroups (200), which read the
 // whole 128-column S row of a step with one TMEM round trip, take the row max first, apply the lazy
 // rescale rule and only then compute the exponentials (MAXFIRST; BFLA_MAXFIRST=0 selects the older
 // single-pass-with-redo variant).  Timeline instrumentation: -DBFLA_TRACE (tools/attn_trace.py).
@@ -32,7 +32,7 @@ namespace bfla {
 // Timeline instrumentation (trace build only: libbfla_trace.so, tools/attn_trace.py).  CTAs below
 // kTraceCtas record (code, clock64) events per warp role into g_trace[cta][role][kTraceN].
 __device__ unsigned long long* g_trace = nullptr;
-constexpr int kTraceCtas = 4, kTraceRoles = 5, kTraceN = 8192;
+constexpr int kTraceCtas = 4, kTraceRoles = 6, kTraceN = 8192;
 extern "C" int bfla_debug_set_trace(void* buf) {
   return (int)cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
 }
@@ -59,18 +59,25 @@ constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
 // lazy-rescale headroom (log2 units): p = 2^(x - m_run) <= 2^24; O <= 2^24 * N_kv * |V| << fp32 max
 constexpr float kLazy = 24.0f;
 
-template <int NQT>
+template <int NQT, bool PAGED = false>
 struct Cfg2 {
-  static constexpr int KS = 3, VS = NQT == 2 ? 2 : 3;
+  // Q ring of NQT + 1 tiles: the next item's first Q tile loads while this item still holds its
+  // tiles (the last ones double as O staging for the TMA-store epilogue; contiguous K/V only —
+  // tiles; paged K/V keep a 3-deep K ring instead: their page-granular loads need the lead)
+#ifndef BFLA_QRING
+#define BFLA_QRING 1
+#endif
+  static constexpr bool QR = BFLA_QRING && !PAGED;
+  static constexpr int QS = QR ? NQT + 1 : NQT, KS = QR ? 2 : 3, VS = NQT == 2 ? 2 : 3;
   static constexpr int QBYTES = BM * D * 2;       // 32 KB
   static constexpr int SLOT = RS * D * 2;         // 32 KB (two 64-row tiles)
   static constexpr int HALF = BN * 128;           // bytes of one 64-row half of a 64-column chunk
   static constexpr int CHUNK = RS * 128;          // bytes of one 64-column chunk of a slot
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + NQT * QBYTES;
+  static constexpr int OFF_K = OFF_Q + QS * QBYTES;
   static constexpr int OFF_V = OFF_K + KS * SLOT;
   static constexpr int OFF_BAR = OFF_V + VS * SLOT;
-  static constexpr int NBAR = 2 + 2 * KS + 2 * VS + 4 * NQT;
+  static constexpr int NBAR = 2 * QS + 2 * KS + 2 * VS + 4 * NQT;
   static constexpr int SMEM_TOTAL = OFF_BAR + NBAR * 8 + 16;
   static constexpr int THREADS = 128 + 128 * NQT;
   static constexpr int COL_S = 0;    // S_q / P_q at columns [128 q, 128 q + 128)
@@ -78,19 +85,23 @@ struct Cfg2 {
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
-template <int NQT, bool PAGED, bool DENSE, bool MAXFIRST, int POLY>
-__global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
+// SMX: softmax variant — 0 fused single pass with exact redo, 1 max-first whole row per thread
+// (MAXFIRST, default).  (Splitting a Q tile's 128 columns over two warpgroups with a row-max
+// exchange was measured 10% slower: the exponential phases of all softmax warps then coincide.)
+template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY>
+__global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
+            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, int otma, Geom g, const int32_t* __restrict__ list,
             const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
             __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC, int opts) {
-  using C = Cfg2<NQT>;
+  constexpr bool MAXFIRST = SMX >= 1;
+  using C = Cfg2<NQT, PAGED>;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
+  uint64_t* q_full = bars + 0;          // [QS]: Q ring slot loaded
+  uint64_t* q_empty = bars + C::QS;     // [QS]: Q ring slot free (last S done / staged O stored from it)
+  uint64_t* k_full = bars + 2 * C::QS;
   uint64_t* k_empty = k_full + C::KS;
   uint64_t* v_full = k_empty + C::KS;
   uint64_t* v_empty = v_full + C::VS;
@@ -102,8 +113,10 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int q = 0; q < C::QS; ++q) {
+      mbar_init(q_full + q, 1);
+      mbar_init(q_empty + q, 1);
+    }
     for (int s = 0; s < C::KS; ++s) {
       mbar_init(k_full + s, 1);
       mbar_init(k_empty + s, 1);
@@ -131,11 +144,14 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int heads_in_chunk = NQT * hpq;
+  // Q tile q of the CTA's my_it-th item lives in ring slot qslot; qpar = parity of that slot's fill
+  auto qslot = [&](uint32_t my_it, int q) -> int { return (int)((NQT * my_it + q) % C::QS); };
+  auto qpar = [&](uint32_t my_it, int q) -> uint32_t { return ((NQT * my_it + q) / C::QS) & 1; };
   // registers (NQT = 2, MAXFIRST): the producer / MMA warpgroup needs few, the softmax warpgroups
-  // hold a whole S row (128 fp32) plus its packed P: 128 x 56 + 256 x 224 = 384 x 168 (the launch
+  // hold a whole S row (128 fp32) plus its packed P: 128 x 96 + 256 x 200 <= 384 x 168 (the launch
   // allocation).  Each setmaxnreg dominates its role's code.
 #ifdef BFLA_TRACE
-  int tr_n[kTraceRoles] = {0, 0, 0, 0, 0};
+  int tr_n[kTraceRoles] = {0, 0, 0, 0, 0, 0};
 #endif
 
   auto row_count = [&](const Item& it) -> int {
@@ -143,6 +159,11 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
     if (DENSE) return (int)req_row_count(R, g.T, it.i);
     return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+  };
+  // the next item's kept-tile count, loaded one item ahead so its latency is off the item boundary
+  auto next_count = [&](int idx) -> int {
+    const int nidx = idx + (int)gridDim.x;
+    return nidx < n_items ? row_count(decode_item(g, nidx, NC)) : 0;
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
@@ -195,45 +216,22 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
   };
 
   if (warp < 4) {
-    if (NQT == 2 && MAXFIRST) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+#ifndef BFLA_REG_PROD
+#define BFLA_REG_PROD 96
+#define BFLA_REG_SMX 200
+#endif
+    if (NQT == 2 && SMX == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD) : "memory");
   if (warp == 0) {
-    // ================================ TMA producer (Q, K) ================================
+    // ================================ TMA producer (K) ================================
     {
-      uint32_t ks = 0, nit = 0;
+      uint32_t ks = 0;
+      int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
         const Item it = decode_item(g, idx, NC);
-        const int cnt = row_count(it);
+        const int cnt = cnt_nx;
+        cnt_nx = next_count(idx);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
-        const uint32_t my_it = nit++;
-        mbar_wait(q_empty, (my_it & 1) ^ 1);
-        TRACE(1, 14);
-        if (lane == 0) {
-          int nq_boxes = 0;
-          for (int q = 0; q < NQT; ++q)
-            for (int s = 0; s < hpq; ++s)
-              if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
-          mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
-        }
-        __syncwarp();
-        {  // lane = (Q tile, head slot, d-chunk)
-          const int q = lane / (hpq * (D / 64)), s = (lane / (D / 64)) % hpq, cc = lane % (D / 64);
-          const int pl = it.c * heads_in_chunk + q * hpq + s;
-          if (q < NQT && pl < g.m)
-            tma_load_4d(smem + C::OFF_Q + q * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full,
-                        cc * 64, it.i * g.T, it.h * g.m + pl, it.r);
-        }
-        TRACE(1, 23);
-        if (!(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q (read once)
-          const Item nx = decode_item(g, idx + gridDim.x, NC);
-          for (int q = 0; q < NQT; ++q)
-            for (int s = 0; s < hpq; ++s) {
-              const int pl = nx.c * heads_in_chunk + q * hpq + s;
-              if (pl >= g.m) continue;
-              for (int cc = 0; cc < D / 64; ++cc) tma_prefetch_4d(&tmQ, cc * 64, nx.i * g.T, nx.h * g.m + pl, nx.r);
-            }
-        }
-        TRACE(1, 22);
         const int ns = (cnt + 1) / 2;
         for (int s = 0; s < ns; ++s, ++ks) {
           load_step(0, ks, lst, cnt, s, it);
@@ -241,13 +239,57 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         }
       }
     }
+  } else if (warp == 2) {
+    // ================================ TMA producer (Q) ================================
+    // Q tile q of the next item is loaded as soon as its smem is free: after the last S_q MMA (STG
+    // epilogue) or after O_q, staged through the same smem, has been read by the TMA store.
+    uint32_t nit = 0;
+    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
+    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      const Item it = decode_item(g, idx, NC);
+      const int cnt = cnt_nx;
+      cnt_nx = next_count(idx);
+      if (cnt == 0) continue;
+      const uint32_t my_it = nit++;
+#pragma unroll
+      for (int q = 0; q < NQT; ++q) {
+        const int qsl = qslot(my_it, q);
+        mbar_wait(q_empty + qsl, qpar(my_it, q) ^ 1);
+        if (q == 0) TRACE(5, 14);
+        if (lane == 0) {
+          int nb = 0;
+          for (int s = 0; s < hpq; ++s)
+            if (it.c * heads_in_chunk + q * hpq + s < g.m) nb += D / 64;
+          mbar_arrive_expect_tx(q_full + qsl, nb * 64 * 64 * 2);
+        }
+        __syncwarp();
+        {  // lane = (head slot, d-chunk)
+          const int s = lane / (D / 64), cc = lane % (D / 64);
+          const int pl = it.c * heads_in_chunk + q * hpq + s;
+          if (s < hpq && pl < g.m)
+            tma_load_4d(smem + C::OFF_Q + qsl * C::QBYTES + cc * (BM * 128) + s * (g.T * 128), &tmQ, q_full + qsl,
+                        cc * 64, it.i * g.T, it.h * g.m + pl, it.r);
+        }
+      }
+      if (!(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q
+        const Item nx = decode_item(g, idx + gridDim.x, NC);
+        for (int q = 0; q < NQT; ++q)
+          for (int s = 0; s < hpq; ++s) {
+            const int pl = nx.c * heads_in_chunk + q * hpq + s;
+            if (pl >= g.m) continue;
+            for (int cc = 0; cc < D / 64; ++cc) tma_prefetch_4d(&tmQ, cc * 64, nx.i * g.T, nx.h * g.m + pl, nx.r);
+          }
+      }
+    }
   } else if (warp == 3) {
     // ================================ TMA producer (V) ================================
     {
       uint32_t ks = 0;
+      int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
       for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
         const Item it = decode_item(g, idx, NC);
-        const int cnt = row_count(it);
+        const int cnt = cnt_nx;
+        cnt_nx = next_count(idx);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const int ns = (cnt + 1) / 2;
@@ -274,9 +316,9 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         umma_f16_ts_warp(tmem + C::COL_O + q * D, aP + kk * 8, b0 + (uint64_t)((kk * 2048) >> 4), idO,
                          (acc_first || kk > 0) ? 1u : 0u);
     };
-    auto issue_S = [&](int q, uint32_t kslot, int ntile) {
+    auto issue_S = [&](int q, int qsl, uint32_t kslot, int ntile) {
       const uint32_t idS = ntile == 2 ? idesc_bf16(BM, 2 * BN, 0, 0) : idesc_bf16(BM, BN, 0, 0);
-      const uint64_t a0 = dQ + (uint64_t)((q * C::QBYTES) >> 4), b0 = dK + (uint64_t)((kslot * C::SLOT) >> 4);
+      const uint64_t a0 = dQ + (uint64_t)((qsl * C::QBYTES) >> 4), b0 = dK + (uint64_t)((kslot * C::SLOT) >> 4);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t offa = ((kk >> 2) * (BM * 128) + (kk & 3) * 32) >> 4;
@@ -285,16 +327,15 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       }
       umma_commit_warp(s_full + q);
     };
+    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = row_count(it);
+      const int cnt = cnt_nx;
+      cnt_nx = next_count(idx);
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
       const int ns = (cnt + 1) / 2;
       TRACE(0, 24);
-      mbar_wait(q_full, my_it & 1);
-      TRACE(0, 15);
-      tc_fence_after();
       for (int s = 0; s < ns; ++s) {
         const uint32_t ksn = ks0 + s, kst = ksn % C::KS;
         mbar_wait(k_full + kst, (ksn / C::KS) & 1);
@@ -316,12 +357,18 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
             tc_fence_after();
             issue_PV(q, vst, 2, s > 1);  // every step but the last holds two tiles
           }
-          issue_S(q, kst, nt);
+          const int qsl = qslot(my_it, q);
+          if (s == 0) {
+            mbar_wait(q_full + qsl, qpar(my_it, q));
+            if (q == 0) TRACE(0, 15);
+            tc_fence_after();
+          }
+          issue_S(q, qsl, kst, nt);
           TRACE(0, 4 + 16 * q);
+          if (s == ns - 1 && !otma) umma_commit_warp(q_empty + qsl);  // every S_q MMA of the item issued
         }
         umma_commit_warp(k_empty + kst);
         if (s > 0) umma_commit_warp(v_empty + vst);
-        if (s == ns - 1) umma_commit_warp(q_empty);  // every S MMA of the item has been issued
       }
       // tail: O_q += P_q(ns-1) [V]
       const uint32_t ksl = ks0 + ns - 1, vst = ksl % C::VS;
@@ -343,7 +390,8 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     }
   }
   } else {
-    if (NQT == 2 && MAXFIRST) asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    if (NQT == 2 && SMX == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BFLA_REG_SMX) : "memory");
+
     // ================================ softmax / epilogue ================================
     const int q = (warp - 4) >> 2;
     const int lg = warp & 3;         // TMEM lane group of this warp
@@ -353,9 +401,11 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     uint32_t st = 0, nit = 0;
+    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
     for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = row_count(it);
+      const int cnt = cnt_nx;
+      cnt_nx = next_count(idx);
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
@@ -569,20 +619,37 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
         mbar_arrive(p_full + q);
         if (lg == 0) TRACE(3 + q, 10);
       }
-      // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2
+      // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2.  With otma, O is
+      // staged (SW128) in this tile's Q smem — free once the last PV is done — and written by TMA
+      // stores: per-thread row stores (32 rows per warp instruction) clog the LSU/MIO path the
+      // producers and the MMA issuer share (measured 6% of the kernel).
       mbar_wait(o_full + q, my_it & 1);
       if (lg == 0) TRACE(3 + q, 12);
       tc_fence_after();
       const float inv_l = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+      const int qsl = qslot(my_it, q);
+      unsigned char* qs = smem + C::OFF_Q + qsl * C::QBYTES;
 #pragma unroll 1
       for (int cc = 0; cc < D; cc += 32) {
         float ov[32];
         tmem_ld32(tO + cc, ov);
         tmem_wait_ld();
-        if (valid) {
-          uint32_t w[16];
+        if (cc == D - 32) {  // O_q fully read from TMEM: the next item's PV may overwrite it
+          tc_fence_before();
+          mbar_arrive(o_free + q);
+        }
+        uint32_t w[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
+        for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
+        if (otma) {
+          // row `row` of the 128-row tile, 16-byte pieces k = (cc % 64) / 8 .. + 3 of d-chunk cc / 64
+          unsigned char* rb = qs + (cc / 64) * (BM * 128) + row * 128;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = ((cc % 64) >> 3) + e;
+            st_shared_v4(rb + ((k ^ (row & 7)) << 4), w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
+        } else if (valid && !(opts & 2)) {
           uint4* dst = reinterpret_cast<uint4*>(orow + cc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
@@ -591,10 +658,28 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
       if (valid && lse)
         lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
             l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
-      tc_fence_before();
-      mbar_arrive(o_free + q);
+      if (lg == 0) TRACE(3 + q, 25);
+      if (otma) {
+        fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+        if (lg == 0) TRACE(3 + q, 26);
+        if (warp == 4 + 4 * q && lane == 0) {
+          for (int s = 0; s < hpq; ++s) {
+            const int pls = it.c * heads_in_chunk + q * hpq + s;
+            if (pls >= g.m) continue;
+            for (int dc = 0; dc < D / 64; ++dc)
+              tma_store_4d(&tmO, qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T, it.h * g.m + pls,
+                           it.r);
+          }
+          bulk_commit();
+          bulk_wait_read0();     // the smem has been read: Q of the next item may land there
+          mbar_arrive(q_empty + qsl);
+          TRACE(3 + q, 27);
+        }
+      }
       if (lg == 0) TRACE(3 + q, 13);
     }
+    if (otma && warp == 4 + 4 * q && lane == 0) bulk_wait_all();  // O stores complete before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -607,24 +692,29 @@ __global__ void __launch_bounds__(Cfg2<NQT>::THREADS, 1)
 template <int NQT, bool PAGED, bool DENSE>
 int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
               void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st) {
-  using C = Cfg2<NQT>;
-  static const bool mf = [] {
-    const char* e = getenv("BFLA_MAXFIRST");
-    return !(e && atoi(e) == 0);
+  static const int smx = [] {
+    const char* e = getenv("BFLA_SMX");  // softmax variant (see k_attn2); default 1
+    const int v = e ? atoi(e) : 1;
+    return v == 0 ? 0 : 1;
   }();
-  // pairs e with e mod 8 in {1, 5} (1 in 4) on the FMA pipe: measured best of 0, 1/8, 1/4, 3/8, 1/2
-  auto kern = mf ? k_attn2<NQT, PAGED, DENSE, true, 0x22> : k_attn2<NQT, PAGED, DENSE, false, 0x22>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
-  if (e != cudaSuccess) return (int)e;
   static const int opts = [] {
     const char* e = getenv("BFLA_ATTN_OPTS");  // experiment switches (bit 0: no Q prefetch)
     return e ? atoi(e) : 0;
   }();
   const int grid = n_items < num_sms ? n_items : num_sms;
-  kern<<<grid, C::THREADS, C::SMEM_TOTAL, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
-                                                static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts);
-  count_launch();
-  return (int)cudaGetLastError();
+  auto go = [&](auto kern, int smem, int threads) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+    kern<<<grid, threads, smem, st>>>(maps.q, maps.k, maps.v, maps.o, maps.o_ok, g, list, count, pt,
+                                      static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts);
+    count_launch();
+    return (int)cudaGetLastError();
+  };
+  // pairs e with e mod 8 in {1, 5} (1 in 4) on the FMA pipe: measured best of 0, 1/8, 1/4, 3/8, 1/2
+  constexpr int PM = 0x22;
+  using C = Cfg2<NQT, PAGED>;
+  if (smx == 0) return go(k_attn2<NQT, PAGED, DENSE, 0, PM>, C::SMEM_TOTAL, C::THREADS);
+  return go(k_attn2<NQT, PAGED, DENSE, 1, PM>, C::SMEM_TOTAL, C::THREADS);
 }
 
 }  // namespace

@@ -38,6 +38,8 @@ void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int
 // Sparse / dense prefill (Eq. 27 / Eq. 1) — tcgen05 + TMEM + TMA.
 struct AttnMaps {
   CUtensorMap q, k, v;
+  CUtensorMap o;  // O as a TMA store target (attention2 epilogue), valid when o_ok
+  int o_ok = 0;
 };
 size_t attn_smem_bytes(int D, int nqt);
 int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,

@@ -25,7 +25,7 @@ import paper_2605_12193_b200 as bf  # noqa: E402
 import workloads  # noqa: E402
 from paper_2605_12193_b200 import _lib  # noqa: E402
 
-CTAS, ROLES, NEV = 4, 5, 8192
+CTAS, ROLES, NEV = 4, 6, 8192
 
 
 def main():
