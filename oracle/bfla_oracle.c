@@ -75,11 +75,23 @@ void orc_flatten(const float* x, int H, int N, int C, int b, int g, float* out, 
             }
 }
 
-/* Canonical fp32 dot product (DESIGN.md §4 item 2): acc = 0; acc = fma(x_k, y_k, acc) for
- * k ascending.  Single-rounding FMA, no reassociation. */
+/* Canonical fp32 dot product of two C-vectors (DESIGN.md §4 item 2): acc = 0; acc = fma(x_c, y_c,
+ * acc) for c ascending.  Single-rounding FMA, no reassociation.  (MEAN scores, and one token pair of
+ * a FLATTEN group dot below.) */
 static float dot_canon(const float* x, const float* y, int n) {
     float acc = 0.0f;
     for (int k = 0; k < n; ++k) acc = fmaf(x[k], y[k], acc);
+    return acc;
+}
+
+/* Canonical fp32 FLATTEN group dot (DESIGN.md §4 item 2, reading R2): the flattened g*C vectors are
+ * g consecutive tokens of C channels (index t*C + c, Eq. 7), so Phi(Q).Phi(K) = sum_t q_t . k_t.
+ * Each token pair is a canonical C-long FMA chain (c ascending); the g token dots are then added in
+ * ascending t with fp32 adds: acc = 0; acc = acc + dot_canon(x_t, y_t).  Padding tokens are exact
+ * zeros and add exact zeros. */
+static float dot_canon_flat(const float* x, const float* y, int g, int C) {
+    float acc = 0.0f;
+    for (int t = 0; t < g; ++t) acc = acc + dot_canon(x + (size_t)t * C, y + (size_t)t * C, C);
     return acc;
 }
 
@@ -118,7 +130,7 @@ void orc_block_scores(const float* q, const float* k, int Hq, int Hkv, int Nq, i
                             for (int v = 0; v < G; ++v) {
                                 if (!vk[(size_t)j * G + v]) continue;
                                 const float* y = pk + (((size_t)h * Lkv + j) * G + v) * gc;
-                                float s = dot_canon(x, y, (int)gc);
+                                float s = dot_canon_flat(x, y, g, C);
                                 if (s > best) best = s;
                             }
                         }

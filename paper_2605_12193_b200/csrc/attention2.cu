@@ -711,7 +711,10 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
     return (int)cudaGetLastError();
   };
   // pairs e with e mod 8 in {1, 5} (1 in 4) on the FMA pipe: measured best of 0, 1/8, 1/4, 3/8, 1/2
-  constexpr int PM = 0x22;
+#ifndef BFLA_POLY_MASK
+#define BFLA_POLY_MASK 0x22
+#endif
+  constexpr int PM = BFLA_POLY_MASK;
   using C = Cfg2<NQT, PAGED>;
   if (smx == 0) return go(k_attn2<NQT, PAGED, DENSE, 0, PM>, C::SMEM_TOTAL, C::THREADS);
   return go(k_attn2<NQT, PAGED, DENSE, 1, PM>, C::SMEM_TOTAL, C::THREADS);

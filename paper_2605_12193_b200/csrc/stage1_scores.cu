@@ -3,11 +3,12 @@
 // FLATTEN (the paper's flattening-g pooling, Eq. 6-10): for query head p (KV head h = p/m) the
 // block score S[p,i,j] = max over valid group pairs (u,v) of Phi(Q)[p,i,u] . Phi(K)[h,j,v], where a
 // group is g consecutive tokens flattened to a g*C vector (a zero-copy view of head-first Q/K).
-// The dot products are accumulated in the canonical order (DESIGN.md §4 item 2): one fp32 FMA per
-// element, element index ascending.  A register-blocked SIMT GEMM does exactly that: every thread
-// owns the G x G accumulators of one (i, j) block pair and updates them once per k, k ascending,
-// so the scores are bit-identical to the oracle's sequential chain and the G x G max-pool (Eq. 10)
-// happens in registers.
+// The dot products are accumulated in the canonical order (DESIGN.md §4 item 2): per token pair a
+// C-long fp32 FMA chain (channel ascending), the g token dots added in ascending token order.  A
+// register-blocked SIMT GEMM does exactly that: every thread owns the G x G token-chain accumulators
+// and G x G group totals of one (i, j) block pair; k (= t*C + c) ascends, and at every token boundary
+// the chains are added into the totals and restarted, so the scores are bit-identical to the
+// oracle's and the G x G max-pool (Eq. 10) happens in registers.
 //
 // MEAN (north_star variant, R1): qbar/kbar = fp32 block means (tokens summed in ascending order,
 // 128-bit loads, one half-warp per block), then one canonical C-long dot product per block pair.
@@ -108,11 +109,11 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
       }
     }
   };
-  float acc[G][G];
+  float acc[G][G], tot[G][G];
 #pragma unroll
   for (int u = 0; u < G; ++u)
 #pragma unroll
-    for (int v = 0; v < G; ++v) acc[u][v] = 0.0f;
+    for (int v = 0; v < G; ++v) acc[u][v] = tot[u][v] = 0.0f;
 
   load(0);
   store(0);
@@ -139,6 +140,15 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
           acc[u][v] = __fmaf_rn(a[u].w, bv[v].w, acc[u][v]);
         }
     }
+    if (((it + 1) * KC) % g.D == 0) {  // token boundary: add the token dot, restart the chain
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+#pragma unroll
+        for (int v = 0; v < G; ++v) {
+          tot[u][v] = __fadd_rn(tot[u][v], acc[u][v]);
+          acc[u][v] = 0.0f;
+        }
+    }
     if (it + 1 < nit) store((it + 1) & 1);
     __syncthreads();
   }
@@ -154,7 +164,7 @@ __global__ void __launch_bounds__(256) k_s1_flatten_scores(Geom g, const __nv_bf
 #pragma unroll
     for (int v = 0; v < G; ++v) {
       if (j * g.b + v * g.g >= R.Nkv) continue;  // padding-only key group
-      best = fmaxf(best, acc[u][v]);
+      best = fmaxf(best, tot[u][v]);
     }
   }
   S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = best;

@@ -26,13 +26,15 @@ constexpr int ABYTES = TM * TK * 2;
 constexpr int BBYTES = TN * TK * 2;
 constexpr int SMEM = ST * (ABYTES + BBYTES) + 2 * ST * 8 + 8 + 16 + 1024;
 
-// ---- group norms: one CTA per (request, head, block) of Q (first) or K; warp w sums the squares of
-// group w (16-byte loads, 4 in flight per lane), lanes combine by shuffles, the block keeps the max
-// over its groups.  Rounded up by a relative 2^-10 so it bounds the exact norm despite fp32 rounding.
+// ---- group norms: one CTA per (request, head, block) of Q (first) or K.  All eight warps stream:
+// warp w takes group w % G and the (w / G)-th of 8 / G contiguous token slices of it (G <= 8), each lane
+// keeps eight 16-byte loads in flight; slices combine through smem, the block keeps the max over its
+// groups.  Rounded up by a relative 2^-10 so it bounds the exact norm despite fp32 rounding.  HBM-bound
+// (reads Q and K once); it runs on a side stream next to the tensor-core scores.
 __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloat16* __restrict__ q,
                                                         const __nv_bfloat16* __restrict__ k, float* __restrict__ qn,
                                                         float* __restrict__ kn) {
-  __shared__ float wmax[8];
+  __shared__ float part[8];
   const long long u = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long nq = (long long)g.B * g.Hq * g.Lq;
@@ -43,36 +45,57 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
   const Req R = req_of(g, r);
   const int N = isq ? R.Nq : R.Nkv;
   const int vec_per_tok = g.D / 8;
-  float best = 0.f;
-  for (int grp = warp; grp < g.G; grp += 8) {
+  const int G = g.G <= 8 ? g.G : 8, parts = 8 / G;
+  float acc = 0.f;
+  for (int grp = warp % G; grp < g.G; grp += G) {  // G > 8 (not built for FLATTEN) stays correct
     const int t0 = blk * g.b + grp * g.g;
     const int ntok = min(g.g, N - t0);
-    float acc = 0.f;
-    if (ntok > 0) {
-      const int nvec = ntok * vec_per_tok;
-#pragma unroll 4
-      for (int x = lane; x < nvec; x += 32) {
-        const int t = t0 + x / vec_per_tok, c = (x % vec_per_tok) * 8;
-        const __nv_bfloat16* row = isq ? q + (long long)r * g.qs0 + (long long)hh * g.qs1 + (long long)t * g.qs2
-                                       : k + (long long)r * g.kvs0 + (long long)hh * g.kvs1 + (long long)t * g.kvs2;
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(row + c));
-        const uint32_t w4[4] = {raw.x, raw.y, raw.z, raw.w};
+    if (ntok <= 0) continue;
+    const int per = (ntok + parts - 1) / parts;
+    const int ta = t0 + (warp / G) * per, tb = min(t0 + ntok, ta + per);
+    if (ta >= tb) continue;
+    const int nvec = (tb - ta) * vec_per_tok;
+    const __nv_bfloat16* base = isq ? q + (long long)r * g.qs0 + (long long)hh * g.qs1
+                                    : k + (long long)r * g.kvs0 + (long long)hh * g.kvs1;
+    const long long ts = isq ? g.qs2 : g.kvs2;
+    float a8[8];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float a = __uint_as_float(w4[e] << 16), b2 = __uint_as_float(w4[e] & 0xffff0000u);
-          acc = fmaf(a, a, fmaf(b2, b2, acc));
+    for (int e = 0; e < 8; ++e) a8[e] = 0.f;
+    for (int x0 = lane; x0 < nvec; x0 += 8 * 32) {
+      uint4 raw[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int x = x0 + e * 32;
+        raw[e] = make_uint4(0, 0, 0, 0);
+        if (x < nvec) {
+          const int t = ta + x / vec_per_tok, c = (x % vec_per_tok) * 8;
+          raw[e] = __ldg(reinterpret_cast<const uint4*>(base + (long long)t * ts + c));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t w4[4] = {raw[e].x, raw[e].y, raw[e].z, raw[e].w};
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const float a = __uint_as_float(w4[f] << 16), b2 = __uint_as_float(w4[f] & 0xffff0000u);
+          a8[e] = fmaf(a, a, fmaf(b2, b2, a8[e]));
         }
       }
     }
+    float s = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    best = fmaxf(best, acc);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    acc = fmaxf(acc, s);  // G > 8: several whole groups per warp (parts = 1), max over them
   }
-  if (lane == 0) wmax[warp] = best;
+  if (lane == 0) part[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     float m = 0.f;
-    for (int e = 0; e < 8; ++e) m = fmaxf(m, wmax[e]);
+    for (int gi = 0; gi < G; ++gi) {  // group gi's slices sit in warps gi, gi + G, ...
+      float s = 0.f;
+      for (int pi = 0; pi < parts; ++pi) s += part[gi + pi * G];
+      m = fmaxf(m, s);
+    }
     (isq ? qn : kn)[w] = sqrtf(m) * (1.0f + 0x1p-10f) + 1e-30f;  // fp32 sum slack
   }
 }
@@ -176,135 +199,99 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   }
 }
 
-// ---- canonical recompute of flagged head rows.  Work unit = (flagged head row (r,p,i), chunk of 16 KV
-// blocks); thread t owns one dot product (j, u, v).  The G query groups and 16 G key groups stream
-// through a 4-stage cp.async ring in k-chunks of 128 elements (bf16, 16-byte copies, padded rows);
-// each thread adds its chunk's 128 products in ascending order with single-rounding FMAs, so every
-// dot product is exactly the canonical chain (k is the outer loop and ascending).  The G x G max is
-// taken through smem.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// ---- canonical recompute of flagged head rows (DESIGN.md §4 item 2 order).  Work unit = (flagged head
+// row (r,p,i), KV block j) for every causal j whose score can still carry canonical probability
+// (S_f >= flag_thr: below it 2^t underflows to an exact 0 whatever the rounding).  The unit's G x G
+// group dots are G*G*g independent token-pair chains (C-long fp32 FMA chains, channel ascending): a
+// thread runs four of them side by side straight from global memory (16-byte loads, L1/L2-resident
+// rows), the token dots land in smem, and G*G threads add them in ascending token order — the
+// oracle's order exactly.  Units are short (one C-long chain plus a g-long sum), so the flagged set
+// spreads over every SM and finishes in a few microseconds.
+constexpr int kRecThreads = 256;
 
-template <int G>
-__global__ void __launch_bounds__(256) k_s1_recompute_rows(Geom g, const __nv_bfloat16* __restrict__ q,
-                                                           const __nv_bfloat16* __restrict__ k,
-                                                           const int32_t* __restrict__ flagged,
-                                                           const int32_t* __restrict__ n_flagged,
-                                                           const float* __restrict__ flag_thr,
-                                                           float* __restrict__ S) {
-  // k-chunk: 256 elements (two tokens at d = 128; rows are contiguous token runs on this path)
-  constexpr int KC = G <= 4 ? 256 : 128, JB = 16, NST = 4;
-  constexpr int ROWS = G + JB * G, RB = KC * 2 + 16;  // row bytes padded by 16 (bank spread)
-  constexpr int NDOT = JB * G * G, PER = (NDOT + 255) / 256;
-  extern __shared__ __align__(16) unsigned char rsm[];
-  float* part = reinterpret_cast<float*>(rsm + NST * ROWS * RB);
-  __shared__ uint32_t live_bits;  // blocks of this chunk whose canonical logit can exceed -127
+__device__ __forceinline__ void bf16x8_f32(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const __nv_bfloat16* __restrict__ q,
+                                                                   const __nv_bfloat16* __restrict__ k,
+                                                                   const int32_t* __restrict__ flagged,
+                                                                   const int32_t* __restrict__ n_flagged,
+                                                                   const float* __restrict__ flag_thr,
+                                                                   float* __restrict__ S) {
+  extern __shared__ float tokdot[];  // [G*G][g] token dots of the current unit
   const int nf = *n_flagged;
-  const int chunks = (g.Lkv + JB - 1) / JB;
-  const long long units = (long long)nf * chunks;
-  const int gc = g.g * g.D, nk = gc / KC;
+  const int G = g.G, gg = g.g, nch = G * G * gg;
+  const long long units = (long long)nf * g.Lkv;
   for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
-    const int chunk = (int)(unit % chunks);
-    const int row = flagged[unit / chunks];  // (r * Hq + p) * Lq + i
+    const int j = (int)(unit % g.Lkv);
+    const int fidx = (int)(unit / g.Lkv);
+    const int row = flagged[fidx];  // (r * Hq + p) * Lq + i
     const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
     const int h = p / g.m;
     const Req R = req_of(g, r);
     long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
-    const int jmax = (int)(e_i / g.b);
-    const int j0 = chunk * JB;
-    if (j0 > jmax) continue;  // uniform over the CTA
-    __syncthreads();          // the previous unit's readers are done with the ring (and live_bits)
+    if ((long long)j * g.b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    if (threadIdx.x < 32) {
-      const float thr = flag_thr[unit / chunks];
-      const int j = j0 + threadIdx.x;
-      const bool live = threadIdx.x < JB && j <= jmax && srow[j] >= thr;
-      const uint32_t bal = __ballot_sync(0xffffffffu, live);
-      if (threadIdx.x == 0) live_bits = bal;
+    if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
+    const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
+    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)h * g.kvs1;
+    // chains c = (u, v, t), t fastest: four per thread per pass
+    for (int c0 = threadIdx.x * 4; c0 < nch; c0 += kRecThreads * 4) {
+      const __nv_bfloat16* xs[4];
+      const __nv_bfloat16* ys[4];
+      bool ok[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = c0 + e;
+        const int t = c % gg, uv = c / gg, u = uv / G, v = uv % G;
+        const int tq = i * g.b + u * gg + t, tk = j * g.b + v * gg + t;
+        ok[e] = c < nch && tq < R.Nq && tk < R.Nkv;  // padding tokens are exact zeros: dot 0
+        xs[e] = qb + (long long)(ok[e] ? tq : 0) * g.qs2;
+        ys[e] = kb + (long long)(ok[e] ? tk : 0) * g.kvs2;
+      }
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+      for (int cc = 0; cc < D; cc += 8) {
+        float xf[4][8], yf[4][8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(xs[e] + cc)), xf[e]);
+          bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(ys[e] + cc)), yf[e]);
+        }
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(xf[e][x], yf[e][x], acc[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (c0 + e < nch) tokdot[c0 + e] = ok[e] ? acc[e] : 0.0f;
     }
     __syncthreads();
-    const uint32_t live = live_bits;
-    if (!live) continue;  // every block of the chunk has an exactly-zero canonical probability
-    auto issue = [&](int kc) {
-      unsigned char* buf = rsm + (kc % NST) * ROWS * RB;
-      const int x0 = kc * KC, tk = x0 / g.D, c0 = x0 % g.D;
-      for (int sidx = threadIdx.x; sidx < ROWS * (KC / 8); sidx += blockDim.x) {
-        const int rr = sidx / (KC / 8), piece = sidx % (KC / 8);
-        const __nv_bfloat16* src = q;
-        bool ok = false;
-        if (rr < G) {
-          const int t = i * g.b + rr * g.g + tk;
-          ok = t < R.Nq;
-          if (ok) src = q + (long long)r * g.qs0 + (long long)p * g.qs1 + (long long)t * g.qs2 + c0 + piece * 8;
-        } else {
-          const int bi = rr - G, jl = bi / G, v = bi % G;
-          const int s = (j0 + jl) * g.b + v * g.g + tk;
-          ok = ((live >> jl) & 1u) && s < R.Nkv;
-          if (ok) src = k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2 + c0 + piece * 8;
-        }
-        cp_async16(buf + rr * RB + piece * 16, src, ok);  // zero-filled when !ok (padding)
-      }
-      cp_async_commit();
-    };
-    float acc[PER];
-#pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] = 0.0f;
-    for (int kc = 0; kc < NST - 1; ++kc) {
-      if (kc < nk) issue(kc);
-      else cp_async_commit();
-    }
-    for (int kc = 0; kc < nk; ++kc) {
-      cp_async_wait<NST - 2>();
-      __syncthreads();
-      if (kc + NST - 1 < nk) issue(kc + NST - 1);
-      else cp_async_commit();
-      const unsigned char* buf = rsm + (kc % NST) * ROWS * RB;
-#pragma unroll
-      for (int e = 0; e < PER; ++e) {
-        const int di = threadIdx.x + e * 256;
-        if (di < NDOT && ((live >> (di / (G * G))) & 1u)) {
-          const int jl = di / (G * G), u = (di / G) % G, v = di % G;
-          const uint2* xa = reinterpret_cast<const uint2*>(buf + u * RB);
-          const uint2* yb = reinterpret_cast<const uint2*>(buf + (G + jl * G + v) * RB);
-          float a = acc[e];
-#pragma unroll 8
-          for (int q4 = 0; q4 < KC / 4; ++q4) {
-            const uint2 xv = xa[q4], yv = yb[q4];
-            a = __fmaf_rn(__uint_as_float(xv.x << 16), __uint_as_float(yv.x << 16), a);
-            a = __fmaf_rn(__uint_as_float(xv.x & 0xffff0000u), __uint_as_float(yv.x & 0xffff0000u), a);
-            a = __fmaf_rn(__uint_as_float(xv.y << 16), __uint_as_float(yv.y << 16), a);
-            a = __fmaf_rn(__uint_as_float(xv.y & 0xffff0000u), __uint_as_float(yv.y & 0xffff0000u), a);
-          }
-          acc[e] = a;
-        }
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-      const int di = threadIdx.x + e * 256;
-      if (di < NDOT) part[di] = acc[e];
+    float* pairtot = tokdot + nch;
+    if (threadIdx.x < G * G) {
+      // thread (u, v): the g token dots added in ascending t (the oracle's order)
+      const int uv = threadIdx.x, u = uv / G, v = uv % G;
+      float a = 0.0f;
+      for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[uv * gg + t]);
+      const bool valid = i * g.b + u * gg < R.Nq && j * g.b + v * gg < R.Nkv;  // padding-only groups (R3)
+      pairtot[uv] = valid ? a : -INFINITY;
     }
     __syncthreads();
-    if (threadIdx.x < JB) {
-      const int jl = threadIdx.x, j = j0 + jl;
-      if ((live >> jl) & 1u) {
-        float mx = -INFINITY;
-        for (int u = 0; u < G; ++u) {
-          if (i * g.b + u * g.g >= R.Nq) continue;  // padding-only query group (R3)
-          for (int v = 0; v < G; ++v)
-            if (j * g.b + v * g.g < R.Nkv) mx = fmaxf(mx, part[(jl * G + u) * G + v]);
-        }
-        srow[j] = mx;
-      }
+    if (threadIdx.x == 0) {
+      float mx = -INFINITY;  // Eq. 10: max over the group pairs (exact, order-free)
+      for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
+      srow[j] = mx;
     }
+    __syncthreads();  // tokdot is reused by the next unit
   }
 }
 
@@ -360,21 +347,17 @@ void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, 
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
                           const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st) {
   (void)pt;
+  if (g.G * g.G > kRecThreads) return -1;
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
-  auto go = [&](auto kern, int G) {
-    const int KC = G <= 4 ? 256 : 128;
-    const size_t smem = (size_t)4 * (G + 16 * G) * (KC * 2 + 16) + (size_t)16 * G * G * 4;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<2 * num_sms, 256, smem, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
+  const int smem = (g.G * g.G * g.g + g.G * g.G) * 4;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<num_sms * 4, kRecThreads, smem, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
   };
-  switch (g.G) {
-    case 1: go(k_s1_recompute_rows<1>, 1); break;
-    case 2: go(k_s1_recompute_rows<2>, 2); break;
-    case 4: go(k_s1_recompute_rows<4>, 4); break;
-    case 8: go(k_s1_recompute_rows<8>, 8); break;
-    default: return -1;
-  }
+  if (g.D == 128) go(k_s1_recompute_rows<128>);
+  else if (g.D == 256) go(k_s1_recompute_rows<256>);
+  else return -1;
   count_launch();
   return (int)cudaGetLastError();
 }

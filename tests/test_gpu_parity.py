@@ -2,6 +2,8 @@
 
 Masks (coarse bits, tile labels, lists, counts) must be bit-exact; O within max-abs 2e-2 and
 mean-abs 2e-3 of the fp64 oracle (BASELINE.json).  Sizes span several tiles and ragged tails."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -122,6 +124,47 @@ def test_fast_scores_certified_equal_canonical(dist, gamma):
     tau = 2.0 ** -24 * (10 * n ** 0.5 + n / 8)
     print(f"max |S_tc - S_canon| / (|x||y|) = {ratio:.3e}  (tau = {tau:.3e})")
     assert ratio < tau / 8
+
+
+def _ws_norms(ws: torch.Tensor, B, Hq, Hkv, Nq, Nkv, d, b, T=64, paged=False):
+    """qn / kn from the workspace (layout of api.cu ws_layout, 256-byte aligned segments)."""
+    al = lambda x: (x + 255) & ~255
+    cd = lambda a, c: -(-a // c)
+    Lq, Lkv, Tq, Tkv = cd(Nq, b), cd(Nkv, b), cd(Nq, T), cd(Nkv, T)
+    a = Nc = Nkv - Nq
+    a = cd(Nc, T) + 1
+    i0 = max(Tkv - a, 0)
+    causal = (i0 * a + i0 * (i0 - 1) // 2 + (Tq - i0) * Tkv) if Tq > i0 else (Tq * a + Tq * (Tq - 1) // 2)
+    o = 0
+    for size in [B * Hq * Lq * Lkv * 4, B * Hq * Lq * d * 4, B * Hkv * Lkv * d * 4, B * Hkv * Lq * cd(Lkv, 32) * 4,
+                 B * Hkv * Tq * cd(Tkv, 32) * 4, B * Hkv * causal * 4, B * Hkv * Tq * 4]:
+        o += al(size)
+    o += al(ctypes.sizeof(bf.bfla_stats))
+    qn = ws[o:o + B * Hq * Lq * 4].view(torch.float32).view(B, Hq, Lq).cpu().numpy()
+    o += al(B * Hq * Lq * 4)
+    kn = ws[o:o + B * Hkv * Lkv * 4].view(torch.float32).view(B, Hkv, Lkv).cpu().numpy()
+    return qn, kn
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8])
+def test_certification_norms(m):
+    """The certification bounds of the fast Stage-1 path (block maxima of the group l2 norms, DESIGN.md
+    §4) bound the exact norms from above and stay within 2^-9 of them, for G = 4 groups per block and
+    every GQA group size; AUTO masks equal CANONICAL masks.  N = 20480 gives two score N tiles."""
+    B, Hkv, N, d, b = 1, 2, 20480, 128, 256
+    Hq = m * Hkv
+    prob = workloads.gaussian(31 + m, B=B, Hq=Hq, Hkv=Hkv, Nq=N, Nkv=N, d=d, sigma=0.8)
+    fast = run_gpu(prob, bf.Config(b=b, g=64, gamma=0.95, scores=bf.SCORES_AUTO), lse=False)
+    canon = run_gpu(prob, bf.Config(b=b, g=64, gamma=0.95, scores=bf.SCORES_CANONICAL), lse=False)
+    assert np.array_equal(fast["coarse"], canon["coarse"])
+    assert np.array_equal(fast["labels"], canon["labels"])
+    qn, kn = _ws_norms(fast["ws"], B, Hq, Hkv, N, N, d, b)
+    L = N // b
+    qx = prob.q[0].float().reshape(Hq, L, b // 64, 64 * d).norm(dim=-1).amax(-1).double().numpy()
+    kx = prob.k[0].float().reshape(Hkv, L, b // 64, 64 * d).norm(dim=-1).amax(-1).double().numpy()
+    for got, want in ((qn[0], qx), (kn[0], kx)):
+        assert (got >= want * (1 - 1e-6)).all(), "norm bound below the exact norm"
+        assert (got <= want * (1 + 2 ** -9) + 1e-6).all(), "norm bound loose"
 
 
 def test_mean_pool_and_keep_ratio():

@@ -144,6 +144,28 @@ def test_block_scores_float_close_to_exact(orc):
                 assert abs(S[p, i, j] - exact.max()) <= bound.max() + 1e-6
 
 
+def test_block_scores_two_level_order_bound(orc):
+    # DESIGN.md §4 item 2: a group dot is g token dots (C-long FMA chains) added in token order, so
+    # every product passes through at most C + g roundings: |S - exact| <= gamma_{C+g} sum|xy| — a
+    # bound the single gC-long chain does not meet in general (tight inputs: large cancelling terms).
+    rng = np.random.default_rng(13)
+    C, g, b = 32, 16, 64
+    q = (rng.standard_normal((1, 256, C)) * np.exp(rng.standard_normal((1, 256, C)) * 2)).astype(np.float32)
+    k = (rng.standard_normal((1, 256, C)) * np.exp(rng.standard_normal((1, 256, C)) * 2)).astype(np.float32)
+    S = orc.block_scores(q, k, b, g)
+    G, gc = b // g, g * C
+    pq = q.reshape(1, 4, G, gc).astype(np.float64)
+    pk = k.reshape(1, 4, G, gc).astype(np.float64)
+    n = C + g
+    for i in range(4):
+        for j in range(i + 1):
+            prods = pq[0, i][:, None, :] * pk[0, j][None, :, :]
+            exact = prods.sum(-1)
+            bound = n * 2.0 ** -24 / (1 - n * 2.0 ** -24) * np.abs(prods).sum(-1)
+            # the max over pairs moves by at most the largest per-pair bound
+            assert abs(S[0, i, j] - exact.max()) <= bound.max()
+
+
 def test_block_scores_linearity(orc):
     # scaling K block j by 2 doubles S[., ., j] (exact: power-of-two scale)
     rng = np.random.default_rng(4)

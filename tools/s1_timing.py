@@ -1,0 +1,38 @@
+"""Live timing of bfla_block_mask on a BASELINE workload (CUDA events, 20 reps after warm-up), printing
+the flagged-row statistics; run under different BFLA_* experiment env vars to attribute Stage-1 time."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2605_12193_b200 as bf  # noqa: E402
+import workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=32768)
+ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--reps", type=int, default=20)
+a = ap.parse_args()
+prob = workloads.structured(303, 1, a.hq, 8, a.n, a.n, 128, block=256, theta=5e5, device="cuda")
+o = torch.empty_like(prob.q)
+cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, n_local=8, eta=16, rho=0.0)
+P = bf.make_problem(prob.q, prob.k, prob.v, o)
+ws = bf.alloc_workspace(P, cfg)
+m = bf.alloc_mask(P, cfg)
+for _ in range(3):
+    bf.bfla_block_mask(P, cfg, m, ws)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ts = []
+for _ in range(a.reps):
+    e0.record()
+    bf.bfla_block_mask(P, cfg, m, ws)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+ts.sort()
+st = m.stats_dict()
+print(f"env={ {k: v for k, v in os.environ.items() if k.startswith('BFLA_')} } n={a.n} block_mask ms: median "
+      f"{ts[len(ts) // 2]:.4f} min {ts[0]:.4f}  flagged {st['rows_flagged']} recomputed {st['rows_recomputed']}")
