@@ -61,11 +61,11 @@ constexpr float kLazy = 24.0f;
 
 template <int NQT, bool PAGED = false>
 struct Cfg2 {
-  // Q ring of NQT + 1 tiles: the next item's first Q tile loads while this item still holds its
-  // tiles (the last ones double as O staging for the TMA-store epilogue; contiguous K/V only —
-  // tiles; paged K/V keep a 3-deep K ring instead: their page-granular loads need the lead)
+  // BFLA_QRING=1: Q ring of NQT + 1 tiles (the next item's first Q tile loads while this item still
+  // holds its tiles) at the price of a 2-deep K ring.  Default off: a 3-deep K ring measured better
+  // (K loads arrive ~2 us after their slot frees; sparse 32K 1.014 -> 1.005 ms, dense 7.81 -> 7.29 ms)
 #ifndef BFLA_QRING
-#define BFLA_QRING 1
+#define BFLA_QRING 0
 #endif
   static constexpr bool QR = BFLA_QRING && !PAGED;
   static constexpr int QS = QR ? NQT + 1 : NQT, KS = QR ? 2 : 3, VS = NQT == 2 ? 2 : 3;
