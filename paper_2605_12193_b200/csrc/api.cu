@@ -242,13 +242,15 @@ static bfla_status cuda_check(const char* what) {
 }
 
 // tau: |S_tc - S_canonical| <= tau * ||x|| * ||y|| for one g*C-long group dot product.  Model: the
-// canonical round-to-nearest chain stays within 10 sqrt(n) u of sum|x_k y_k| (probabilistic rounding
-// error analysis; exceeding it has probability < 2n exp(-50)); the tensor-core chain of n/16 MMA steps
-// within 2 (n/16) u even if every internal step truncated.  Cauchy-Schwarz: sum|x_k y_k| <= ||x|| ||y||.
-// The bench/tests measure the observed ratio — it sits orders of magnitude below tau.
+// canonical order (g token chains of C FMAs, then g - 1 adds; DESIGN.md §4 item 2) makes C + g
+// round-to-nearest errors per product path, each at most u times a partial sum bounded by
+// sum|x_k y_k|; as independent mean-zero terms they stay within 10 sqrt(C + g) u sum|x_k y_k| (Hoeffding;
+// exceeding it has probability < 2 exp(-50)); the tensor-core chain of n/16 MMA steps stays within
+// 2 (n/16) u even if every internal step truncated (biased, so no square root).  Cauchy-Schwarz:
+// sum|x_k y_k| <= ||x|| ||y||.  The tests measure the observed ratio — it sits far below tau.
 static float certify_tau(const Geom& g) {
   const double n = (double)g.g * g.D, u = std::ldexp(1.0, -24);
-  double tau = u * (10.0 * std::sqrt(n) + n / 8.0);
+  double tau = u * (10.0 * std::sqrt((double)g.D + g.g) + n / 8.0);
   if (const char* e = getenv("BFLA_TAU_SCALE")) tau *= atof(e);  // calibration experiments only
   return (float)tau;
 }
@@ -321,7 +323,18 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     const int sms = num_sms_current();
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
                   1, qn, kn, certify_tau(g), flagged, nflag, sms, fthr);
-    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, fthr, S, sms, st))
+    CUtensorMap rq, rk;  // token-row maps (64 x 64 SW128 boxes) for the TMA-staged recompute
+    bool rmaps;
+    {
+      const uint64_t dq[4] = {(uint64_t)g.D, (uint64_t)g.Nq, (uint64_t)g.Hq, (uint64_t)g.B};
+      const uint64_t sq[3] = {(uint64_t)g.qs2 * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
+      const uint64_t dk[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv, (uint64_t)g.B};
+      const uint64_t sk[3] = {(uint64_t)gk.kvs2 * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
+      const uint32_t box[4] = {64, 64, 1, 1};
+      rmaps = encode_4d_quiet(&rq, P->q, dq, sq, box) && encode_4d_quiet(&rk, kc, dk, sk, box);
+    }
+    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, fthr, S, sms, st, rmaps ? &rq : nullptr,
+                              rmaps ? &rk : nullptr))
       return fail(BFLA_ERR_CUDA, "recompute launch failed");
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
                   2, nullptr, nullptr, 0.f, flagged, nflag, sms);

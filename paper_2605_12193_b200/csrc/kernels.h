@@ -27,8 +27,10 @@ constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, cudaStream_t st);
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st);
+// tmQ / tmK (optional): {D, N, H, B} maps with 64 x 64 SW128 boxes for the TMA-staged variant
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st);
+                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st,
+                          const CUtensorMap* tmQ = nullptr, const CUtensorMap* tmK = nullptr);
 void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, void* kout, cudaStream_t st);
 // Stage 2 (Eq. 19-26)
 void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int n_local, int eta, double rho,

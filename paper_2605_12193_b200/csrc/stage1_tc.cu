@@ -11,6 +11,8 @@
 // rows it cannot certify are recomputed here in the canonical order (k_s1_recompute_rows).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -295,6 +297,256 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
   }
 }
 
+// Same units and the same arithmetic order, operands staged in shared memory: the unit's K block and
+// its query groups (double-buffered, one group per phase) arrive by bulk copies (one per token row,
+// rows padded by 16 bytes so the 32 lanes of a warp — consecutive tokens — read distinct banks);
+// thread = token-pair chain (v, t) of the current query group u.  Used when the block fits in smem.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const __nv_bfloat16* __restrict__ q,
+                                                                   const __nv_bfloat16* __restrict__ k,
+                                                                   const int32_t* __restrict__ flagged,
+                                                                   const int32_t* __restrict__ n_flagged,
+                                                                   const float* __restrict__ flag_thr,
+                                                                   float* __restrict__ S) {
+  constexpr int PITCH = D * 2 + 16;  // bytes per staged token row
+  extern __shared__ __align__(16) unsigned char rs[];
+  const int G = g.G, gg = g.g, b = g.b;
+  unsigned char* kb_s = rs;                                  // [b][PITCH]
+  unsigned char* qg_s = rs + (size_t)b * PITCH;              // [2][g][PITCH]
+  float* tokdot = reinterpret_cast<float*>(qg_s + (size_t)2 * gg * PITCH);  // [G*G][g]
+  float* pairtot = tokdot + G * G * gg;                      // [G*G]
+  __shared__ __align__(8) uint64_t bar[3];                   // K block, query group buffers 0 / 1
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < 3; ++e) mbar_init(bar + e, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  uint32_t ph[3] = {0, 0, 0};
+  const int nf = *n_flagged;
+  const long long units = (long long)nf * g.Lkv;
+  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int j = (int)(unit % g.Lkv);
+    const int fidx = (int)(unit / g.Lkv);
+    const int row = flagged[fidx];  // (r * Hq + p) * Lq + i
+    const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
+    const int h = p / g.m;
+    const Req R = req_of(g, r);
+    long long e_i = (long long)R.Nc + (long long)(i + 1) * b - 1;
+    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+    if ((long long)j * b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
+    float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
+    if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
+    const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
+    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)h * g.kvs1;
+    const int kt0 = j * b, nkt = min(b, R.Nkv - kt0);  // valid key tokens of the block
+    auto stage_q = [&](int u, int buf) {  // warp 0: query group u -> buffer buf
+      const int qt0 = i * b + u * gg, nqt = max(0, min(gg, R.Nq - qt0));
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(bar + 1 + buf, (uint32_t)(nqt * D * 2));
+      __syncwarp();
+      for (int t = threadIdx.x; t < nqt; t += 32)
+        bulk_g2s(qg_s + ((size_t)buf * gg + t) * PITCH, qb + (long long)(qt0 + t) * g.qs2, D * 2, bar + 1 + buf);
+    };
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (uint32_t)(nkt * D * 2));
+      __syncwarp();
+      for (int t = threadIdx.x; t < nkt; t += 32)
+        bulk_g2s(kb_s + (size_t)t * PITCH, kb + (long long)(kt0 + t) * g.kvs2, D * 2, bar);
+      stage_q(0, 0);
+    }
+    mbar_wait(bar, ph[0]);
+    ph[0] ^= 1;
+    for (int u = 0; u < G; ++u) {
+      const int buf = u & 1;
+      if (u + 1 < G && threadIdx.x < 32) stage_q(u + 1, buf ^ 1);  // buffer buf^1 was released at u-1
+      mbar_wait(bar + 1 + buf, ph[1 + buf]);
+      ph[1 + buf] ^= 1;
+      const int qt0 = i * b + u * gg;
+      for (int c = threadIdx.x; c < G * gg; c += kRecThreads) {  // chain (v, t), t fastest
+        const int t = c % gg, v = c / gg;
+        const bool ok = qt0 + t < R.Nq && v * gg + t < nkt;  // padding tokens: exact zero dot
+        float acc = 0.f;
+        if (ok) {
+          const unsigned char* xr = qg_s + ((size_t)buf * gg + t) * PITCH;
+          const unsigned char* yr = kb_s + (size_t)(v * gg + t) * PITCH;
+#pragma unroll 4
+          for (int cc = 0; cc < D; cc += 8) {
+            float xf[8], yf[8];
+            bf16x8_f32(*reinterpret_cast<const uint4*>(xr + cc * 2), xf);
+            bf16x8_f32(*reinterpret_cast<const uint4*>(yr + cc * 2), yf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xf[e], yf[e], acc);
+          }
+        }
+        tokdot[(u * G + v) * gg + t] = acc;
+      }
+      __syncthreads();  // query buffer buf is free again; after the last u tokdot is complete
+    }
+    if (threadIdx.x < G * G) {
+      const int uv = threadIdx.x, u = uv / G, v = uv % G;
+      float a = 0.0f;
+      for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[uv * gg + t]);  // ascending t
+      const bool valid = i * b + u * gg < R.Nq && j * b + v * gg < R.Nkv;  // padding-only groups (R3)
+      pairtot[uv] = valid ? a : -INFINITY;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mx = -INFINITY;  // Eq. 10
+      for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
+      srow[j] = mx;
+    }
+    __syncthreads();  // smem reused by the next unit
+  }
+}
+
+// TMA-staged variant (head_dim 128): each CTA walks a contiguous range of units (flagged row, KV
+// block), so consecutive units share the row's query block, which is loaded once; the KV blocks are
+// double-buffered (the next live unit's block loads while the current one is computed).  Blocks arrive
+// as 64-token x 64-column SW128 boxes through the same kind of tensor maps as the attention, so a
+// warp's lanes — consecutive tokens — read distinct banks.  Thread = (query group u, token t); it
+// runs the G chains (u, v, t), v = 0..G-1, side by side (the query token is shared).
+template <int D>
+__global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_constant__ CUtensorMap tmQ,
+                                                                  const __grid_constant__ CUtensorMap tmK, Geom g,
+                                                                  const int32_t* __restrict__ flagged,
+                                                                  const int32_t* __restrict__ n_flagged,
+                                                                  const float* __restrict__ flag_thr,
+                                                                  float* __restrict__ S) {
+  constexpr int NCH = D / 64;  // 64-column chunks per token row
+  extern __shared__ __align__(1024) unsigned char rs_raw[];
+  unsigned char* rs = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(rs_raw) + 1023) & ~uintptr_t(1023));
+  const int G = g.G, gg = g.g, b = g.b, nrt = b / 64;  // 64-token row tiles per block
+  const int blk_bytes = b * D * 2;
+  unsigned char* qs = rs;                                      // query block
+  unsigned char* ks[2] = {rs + blk_bytes, rs + 2 * blk_bytes};  // KV blocks (double buffer)
+  float* tokdot = reinterpret_cast<float*>(rs + 3 * blk_bytes);  // [G*G][g]
+  float* pairtot = tokdot + G * G * gg;
+  __shared__ __align__(8) uint64_t bar[3];  // query block, KV buffers 0 / 1
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < 3; ++e) mbar_init(bar + e, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int nf = *n_flagged;
+  const long long units = (long long)nf * g.Lkv;
+  const long long per = (units + gridDim.x - 1) / gridDim.x;
+  const long long u0 = (long long)blockIdx.x * per, u1 = min(units, u0 + per);
+  // a unit is live if causal and its score can still carry canonical probability (uniform test)
+  auto live = [&](long long unit) -> bool {
+    const int j = (int)(unit % g.Lkv), fidx = (int)(unit / g.Lkv);
+    const int row = flagged[fidx];
+    const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
+    const Req R = req_of(g, r);
+    long long e_i = (long long)R.Nc + (long long)(i + 1) * b - 1;
+    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+    if ((long long)j * b > e_i || j >= R.Lkv) return false;
+    return S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] >= flag_thr[fidx];
+  };
+  auto next_live = [&](long long from) -> long long {
+    while (from < u1 && !live(from)) ++from;
+    return from;
+  };
+  auto load_block = [&](unsigned char* dst, const CUtensorMap* map, uint64_t* br, int t0, int hh, int r) {
+    mbar_arrive_expect_tx(br, (uint32_t)blk_bytes);
+    for (int rt = 0; rt < nrt; ++rt)
+      for (int cc = 0; cc < NCH; ++cc)
+        tma_load_4d(dst + (rt * NCH + cc) * 8192, map, br, cc * 64, t0 + rt * 64, hh, r);
+  };
+  auto decode = [&](long long unit, int& j, int& i, int& p, int& r, int& fidx) {
+    j = (int)(unit % g.Lkv);
+    fidx = (int)(unit / g.Lkv);
+    const int row = flagged[fidx];
+    i = row % g.Lq;
+    p = (row / g.Lq) % g.Hq;
+    r = row / (g.Lq * g.Hq);
+  };
+  uint32_t qph = 0, kph[2] = {0, 0};
+  long long cu = next_live(u0);
+  int buf = 0, qrow = -1;
+  if (cu < u1 && threadIdx.x == 0) {
+    int j, i, p, r, f;
+    decode(cu, j, i, p, r, f);
+    load_block(qs, &tmQ, bar, i * b, p, r);
+    load_block(ks[0], &tmK, bar + 1, j * b, p / g.m, r);
+  }
+  while (cu < u1) {
+    int j, i, p, r, fidx;
+    decode(cu, j, i, p, r, fidx);
+    const long long nu = next_live(cu + 1);
+    int nj = 0, ni = 0, np = 0, nr = 0, nfi = 0;
+    if (nu < u1) decode(nu, nj, ni, np, nr, nfi);
+    const bool new_q = nu < u1 && (ni != i || np != p || nr != r);
+    if (nu < u1 && threadIdx.x == 0) load_block(ks[buf ^ 1], &tmK, bar + 1 + (buf ^ 1), nj * b, np / g.m, nr);
+    if (qrow != fidx) {  // this unit's query block (loaded at the previous unit's end, or first)
+      mbar_wait(bar, qph);
+      qph ^= 1;
+      qrow = fidx;
+    }
+    mbar_wait(bar + 1 + buf, kph[buf]);
+    kph[buf] ^= 1;
+    const Req R = req_of(g, r);
+    const int kt0 = j * b;
+    const unsigned char* kbuf = ks[buf];
+    auto elem16 = [&](const unsigned char* base, int tok, int cc, int k16) -> uint4 {
+      const int rt = tok >> 6, row = tok & 63;
+      return *reinterpret_cast<const uint4*>(base + (rt * NCH + cc) * 8192 + row * 128 + ((k16 ^ (row & 7)) << 4));
+    };
+    for (int idx = threadIdx.x; idx < G * gg; idx += kRecThreads) {
+      const int t = idx % gg, u = idx / gg;
+      const int qtok = u * gg + t;
+      float acc[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[v] = 0.f;
+      const bool qok = i * b + qtok < R.Nq;
+      if (qok) {
+        for (int cc = 0; cc < NCH; ++cc) {
+#pragma unroll 2
+          for (int k16 = 0; k16 < 8; ++k16) {
+            float xf[8];
+            bf16x8_f32(elem16(qs, qtok, cc, k16), xf);
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              if (v >= G) break;
+              float yf[8];
+              bf16x8_f32(elem16(kbuf, v * gg + t, cc, k16), yf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[v] = __fmaf_rn(xf[e], yf[e], acc[v]);
+            }
+          }
+        }
+      }
+      for (int v = 0; v < G; ++v) {
+        const bool ok = qok && kt0 + v * gg + t < R.Nkv;  // padding tokens: exact zero dot
+        tokdot[(u * G + v) * gg + t] = ok ? acc[v] : 0.0f;
+      }
+    }
+    __syncthreads();  // tokdot complete; buffer buf and the query block are free again
+    if (new_q && threadIdx.x == 0) load_block(qs, &tmQ, bar, ni * b, np, nr);
+    if (threadIdx.x < G * G) {
+      const int uv = threadIdx.x, u = uv / G, v = uv % G;
+      float a = 0.0f;
+      for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[uv * gg + t]);  // ascending t
+      const bool valid = i * b + u * gg < R.Nq && j * b + v * gg < R.Nkv;  // padding-only groups (R3)
+      pairtot[uv] = valid ? a : -INFINITY;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mx = -INFINITY;  // Eq. 10
+      for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
+      S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = mx;
+    }
+    __syncthreads();  // tokdot / pairtot reused by the next unit
+    buf ^= 1;
+    cu = nu;
+  }
+}
+
 // vLLM pages -> contiguous [B][Hkv][Nkv][D] (Stage-1 FLATTEN groups span several pages; the gathered
 // copy lets one TMA box cover a whole group row).  One thread per 16 bytes.
 __global__ void __launch_bounds__(256) k_paged_gather(Geom g, const uint4* __restrict__ kc, const int32_t* __restrict__ pt,
@@ -345,11 +597,42 @@ void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, 
 }
 
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st) {
+                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st,
+                          const CUtensorMap* tmQ, const CUtensorMap* tmK) {
   (void)pt;
   if (g.G * g.G > kRecThreads) return -1;
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
+  static const int mode = [] {
+    const char* e = getenv("BFLA_RECOMPUTE");  // experiments: 0 auto (TMA), 1 global loads, 2 bulk rows
+    return e ? atoi(e) : 0;
+  }();
+  {
+    const size_t smem_t = (size_t)3 * g.b * g.D * 2 + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4 + 1024;
+    if (mode == 0 && tmQ && tmK && g.D == 128 && g.G <= 8 && g.b % 64 == 0 && smem_t <= 226 * 1024) {
+      auto kern = k_s1_recompute_tma<128>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
+      kern<<<num_sms, kRecThreads, smem_t, st>>>(*tmQ, *tmK, g, flagged, n_flagged, flag_thr, S);
+      count_launch();
+      return (int)cudaGetLastError();
+    }
+  }
+  // staged variant: K block + two query groups (padded rows) + token dots
+  const size_t pitch = (size_t)g.D * 2 + 16;
+  const size_t smem_s = ((size_t)g.b + 2 * g.g) * pitch + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4;
+  if (mode != 1 && smem_s <= 226 * 1024 && (g.qs2 % 8) == 0 && (g.kvs2 % 8) == 0) {
+    auto gs = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRecThreads, smem_s);
+      kern<<<num_sms * (per_sm > 0 ? per_sm : 1), kRecThreads, smem_s, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
+    };
+    if (g.D == 128) gs(k_s1_recompute_smem<128>);
+    else if (g.D == 256) gs(k_s1_recompute_smem<256>);
+    else return -1;
+    count_launch();
+    return (int)cudaGetLastError();
+  }
   const int smem = (g.G * g.G * g.g + g.G * g.G) * 4;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
