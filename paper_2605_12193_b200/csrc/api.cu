@@ -292,16 +292,20 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       gk.kvs1 = (long long)g.Nkv * g.D;
       gk.kvs0 = (long long)g.Hkv * g.Nkv * g.D;
     }
-    // norms (HBM-bound) run on a side stream concurrently with the tensor-core scores; joined before
-    // the certified selection that reads them
+    // query-group norms come from the scores kernel (Gram diagonal, no extra HBM bytes); key-group
+    // norms (HBM-bound, K only) run on a side stream concurrently; joined before the selection
+    static const bool q_norms_separate = [] {
+      const char* e = getenv("BFLA_QNORM_KERNEL");  // A/B: 1 = query norms in the norm kernel
+      return e && atoi(e) == 1;
+    }();
     SideStream* ss = side_stream();
     if (ss) {
       cudaEventRecord(ss->fork, st);
       cudaStreamWaitEvent(ss->s, ss->fork, 0);
-      launch_block_norms(gk, P->q, kc, qn, kn, ss->s);
+      launch_block_norms(gk, P->q, kc, qn, kn, ss->s, q_norms_separate);
       cudaEventRecord(ss->join, ss->s);
     } else {
-      launch_block_norms(gk, P->q, kc, qn, kn, st);
+      launch_block_norms(gk, P->q, kc, qn, kn, st, q_norms_separate);
     }
     CUtensorMap tmA, tmB;
     bfla_status s;
@@ -317,7 +321,8 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, (uint32_t)kTcTileN, 1, 1};
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
-    if (launch_tc_scores(gk, tmA, tmB, S, st)) return fail(BFLA_ERR_CUDA, "tc scores launch failed");
+    if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st))
+      return fail(BFLA_ERR_CUDA, "tc scores launch failed");
     cudaMemsetAsync(nflag, 0, sizeof(int32_t), st);
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);
     const int sms = num_sms_current();

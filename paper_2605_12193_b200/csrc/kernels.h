@@ -25,8 +25,12 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
 constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
-int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, cudaStream_t st);
-void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st);
+// qn (optional): the scores kernel also writes the query-group norm bounds (Gram diagonal)
+int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
+                     cudaStream_t st);
+// with_q = false: key-group norms only (the scores kernel wrote the query norms)
+void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st,
+                        bool with_q = true);
 // tmQ / tmK (optional): {D, N, H, B} maps with 64 x 64 SW128 boxes for the TMA-staged variant
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
                           const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st,

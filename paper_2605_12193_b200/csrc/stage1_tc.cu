@@ -35,9 +35,9 @@ constexpr int SMEM = ST * (ABYTES + BBYTES) + 2 * ST * 8 + 8 + 16 + 1024;
 // (reads Q and K once); it runs on a side stream next to the tensor-core scores.
 __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloat16* __restrict__ q,
                                                         const __nv_bfloat16* __restrict__ k, float* __restrict__ qn,
-                                                        float* __restrict__ kn) {
+                                                        float* __restrict__ kn, int with_q) {
   __shared__ float part[8];
-  const long long u = blockIdx.x;
+  const long long u = blockIdx.x + (with_q ? 0 : (long long)g.B * g.Hq * g.Lq);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long nq = (long long)g.B * g.Hq * g.Lq;
   const bool isq = u < nq;
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
   const int blk = (int)(w % L), hh = (int)((w / L) % H), r = (int)(w / ((long long)L * H));
   const Req R = req_of(g, r);
   const int N = isq ? R.Nq : R.Nkv;
-  const int vec_per_tok = g.D / 8;
+  const int vec_per_tok = g.D / 8;  // 16 or 32 (head_dim 128 / 256)
+  const int vsh = vec_per_tok == 16 ? 4 : 5;
   const int G = g.G <= 8 ? g.G : 8, parts = 8 / G;
   float acc = 0.f;
   for (int grp = warp % G; grp < g.G; grp += G) {  // G > 8 (not built for FLATTEN) stays correct
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
         const int x = x0 + e * 32;
         raw[e] = make_uint4(0, 0, 0, 0);
         if (x < nvec) {
-          const int t = ta + x / vec_per_tok, c = (x % vec_per_tok) * 8;
+          const int t = ta + (x >> vsh), c = (x & (vec_per_tok - 1)) * 8;
           raw[e] = __ldg(reinterpret_cast<const uint4*>(base + (long long)t * ts + c));
         }
       }
@@ -106,9 +107,16 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
 // groups); causally dead tiles exit.  Warp 0: TMA producer; warp 1: MMA issuer; warp 2: TMEM alloc;
 // warps 4-7: epilogue (thread = query group row): max over the G key groups of each KV block in
 // registers, max over the G query groups of each query block by shuffles (Eq. 10).
+//
+// Query-group norms for the certification come out of the same kernel: the CTAs of the
+// first N tile (nt = 0, every query group) also accumulate A A^T (the query tile against itself,
+// M128 x N128, into TMEM columns 256-383) from the A stages already in shared memory — no extra bytes
+// from L2 — and read its diagonal ||x_u||^2 (fp32 tensor-core sum of exact bf16 squares: relative
+// error <= 2(n/16)u, far inside the 2^-10 slack).  Only the K norms remain for k_s1_block_norms.
 __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, Geom g,
-                                                         float* __restrict__ S, int n_mt, int n_nt) {
+                                                         float* __restrict__ S, int n_mt, int n_nt,
+                                                         float* __restrict__ qn) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ABYTES + BBYTES));
@@ -137,7 +145,11 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<TN>(tslot);
+  const bool qduty = qn != nullptr && nt == 0;  // uniform over the CTA
+  if (warp == 2) {
+    if (qduty) tmem_alloc<2 * TN>(tslot);
+    else tmem_alloc<TN>(tslot);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -154,6 +166,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     }
   } else if (warp == 1) {  // converged warp, one elected lane issues (see umma_f16_ss_warp)
     constexpr uint32_t idesc = idesc_bf16(TM, TN, 0, 0);
+    constexpr uint32_t idesc_g = idesc_bf16(TM, TM, 0, 0);  // Gram A A^T
     const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
     for (int kk = 0; kk < nk; ++kk) {
       const int s = kk % ST;
@@ -163,6 +176,11 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 #pragma unroll
       for (int k16 = 0; k16 < TK / 16; ++k16)
         umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk | k16) ? 1u : 0u);
+      if (qduty) {
+#pragma unroll
+        for (int k16 = 0; k16 < TK / 16; ++k16)
+          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_g, (kk | k16) ? 1u : 0u);
+      }
       umma_commit_warp(empty + s);
     }
     umma_commit_warp(done);
@@ -173,6 +191,19 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     tc_fence_after();
     const int grow = mt * TM + row;           // global query group of head p
     const int ib = grow / g.G, u = grow % g.G;
+    if (qduty) {
+      // ||x_row||^2 = (A A^T)[row][row]: this warp's 32 lanes x columns [32 lg, 32 lg + 32)
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
+      tmem_wait_ld();
+      float sq = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e == lane) sq = v[e];
+      float mx = sqrtf(fmaxf(sq, 0.f));
+      for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
+    }
     const bool uvalid = (long long)grow * g.g < R.Nq;  // padding-only groups never take the max (R3)
     long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
@@ -197,7 +228,8 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<TN>(tmem);
+    if (qduty) tmem_dealloc<2 * TN>(tmem);
+    else tmem_dealloc<TN>(tmem);
   }
 }
 
@@ -577,22 +609,24 @@ void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, v
 
 size_t tc_scores_smem() { return SMEM; }
 
-int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, cudaStream_t st) {
+int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
+                     cudaStream_t st) {
   const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
   const int n_mt = (ngq + TM - 1) / TM, n_nt = (ngk + TN - 1) / TN;
   const long long ctas = (long long)g.B * g.Hq * n_mt * n_nt;
   if (ctas <= 0 || ctas > 0x7fffffff) return -1;
   cudaError_t e = cudaFuncSetAttribute(k_s1_tc_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return (int)e;
-  k_s1_tc_scores<<<(int)ctas, 256, SMEM, st>>>(tmA, tmB, g, S, n_mt, n_nt);
+  k_s1_tc_scores<<<(int)ctas, 256, SMEM, st>>>(tmA, tmB, g, S, n_mt, n_nt, qn);
   count_launch();
   return (int)cudaGetLastError();
 }
 
-void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st) {
-  const long long ctas = (long long)g.B * g.Hq * g.Lq + (long long)g.B * g.Hkv * g.Lkv;
+void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st,
+                        bool with_q) {
+  const long long ctas = (with_q ? (long long)g.B * g.Hq * g.Lq : 0) + (long long)g.B * g.Hkv * g.Lkv;
   k_s1_block_norms<<<(int)ctas, 256, 0, st>>>(g, static_cast<const __nv_bfloat16*>(q),
-                                                                     static_cast<const __nv_bfloat16*>(k), qn, kn);
+                                              static_cast<const __nv_bfloat16*>(k), qn, kn, with_q ? 1 : 0);
   count_launch();
 }
 

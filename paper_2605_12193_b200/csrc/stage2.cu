@@ -17,12 +17,26 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+// Exact divisibility test chi mod eta == 0 without a 64-bit division (Hacker's Delight 10-17): with
+// eta = e0 * 2^k, e0 odd and e0_inv its inverse mod 2^64, x is a multiple of eta iff
+// rotr(x * e0_inv, k) <= floor((2^64 - 1) / eta).  (A runtime 64-bit urem is ~100 instructions per
+// tile; this is a multiply and a compare.)
+struct Div64 {
+  uint64_t inv, lim;
+  int k;
+};
+__device__ __forceinline__ bool divisible(uint64_t x, const Div64& d) {
+  const uint64_t y = x * d.inv;
+  const uint64_t r = d.k ? ((y >> d.k) | (y << (64 - d.k))) : y;
+  return r <= d.lim;
+}
+
 // One warp per (request r, KV head h, query tile i).  Labels (precedence mass > sink > band >
 // stride > random, R13): 1 mass (Eq. 20), 2 sink (Eq. 22), 3 band (Eq. 21), 4 stride (Eq. 24),
 // 5 random (Eq. 25); 0 = dropped or non-causal.  The kept list of row (r,h,i) is written in
 // ascending j at its closed-form causal offset, so rows need no global scan.
 __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t* __restrict__ coarse,
-                                                          int n_sink, int n_local, int eta, double rho,
+                                                          int n_sink, int n_local, int eta, Div64 deta, double rho,
                                                           uint64_t seed, uint32_t* __restrict__ tile_bits,
                                                           int32_t* __restrict__ list, int32_t* __restrict__ count,
                                                           uint8_t* __restrict__ label,
@@ -67,7 +81,7 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
         lab = 3;
       } else {
         const uint64_t key = ((uint64_t)(uint32_t)i << 32) | (uint64_t)(uint32_t)j;
-        if (eta > 0 && mix64(key ^ seed) % (uint64_t)eta == 0) {
+        if (eta > 0 && divisible(mix64(key ^ seed), deta)) {
           lab = 4;
         } else if (rho > 0.0) {
           const uint64_t z = mix64(mix64(key ^ seed ^ 0xD1B54A32D192ED03ULL) ^ (hglob * 0x9E3779B97F4A7C15ULL));
@@ -102,8 +116,21 @@ void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int
                           unsigned long long* stats, cudaStream_t st) {
   const long long rows = (long long)g.B * g.Hkv * g.Tq;
   const int blocks = (int)((rows + 7) / 8);
-  k_s2_expand_rescue<<<blocks, 256, 0, st>>>(g, coarse, n_sink, n_local, eta, rho, seed, tile_bits, list, count,
-                                               label, stats);
+  Div64 d{1, ~0ull, 0};
+  if (eta > 0) {
+    uint64_t e0 = (uint64_t)eta;
+    d.k = 0;
+    while (!(e0 & 1)) {
+      e0 >>= 1;
+      ++d.k;
+    }
+    uint64_t inv = e0;  // Newton: each step doubles the correct low bits (e0 * e0 = 1 mod 8 to start)
+    for (int it = 0; it < 6; ++it) inv *= 2 - e0 * inv;
+    d.inv = inv;
+    d.lim = ~0ull / (uint64_t)eta;
+  }
+  k_s2_expand_rescue<<<blocks, 256, 0, st>>>(g, coarse, n_sink, n_local, eta, d, rho, seed, tile_bits, list,
+                                               count, label, stats);
   count_launch();
 }
 

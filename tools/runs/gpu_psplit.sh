@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/psplit_tests.txt 2>&1
+echo "rc=$?" >> gpurun_out/psplit_tests.txt
+for rep in 1 2; do for v in "" old; do
+BFLA_LIB_VARIANT=$v timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/psplit_${v:-new}_$rep.json 2>&1
+done; done
+timeout 300 python tools/attn_trace.py --dense --out gpurun_out/trace_psplit.json > gpurun_out/trace_psplit.txt 2>&1
