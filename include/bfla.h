@@ -59,6 +59,11 @@ enum { BFLA_SELECT_MASS = 0, BFLA_SELECT_RATIO = 1 };
    (used when Q/K token rows are contiguous, n_q and n_kv are multiples of g, and kept_mass is not
    requested; otherwise CANONICAL); CANONICAL = every score on the fp32 FMA pipes in canonical order. */
 enum { BFLA_SCORES_AUTO = 0, BFLA_SCORES_CANONICAL = 1 };
+/* Mask groups: PER_KV_HEAD (default) ORs the m query heads' Stage-1 masks into one mask per KV head
+   (R8; enables GQA packing in the prefill kernel); PER_Q_HEAD keeps Eq. 18 literal — one mask per
+   query head p, Stage 2 (Eq. 19-26) per query head, psi (Eq. 25) indexed by the global query head —
+   and the mask buffers then have h_q rows where the comments below say h_kv. */
+enum { BFLA_MASK_PER_KV_HEAD = 0, BFLA_MASK_PER_Q_HEAD = 1 };
 
 /* One attention layer call: Q/K/V in the paper's head-first layout (Eq. 2), GQA m = h_q / h_kv
    (Eq. 3), head group H_h = {h m, ..., h m + m - 1} (Eq. 8); the batch index is the paper's
@@ -110,6 +115,7 @@ typedef struct {
     float rho;          /* random-rescue probability (Eq. 25), [0, 1]                                  */
     uint64_t seed;      /* s of Eq. 24-25                                                               */
     int32_t scores_path; /* BFLA_SCORES_* (FLATTEN only; MEAN is always canonical)                      */
+    int32_t mask_groups; /* BFLA_MASK_* (0 = per KV head, the default)                                  */
 } bfla_config;
 
 /* Statistics, accumulated with integer atomics (values are order independent). */

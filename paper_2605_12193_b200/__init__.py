@@ -15,14 +15,14 @@ from typing import Optional
 import torch
 
 from . import _lib
-from ._lib import (KV_CONTIGUOUS, KV_PAGED, POOL_FLATTEN, POOL_MEAN, SCORES_AUTO, SCORES_CANONICAL, SELECT_MASS,
-                   SELECT_RATIO, bfla_config,
+from ._lib import (KV_CONTIGUOUS, KV_PAGED, MASK_PER_KV_HEAD, MASK_PER_Q_HEAD, POOL_FLATTEN, POOL_MEAN, SCORES_AUTO,
+                   SCORES_CANONICAL, SELECT_MASS, SELECT_RATIO, bfla_config,
                    bfla_mask, bfla_problem, bfla_stats, check, lib)
 
 __all__ = ["Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
            "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill", "bfla_prefill",
            "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
-           "SCORES_CANONICAL"]
+           "SCORES_CANONICAL", "MASK_PER_KV_HEAD", "MASK_PER_Q_HEAD"]
 
 
 @dataclasses.dataclass
@@ -41,10 +41,11 @@ class Config:
     rho: float = 0.0
     seed: int = 0
     scores: int = SCORES_AUTO
+    mask_groups: int = MASK_PER_KV_HEAD  # MASK_PER_Q_HEAD: Eq. 18 literal, one mask per query head
 
     def c(self) -> bfla_config:
         return bfla_config(self.b, self.g, self.T, self.pool, self.select, self.gamma, self.keep_ratio,
-                           self.n_sink, self.n_local, self.eta, self.rho, self.seed, self.scores)
+                           self.n_sink, self.n_local, self.eta, self.rho, self.seed, self.scores, self.mask_groups)
 
 
 @dataclasses.dataclass
@@ -134,6 +135,8 @@ class Mask:
     def __init__(self, problem: Problem, cfg: Config, labels: bool = False, kept_mass: bool = False,
                  stats: bool = True):
         B, Hq, Hkv, Nq, Nkv, _ = problem.shape
+        if cfg.mask_groups == MASK_PER_Q_HEAD:
+            Hkv = Hq  # one mask group per query head
         dev = "cuda"
         cd = lambda a, b: -(-a // b)
         Lq, Lkv, Tq, Tkv = cd(Nq, cfg.b), cd(Nkv, cfg.b), cd(Nq, cfg.T), cd(Nkv, cfg.T)

@@ -24,6 +24,7 @@ KV_CONTIGUOUS, KV_PAGED = 0, 1
 POOL_FLATTEN, POOL_MEAN = 0, 1
 SELECT_MASS, SELECT_RATIO = 0, 1
 SCORES_AUTO, SCORES_CANONICAL = 0, 1
+MASK_PER_KV_HEAD, MASK_PER_Q_HEAD = 0, 1
 
 i32, i64, f32, u64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_uint64, ctypes.c_void_p
 
@@ -40,7 +41,7 @@ class bfla_problem(ctypes.Structure):
 class bfla_config(ctypes.Structure):
     _fields_ = [("block_b", i32), ("group_g", i32), ("tile_t", i32), ("pool", i32), ("select", i32),
                 ("gamma", f32), ("keep_ratio", f32), ("n_sink", i32), ("n_local", i32), ("eta", i32),
-                ("rho", f32), ("seed", u64), ("scores_path", i32)]
+                ("rho", f32), ("seed", u64), ("scores_path", i32), ("mask_groups", i32)]
 
 
 class bfla_stats(ctypes.Structure):

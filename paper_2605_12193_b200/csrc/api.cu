@@ -119,6 +119,8 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
   g->Hq = P->h_q;
   g->Hkv = P->h_kv;
   g->m = P->h_q / P->h_kv;
+  g->kvdiv = 1;
+  g->Hkv_real = P->h_kv;
   g->D = P->head_dim;
   g->Nq = P->n_q;
   g->Nkv = P->n_kv;
@@ -176,6 +178,15 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
     if (T != 64) return fail(BFLA_ERR_UNSUPPORTED, "tile_t %d not built (64)", T);
     if (cfg->pool == BFLA_POOL_FLATTEN && b / gg > 8)
       return fail(BFLA_ERR_UNSUPPORTED, "G = b/g = %d > 8 not built for FLATTEN", b / gg);
+    if (cfg->mask_groups != BFLA_MASK_PER_KV_HEAD && cfg->mask_groups != BFLA_MASK_PER_Q_HEAD)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "mask_groups");
+    if (cfg->mask_groups == BFLA_MASK_PER_Q_HEAD) {
+      // one mask group per query head (Eq. 18 literal): groups of size 1 over KV head p / m
+      g->kvdiv = g->m;
+      g->Hkv = g->Hq;
+      g->m = 1;
+      g->head_offset = P->head_offset * g->kvdiv;  // psi's global index is the query head's
+    }
   }
   g->b = b;
   g->g = gg;
@@ -230,7 +241,7 @@ static WsLayout ws_layout(const Geom& g) {
   L.nflag = o;
   o += al(16);
   L.kgather = o;
-  if (g.paged) o += al((size_t)g.B * g.Hkv * g.Nkv * g.D * 2);
+  if (g.paged) o += al((size_t)g.B * g.Hkv_real * g.Nkv * g.D * 2);
   L.total = o;
   return L;
 }
@@ -290,7 +301,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       gk.paged = 0;
       gk.kvs2 = g.D;
       gk.kvs1 = (long long)g.Nkv * g.D;
-      gk.kvs0 = (long long)g.Hkv * g.Nkv * g.D;
+      gk.kvs0 = (long long)g.Hkv_real * g.Nkv * g.D;
     }
     // query-group norms come from the scores kernel (Gram diagonal, no extra HBM bytes); key-group
     // norms (HBM-bound, K only) run on a side stream concurrently; joined before the selection
@@ -316,7 +327,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       if ((s = encode_4d(&tmA, P->q, dims, str, box)) != BFLA_OK) return s;
     }
     {
-      const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv, (uint64_t)g.B};
+      const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv_real, (uint64_t)g.B};
       const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
       const uint32_t box[4] = {64, (uint32_t)kTcTileN, 1, 1};
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
@@ -333,7 +344,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     {
       const uint64_t dq[4] = {(uint64_t)g.D, (uint64_t)g.Nq, (uint64_t)g.Hq, (uint64_t)g.B};
       const uint64_t sq[3] = {(uint64_t)g.qs2 * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
-      const uint64_t dk[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv, (uint64_t)g.B};
+      const uint64_t dk[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv_real, (uint64_t)g.B};
       const uint64_t sk[3] = {(uint64_t)gk.kvs2 * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
       const uint32_t box[4] = {64, 64, 1, 1};
       rmaps = encode_4d_quiet(&rq, P->q, dq, sq, box) && encode_4d_quiet(&rk, kc, dk, sk, box);
@@ -383,14 +394,15 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     if (oal && !g.lens && !no_otma && encode_4d_quiet(&maps.o, P->o, dims, ostr, box)) maps.o_ok = 1;
   }
   if (!g.paged) {
-    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv, (uint64_t)g.B};
+    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv_real, (uint64_t)g.B};
     const uint64_t str[3] = {(uint64_t)g.kvs2 * 2, (uint64_t)g.kvs1 * 2, (uint64_t)g.kvs0 * 2};
     const uint32_t box[4] = {64, 64, 1, 1};
     if ((s = encode_4d(&maps.k, P->k, dims, str, box)) != BFLA_OK) return s;
     if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;
   } else {
-    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Hkv, (uint64_t)g.page_size, (uint64_t)g.num_pages};
-    const uint64_t str[3] = {(uint64_t)g.D * 2, (uint64_t)g.Hkv * g.D * 2, (uint64_t)g.page_size * g.Hkv * g.D * 2};
+    const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Hkv_real, (uint64_t)g.page_size, (uint64_t)g.num_pages};
+    const uint64_t str[3] = {(uint64_t)g.D * 2, (uint64_t)g.Hkv_real * g.D * 2,
+                             (uint64_t)g.page_size * g.Hkv_real * g.D * 2};
     const uint32_t box[4] = {64, 1, (uint32_t)g.page_size, 1};
     if ((s = encode_4d(&maps.k, P->k, dims, str, box)) != BFLA_OK) return s;
     if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;

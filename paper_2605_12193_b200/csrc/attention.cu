@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     unsigned char* dst = smem + (kvsel ? C::OFF_V : C::OFF_K) + st * C::KVBYTES;
     const CUtensorMap* map = kvsel ? &tmV : &tmK;
     if (!PAGED) {
-      for (int cc = 0; cc < D / 64; ++cc) tma_load_4d(dst + cc * (BN * 128), map, full, cc * 64, j * BN, it.h, it.r);
+      for (int cc = 0; cc < D / 64; ++cc)
+        tma_load_4d(dst + cc * (BN * 128), map, full, cc * 64, j * BN, it.h / g.kvdiv, it.r);
     } else {
       // vLLM pages: the 64-token tile is BN/ps page boxes of (64 cols x ps rows); a page past the
       // request's last logical page (ragged tail) is replaced by its first page (finite data; those
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         const int lp = j * BN / ps + pc;
         const int phys = __ldg(table + (lp < npl ? lp : 0));
         for (int cc = 0; cc < D / 64; ++cc)
-          tma_load_4d(dst + cc * (BN * 128) + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
+          tma_load_4d(dst + cc * (BN * 128) + pc * ps * 128, map, full, cc * 64, it.h / g.kvdiv, 0, phys);
       }
     }
   };

@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
       const int ntile = two ? 2 : 1;
       if (lane < ntile * (D / 64)) {
         const int hf = lane / (D / 64), cc = lane % (D / 64);
-        tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF, map, full, cc * 64, (hf ? jb : ja) * BN, it.h, it.r);
+        tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF, map, full, cc * 64, (hf ? jb : ja) * BN, it.h / g.kvdiv,
+                    it.r);
       }
     } else {
       // lane = (tile, page of the tile): BN / page_size page boxes of (64 columns x ps rows) per
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
         const int lp = (hf ? jb : ja) * ppt + pc;
         const int phys = __ldg(page_table + (long long)it.r * g.max_pages + (lp < npl ? lp : 0));
         for (int cc = 0; cc < D / 64; ++cc)
-          tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF + pc * ps * 128, map, full, cc * 64, it.h, 0, phys);
+          tma_load_4d(dst + cc * C::CHUNK + hf * C::HALF + pc * ps * 128, map, full, cc * 64, it.h / g.kvdiv, 0,
+                      phys);
       }
     }
   };

@@ -26,6 +26,10 @@ struct Geom {
   // varlen batches (§8 f1): optional device int32 [B][2] = (n_q_r, n_kv_r), each <= (Nq, Nkv).  The
   // fields above are then the padded LAYOUT of every buffer; Req below holds request r's logical dims.
   const int32_t* lens;
+  // mask groups (bfla_config.mask_groups): Hkv / m above are the mask-group count / size; a mask
+  // group h reads KV head h / kvdiv of a tensor with Hkv_real heads (per KV head: kvdiv = 1,
+  // Hkv_real = Hkv; per query head: Hkv = Hq, m = 1, kvdiv = the GQA group size)
+  int kvdiv, Hkv_real;
 };
 
 // Logical dimensions of request r (Eq. 4, 11, 19 with that request's N_q, N_kv).

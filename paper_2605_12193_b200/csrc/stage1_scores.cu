@@ -28,9 +28,10 @@ constexpr int BJ = 16;       // KV blocks per CTA tile
 
 __device__ __forceinline__ const __nv_bfloat16* k_token(const Geom& g, const __nv_bfloat16* k, const int32_t* pt,
                                                         int r, int h, int s) {
+  h /= g.kvdiv;  // mask group -> KV head
   if (!g.paged) return k + (long long)r * g.kvs0 + (long long)h * g.kvs1 + (long long)s * g.kvs2;
   const int page = pt[(long long)r * g.max_pages + s / g.page_size];
-  return k + (((long long)page * g.page_size + s % g.page_size) * g.Hkv + h) * g.D;
+  return k + (((long long)page * g.page_size + s % g.page_size) * g.Hkv_real + h) * g.D;
 }
 
 __device__ __forceinline__ void bf16x8_to_f32(uint4 u, float* f) {

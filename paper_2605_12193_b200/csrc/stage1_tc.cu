@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
     if (ta >= tb) continue;
     const int nvec = (tb - ta) * vec_per_tok;
     const __nv_bfloat16* base = isq ? q + (long long)r * g.qs0 + (long long)hh * g.qs1
-                                    : k + (long long)r * g.kvs0 + (long long)hh * g.kvs1;
+                                    : k + (long long)r * g.kvs0 + (long long)(hh / g.kvdiv) * g.kvs1;
     const long long ts = isq ? g.qs2 : g.kvs2;
     float a8[8];
 #pragma unroll
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
       mbar_arrive_expect_tx(full + s, ABYTES + BBYTES);
       unsigned char* a = smem + s * (ABYTES + BBYTES);
       tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
-      tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h, r);
+      tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h / g.kvdiv, r);
     }
   } else if (warp == 1) {  // converged warp, one elected lane issues (see umma_f16_ss_warp)
     constexpr uint32_t idesc = idesc_bf16(TM, TN, 0, 0);
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
     if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
-    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)h * g.kvs1;
+    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     // chains c = (u, v, t), t fastest: four per thread per pass
     for (int c0 = threadIdx.x * 4; c0 < nch; c0 += kRecThreads * 4) {
       const __nv_bfloat16* xs[4];
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
     if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
-    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)h * g.kvs1;
+    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     const int kt0 = j * b, nkt = min(b, R.Nkv - kt0);  // valid key tokens of the block
     auto stage_q = [&](int u, int buf) {  // warp 0: query group u -> buffer buf
       const int qt0 = i * b + u * gg, nqt = max(0, min(gg, R.Nq - qt0));
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
     int j, i, p, r, f;
     decode(cu, j, i, p, r, f);
     load_block(qs, &tmQ, bar, i * b, p, r);
-    load_block(ks[0], &tmK, bar + 1, j * b, p / g.m, r);
+    load_block(ks[0], &tmK, bar + 1, j * b, p / g.m / g.kvdiv, r);
   }
   while (cu < u1) {
     int j, i, p, r, fidx;
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
     int nj = 0, ni = 0, np = 0, nr = 0, nfi = 0;
     if (nu < u1) decode(nu, nj, ni, np, nr, nfi);
     const bool new_q = nu < u1 && (ni != i || np != p || nr != r);
-    if (nu < u1 && threadIdx.x == 0) load_block(ks[buf ^ 1], &tmK, bar + 1 + (buf ^ 1), nj * b, np / g.m, nr);
+    if (nu < u1 && threadIdx.x == 0) load_block(ks[buf ^ 1], &tmK, bar + 1 + (buf ^ 1), nj * b, np / g.m / g.kvdiv, nr);
     if (qrow != fidx) {  // this unit's query block (loaded at the previous unit's end, or first)
       mbar_wait(bar, qph);
       qph ^= 1;
@@ -585,23 +585,23 @@ __global__ void __launch_bounds__(256) k_paged_gather(Geom g, const uint4* __res
                                                       uint4* __restrict__ out) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int per_tok = g.D / 8;
-  const long long total = (long long)g.B * g.Hkv * g.Nkv * per_tok;
+  const long long total = (long long)g.B * g.Hkv_real * g.Nkv * per_tok;
   if (idx >= total) return;
   const int c = (int)(idx % per_tok);
   long long rest = idx / per_tok;
   const int s = (int)(rest % g.Nkv);
   rest /= g.Nkv;
-  const int h = (int)(rest % g.Hkv);
-  const int r = (int)(rest / g.Hkv);
+  const int h = (int)(rest % g.Hkv_real);
+  const int r = (int)(rest / g.Hkv_real);
   if (g.lens && s >= __ldg(g.lens + 2 * r + 1)) return;  // past this request's KV (no page mapped)
   const long long page = pt[(long long)r * g.max_pages + s / g.page_size];
-  out[idx] = __ldg(kc + ((page * g.page_size + s % g.page_size) * g.Hkv + h) * per_tok + c);
+  out[idx] = __ldg(kc + ((page * g.page_size + s % g.page_size) * g.Hkv_real + h) * per_tok + c);
 }
 
 }  // namespace
 
 void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, void* kout, cudaStream_t st) {
-  const long long total = (long long)g.B * g.Hkv * g.Nkv * (g.D / 8);
+  const long long total = (long long)g.B * g.Hkv_real * g.Nkv * (g.D / 8);
   k_paged_gather<<<(int)((total + 255) / 256), 256, 0, st>>>(g, static_cast<const uint4*>(kcache), pt,
                                                               static_cast<uint4*>(kout));
   count_launch();

@@ -167,6 +167,29 @@ def test_certification_norms(m):
         assert (got <= want * (1 + 2 ** -9) + 1e-6).all(), "norm bound loose"
 
 
+@pytest.mark.parametrize("case", [
+    dict(Nq=1000, Nkv=1500, b=128, paged=0),      # chunked, ragged: canonical SIMT scores
+    dict(Nq=2048, Nkv=2048, b=256, paged=0),      # tensor-core scores + certification + recompute
+    dict(Nq=2048, Nkv=2048, b=256, paged=16),     # paged K/V
+])
+def test_per_query_head_masks(case):
+    """§8 f3: BFLA_MASK_PER_Q_HEAD keeps Eq. 18 literal (one mask per query head, Stage 2 per query
+    head, psi by query head).  Reference: the oracle on K/V repeated per query head, where the OR over
+    a one-head group is that head's own mask; masks bit-exact, O within tolerance."""
+    m = 4
+    prob = workloads.gaussian(41, B=1, Hq=8, Hkv=2, Nq=case["Nq"], Nkv=case["Nkv"], d=128, sigma=0.8)
+    cfg = bf.Config(b=case["b"], g=64, T=64, gamma=0.95, eta=4, rho=0.2, seed=5, mask_groups=bf.MASK_PER_Q_HEAD)
+    gpu = run_gpu(prob, cfg, paged_page=case["paged"])
+    rep = workloads.Problem(q=prob.q, k=prob.k.repeat_interleave(m, dim=1), v=prob.v.repeat_interleave(m, dim=1))
+    ref = oracle_masks(rep, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    assert labels.shape[1] == 8
+    check_lists(gpu, labels, case["Nq"], case["Nkv"], 64)
+    (o_ref, lse_ref), = oracle_attention(rep, labels, 64)
+    compare_o(gpu["o"][0], o_ref, str(case))
+    assert np.abs(gpu["lse"][0].cpu().numpy() - lse_ref).max() <= 1e-3
+
+
 def test_mean_pool_and_keep_ratio():
     prob = workloads.gaussian(21, B=1, Hq=4, Hkv=2, Nq=1500, Nkv=1500, d=128, sigma=1.0)
     for cfg in [bf.Config(b=128, g=64, pool=bf.POOL_MEAN, gamma=0.9),
