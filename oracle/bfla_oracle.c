@@ -214,23 +214,26 @@ void orc_block_softmax_row(const float* S, int n, int C, float* A) {
  * Eq. 16-18: keep-mass selection on one row of probabilities A (n entries,
  * causal[j] marks causal blocks).  Order = (A desc, j asc) (R6); P_r = sequential fp32 prefix;
  * r* = min{r : P_r >= (float)gamma} (R7); if none, or gamma >= 1, all causal blocks are kept.
- * select == RATIO (north_star extension, R9): keep the first ceil(ratio * n_causal) blocks.
- * Outputs keep[j] in {0,1}; returns r*.  *kept_mass = P_{r*}; *p_prev = P_{r*-1} (0 if r*=1);
- * *tie = 1 iff the cut falls between two equal probabilities (reported, R6);
- * *next_j = the first dropped block in sort order (-1 if none).
+ * select == RATIO (north_star extension, R9): keep the first ceil(ratio * n_causal) blocks of the
+ * order (S desc, j asc) when the scores S are given (the block softmax is monotone in S, so this is
+ * the top-k by probability without fp32 underflow ties), else (A desc, j asc).
+ * Outputs keep[j] in {0,1}; returns r*.  *kept_mass = P_{r*} (A summed in the selection order);
+ * *p_prev = P_{r*-1} (0 if r*=1); *tie = 1 iff the cut falls between two equal sort keys (reported,
+ * R6); order_out = the causal blocks in sort order.
  * Pin: S:207-209 examples, mass >= gamma, minimality, monotonicity in gamma.
  * ---------------------------------------------------------------------------------------- */
-int orc_keep_select(const float* A, const uint8_t* causal, int n, int select, float gamma,
-                    float keep_ratio, uint8_t* keep, float* kept_mass, float* p_prev, int* tie,
-                    int* order_out) {
+int orc_keep_select_keyed(const float* A, const float* S, const uint8_t* causal, int n, int select,
+                          float gamma, float keep_ratio, uint8_t* keep, float* kept_mass, float* p_prev,
+                          int* tie, int* order_out) {
+    const float* key = (select == ORC_SELECT_RATIO && S) ? S : A;
     int* ord = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
     int nc = 0;
     for (int j = 0; j < n; ++j)
         if (causal[j]) ord[nc++] = j;
-    /* insertion sort: (A desc, j asc) — stable on the ascending-j input */
+    /* insertion sort: (key desc, j asc) — stable on the ascending-j input */
     for (int a = 1; a < nc; ++a) {
         int x = ord[a], bpos = a - 1;
-        while (bpos >= 0 && A[ord[bpos]] < A[x]) { ord[bpos + 1] = ord[bpos]; --bpos; }
+        while (bpos >= 0 && key[ord[bpos]] < key[x]) { ord[bpos + 1] = ord[bpos]; --bpos; }
         ord[bpos + 1] = x;
     }
     int r = nc;
@@ -252,10 +255,17 @@ int orc_keep_select(const float* A, const uint8_t* causal, int n, int select, fl
     for (int t = 0; t < r; ++t) keep[ord[t]] = 1;
     if (kept_mass) *kept_mass = P;
     if (p_prev) *p_prev = Pp;
-    if (tie) *tie = (r < nc) && (A[ord[r - 1]] == A[ord[r]]);
+    if (tie) *tie = (r < nc) && (key[ord[r - 1]] == key[ord[r]]);
     if (order_out) memcpy(order_out, ord, sizeof(int) * (size_t)nc);
     free(ord);
     return r;
+}
+
+int orc_keep_select(const float* A, const uint8_t* causal, int n, int select, float gamma,
+                    float keep_ratio, uint8_t* keep, float* kept_mass, float* p_prev, int* tie,
+                    int* order_out) {
+    return orc_keep_select_keyed(A, NULL, causal, n, select, gamma, keep_ratio, keep, kept_mass, p_prev, tie,
+                                 order_out);
 }
 
 /* ------------------------------------------------------------------------------------------
@@ -283,7 +293,7 @@ void orc_select(const float* S, int Hq, int Hkv, int Nq, int Nkv, int C, int b, 
             uint8_t* keep = mass + ((size_t)p * Lq + i) * Lkv;
             float km, pp;
             int tt;
-            int r = orc_keep_select(A, causal, Lkv, select, gamma, keep_ratio, keep, &km, &pp, &tt, ord);
+            int r = orc_keep_select_keyed(A, s, causal, Lkv, select, gamma, keep_ratio, keep, &km, &pp, &tt, ord);
             int nc = 0;
             for (int j = 0; j < Lkv; ++j) nc += causal[j];
             size_t row = (size_t)p * Lq + i;

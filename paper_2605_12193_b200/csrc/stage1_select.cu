@@ -54,6 +54,7 @@ struct RowResult {
   float P;
   bool tie, certified;
   float M, dmax;  // fast row max and largest score-error bound (mode 1)
+  float s_cut;    // RATIO: fast score of the last kept block (mode 1)
 };
 
 __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int nc, float c_alpha, int select,
@@ -72,14 +73,25 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
   Z = __shfl_sync(0xffffffffu, Z, 0);
   __syncwarp();
-  // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j.  Built back to front so the
-  // float area (aliasing the low half of the key array) is read before it is overwritten.
+  // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j (MASS, R6).  RATIO (R9) ranks
+  // by the score instead — the block softmax is monotone in S, so this is the top-k by probability
+  // without the ties fp32 underflow of A would create: (order-preserving bits of S << 32) | ~j.
+  // Built back to front so the float area (aliasing the low half of the key array) is read before
+  // it is overwritten.
+  const bool by_score = select == 1;
   for (int j0 = ((nc - 1) / 32) * 32; j0 >= 0; j0 -= 32) {
     const int j = j0 + lane;
-    float a = 0.0f;
-    if (j < nc) a = __fdiv_rn(e[j], Z);
+    uint32_t hi = 0u;
+    if (j < nc) {
+      if (by_score) {
+        const uint32_t u = __float_as_uint(s[j]);
+        hi = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      } else {
+        hi = __float_as_uint(__fdiv_rn(e[j], Z));
+      }
+    }
     __syncwarp();
-    if (j < nc) keys[j] = ((unsigned long long)__float_as_uint(a) << 32) | (unsigned long long)(~(uint32_t)j);
+    if (j < nc) keys[j] = ((unsigned long long)hi << 32) | (unsigned long long)(~(uint32_t)j);
     __syncwarp();
   }
   int target = nc;
@@ -91,14 +103,18 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
   }
   const bool keep_all = (select == 0 && gamma >= 1.0f);
   certify = certify && !keep_all;
-  float P = 0.0f, a_last = 0.0f, P_prev = 0.0f, kept_lo = INFINITY, t_last = 0.0f;
+  float P = 0.0f, a_last = 0.0f, P_prev = 0.0f, kept_lo = INFINITY, t_last = 0.0f, s_last = 0.0f;
+  uint32_t key_last = 0u;
   int nsel = 0;
   while (nsel < nc) {
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
     best = warp_max_u64(best);
     const int jsel = (int)(~(uint32_t)(best & 0xffffffffull));
-    a_last = __uint_as_float((uint32_t)(best >> 32));
+    // A of the extracted block: the key itself (MASS) or recomputed exactly as above (RATIO)
+    a_last = by_score ? __fdiv_rn(exp2_canon(__fmul_rn(__fsub_rn(s[jsel], M), c_alpha)), Z)
+                      : __uint_as_float((uint32_t)(best >> 32));
+    key_last = (uint32_t)(best >> 32);
     P_prev = P;
     P = __fadd_rn(P, a_last);
     ++nsel;
@@ -106,18 +122,19 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
       const float sj = s[jsel];
       kept_lo = fminf(kept_lo, sj - tau * qnorm * knrow[jsel]);
       t_last = (sj - M) * c_alpha;
+      s_last = sj;
     }
     if (lane == 0) keys[jsel] = 0ull;
     __syncwarp();
     if (keep_all) continue;
     if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
   }
-  RowResult res{nsel, P, false, true, M, 0.f};
+  RowResult res{nsel, P, false, true, M, 0.f, 0.f};
   if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
     best = warp_max_u64(best);
-    res.tie = __uint_as_float((uint32_t)(best >> 32)) == a_last;
+    res.tie = (uint32_t)(best >> 32) == key_last;
   }
   if (certify) {
     float drop_hi = -INFINITY, dmax = 0.f;
@@ -132,8 +149,14 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
       dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
     bool ok = true;
-    if (nsel < nc) ok = (kept_lo - drop_hi) * c_alpha > 0x1p-18f;  // order of the cut
-    if (t_last - 2.0f * c_alpha * dmax < -120.0f) ok = false;     // kept block near exp2 underflow
+    if (select == 1) {
+      // RATIO: only the order of the scores at the cut matters (strict separation, with room for the
+      // fp32 rounding of S_f -/+ delta)
+      if (nsel < nc) ok = kept_lo - drop_hi > 0x1p-22f * (fabsf(kept_lo) + fabsf(drop_hi)) + 1e-30f;
+    } else {
+      if (nsel < nc) ok = (kept_lo - drop_hi) * c_alpha > 0x1p-18f;  // order of the cut
+      if (t_last - 2.0f * c_alpha * dmax < -120.0f) ok = false;     // kept block near exp2 underflow
+    }
     if (select == 0) {
       const float eta = 2.0f * 0.6931472f * c_alpha * dmax;
       const float grow = expm1f(eta);
@@ -148,6 +171,7 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     }
     res.certified = ok;
     res.dmax = dmax;
+    res.s_cut = s_last;
   }
   return res;
 }
@@ -228,7 +252,10 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
         if (lane == 0) {
           const int f = atomicAdd(n_flagged, 1);
           flagged[f] = (int32_t)rowid;
-          flag_thr[f] = res.M - 2.0f * res.dmax - 127.0f / c_alpha;
+          // MASS: blocks below thr have canonical logit < -127 (exact zero probability); RATIO: blocks
+          // below thr rank below the canonical k-th score (only the cut's neighbourhood is recomputed)
+          flag_thr[f] = select == 1 ? res.s_cut - 2.0f * res.dmax * (1.0f + 0x1p-10f) - 0x1p-20f * fabsf(res.s_cut)
+                                    : res.M - 2.0f * res.dmax - 127.0f / c_alpha;
         }
       }
       __syncwarp();

@@ -190,6 +190,20 @@ def test_per_query_head_masks(case):
     assert np.abs(gpu["lse"][0].cpu().numpy() - lse_ref).max() <= 1e-3
 
 
+@pytest.mark.parametrize("ratio", [0.05, 0.2, 0.6])
+def test_keep_ratio_fast_path(ratio):
+    """Keep-ratio (R9, ranked by score) on the tensor-core path: certification by the score gap at the
+    cut, recompute of the cut's neighbourhood only; AUTO == CANONICAL == oracle, bit for bit."""
+    prob = workloads.structured(9, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128, block=256)
+    kw = dict(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=ratio)
+    fast = run_gpu(prob, bf.Config(**kw, scores=bf.SCORES_AUTO), lse=False)
+    canon = run_gpu(prob, bf.Config(**kw, scores=bf.SCORES_CANONICAL), lse=False)
+    assert np.array_equal(fast["coarse"], canon["coarse"])
+    assert np.array_equal(fast["labels"], canon["labels"])
+    _check_masks(fast, oracle_masks(prob, bf.Config(**kw)), None)
+    print(f"ratio {ratio}: flagged {fast['stats']['rows_flagged']} of {fast['stats']['rows']}")
+
+
 def test_mean_pool_and_keep_ratio():
     prob = workloads.gaussian(21, B=1, Hq=4, Hkv=2, Nq=1500, Nkv=1500, d=128, sigma=1.0)
     for cfg in [bf.Config(b=128, g=64, pool=bf.POOL_MEAN, gamma=0.9),

@@ -247,6 +247,20 @@ def test_keep_select_spec_examples(orc):
     assert keep.tolist() == [1, 0, 1]
 
 
+def test_keep_ratio_ranks_by_score_through_underflow(orc):
+    # R9: keep-ratio keeps the top-k blocks by probability; the block softmax is monotone in S, so the
+    # exact top-k is the top-k by score even where fp32 probabilities underflow to 0 (where ranking by
+    # the rounded A would fall back to ascending j).  One head, one query block of 4 causal KV blocks.
+    C, b = 128, 16
+    S = np.full((1, 1, 4), -np.inf, np.float32)
+    S[0, 0] = [20000.0, 0.0, 9000.0, 10.0]  # everything but block 0 underflows: t < -126
+    out = orc.select(S, 1, b, 4 * b, C, b, select_mode=orc.SELECT_RATIO, keep_ratio=0.5)
+    assert out["A"][0, 0, 1] == 0.0 and out["A"][0, 0, 2] == 0.0
+    assert out["mass"][0, 0].tolist() == [1, 0, 1, 0]
+    out = orc.select(S, 1, b, 4 * b, C, b, select_mode=orc.SELECT_RATIO, keep_ratio=0.75)
+    assert out["mass"][0, 0].tolist() == [1, 0, 1, 1]
+
+
 def test_keep_ratio(orc):
     A = np.array([0.1, 0.4, 0.2, 0.3], np.float32)
     keep, r, *_ = orc.keep_select(A, select=orc.SELECT_RATIO, keep_ratio=0.5)

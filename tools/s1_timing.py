@@ -14,10 +14,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=32768)
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--ratio", type=float, default=0.0, help="keep-ratio selection (R9) instead of gamma")
 a = ap.parse_args()
 prob = workloads.structured(303, 1, a.hq, 8, a.n, a.n, 128, block=256, theta=5e5, device="cuda")
 o = torch.empty_like(prob.q)
 cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, n_local=8, eta=16, rho=0.0)
+if a.ratio > 0:
+    cfg = bf.Config(b=256, g=64, T=64, select=bf.SELECT_RATIO, keep_ratio=a.ratio, n_local=8, eta=16)
 P = bf.make_problem(prob.q, prob.k, prob.v, o)
 ws = bf.alloc_workspace(P, cfg)
 m = bf.alloc_mask(P, cfg)
@@ -34,5 +37,5 @@ for _ in range(a.reps):
     ts.append(e0.elapsed_time(e1))
 ts.sort()
 st = m.stats_dict()
-print(f"env={ {k: v for k, v in os.environ.items() if k.startswith('BFLA_')} } n={a.n} block_mask ms: median "
+print(f"env={ {k: v for k, v in os.environ.items() if k.startswith('BFLA_')} } n={a.n} ratio={a.ratio} block_mask ms: median "
       f"{ts[len(ts) // 2]:.4f} min {ts[0]:.4f}  flagged {st['rows_flagged']} recomputed {st['rows_recomputed']}")
