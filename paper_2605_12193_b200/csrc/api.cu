@@ -329,7 +329,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     {
       const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv_real, (uint64_t)g.B};
       const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
-      const uint32_t box[4] = {64, (uint32_t)kTcTileN, 1, 1};
+      const uint32_t box[4] = {64, (uint32_t)kTcTileN / 2, 1, 1};  // two boxes per stage (one on diagonal tiles)
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
     if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st))

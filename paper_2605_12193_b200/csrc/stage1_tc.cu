@@ -132,10 +132,13 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
   const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
   const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
+  int nlive = TN;  // key-group columns with any causal block for this M tile: 256, or 128 when the
+                   // tile's second half lies entirely past the causal frontier (diagonal tiles)
   {  // causal skip (Eq. 11-13): smallest j of the N tile vs the largest i of the M tile
     long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
     if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
     if ((long long)nt * BK * g.b > e_last || mt * BQ >= R.Lq) return;
+    if ((long long)(nt * BK + BK / 2) * g.b > e_last) nlive = TN / 2;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -159,13 +162,14 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     for (int kk = 0; kk < nk; ++kk) {
       const int s = kk % ST;
       mbar_wait(empty + s, ((kk / ST) & 1) ^ 1);
-      mbar_arrive_expect_tx(full + s, ABYTES + BBYTES);
+      mbar_arrive_expect_tx(full + s, ABYTES + (nlive == TN ? BBYTES : BBYTES / 2));
       unsigned char* a = smem + s * (ABYTES + BBYTES);
       tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
-      tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h / g.kvdiv, r);
+      tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h / g.kvdiv, r);  // 128-row boxes
+      if (nlive == TN) tma_load_4d(a + ABYTES + BBYTES / 2, &tmB, full + s, kk * TK, nt * TN + TN / 2, h / g.kvdiv, r);
     }
   } else if (warp == 1) {  // converged warp, one elected lane issues (see umma_f16_ss_warp)
-    constexpr uint32_t idesc = idesc_bf16(TM, TN, 0, 0);
+    const uint32_t idesc = nlive == TN ? idesc_bf16(TM, TN, 0, 0) : idesc_bf16(TM, TN / 2, 0, 0);
     constexpr uint32_t idesc_g = idesc_bf16(TM, TM, 0, 0);  // Gram A A^T
     const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
     for (int kk = 0; kk < nk; ++kk) {
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
-    for (int c0 = 0; c0 < TN; c0 += 32) {
+    for (int c0 = 0; c0 < nlive; c0 += 32) {
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
       tmem_wait_ld();

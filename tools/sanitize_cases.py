@@ -1,0 +1,56 @@
+"""Small end-to-end cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel of the
+path — tensor-core Stage 1 with forced recompute (TMA-staged units), canonical SIMT Stage 1, MEAN,
+keep-ratio, per-query-head masks, paged K/V, Stage 2, both attention kernels (d = 128 / 256), dense.
+Run on a GPU box:  compute-sanitizer --tool memcheck python tools/sanitize_cases.py"""
+import os
+import sys
+
+os.environ.setdefault("BFLA_TAU_SCALE", "50")  # force flagged rows so the recompute kernel runs
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2605_12193_b200 as bf  # noqa: E402
+import workloads  # noqa: E402
+
+
+def run(prob, cfg, paged=0):
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o = torch.empty_like(q)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    if paged:
+        kc, vc, pt = workloads.paged(k, v, paged, seed=3, extra_pages=3)
+        P = bf.make_problem(q, kc, vc, o, lse, page_table=pt, n_kv=k.shape[2])
+    else:
+        P = bf.make_problem(q, k, v, o, lse)
+    if cfg is None:
+        bf.bfla_prefill(P, None, None, None)
+    else:
+        ws = bf.alloc_workspace(P, cfg)
+        m = bf.alloc_mask(P, cfg, labels=True)
+        bf.bfla_block_mask(P, cfg, m, ws)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        bf.bfla_sparse_prefill(P, cfg, m, ws)
+    torch.cuda.synchronize()
+    return o
+
+
+def main():
+    g1 = workloads.gaussian(5, B=1, Hq=8, Hkv=2, Nq=2048, Nkv=2048, d=128, sigma=0.8)
+    cases = [
+        ("tc scores + recompute", g1, bf.Config(b=256, g=64, eta=4, rho=0.1), 0),
+        ("keep-ratio", g1, bf.Config(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=0.2), 0),
+        ("per-query-head masks", g1, bf.Config(b=256, g=64, mask_groups=bf.MASK_PER_Q_HEAD), 0),
+        ("paged", g1, bf.Config(b=256, g=64), 16),
+        ("canonical SIMT, ragged chunk", workloads.gaussian(6, B=1, Hq=4, Hkv=1, Nq=1000, Nkv=1500, d=128, sigma=0.8),
+         bf.Config(b=128, g=64), 0),
+        ("MEAN", g1, bf.Config(b=128, g=64, pool=bf.POOL_MEAN), 0),
+        ("d=256", workloads.gaussian(7, B=1, Hq=4, Hkv=2, Nq=1024, Nkv=1024, d=256, sigma=0.8), bf.Config(b=256, g=64), 0),
+        ("dense", g1, None, 0),
+    ]
+    for name, prob, cfg, paged in cases:
+        o = run(prob, cfg, paged)
+        print(f"{name}: ok, |O| max {o.float().abs().max().item():.3f}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
