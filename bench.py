@@ -200,14 +200,15 @@ def run_ours(args, w, rank, world, local_rank):
 
     # ---- dense comparator (same kernel template, all causal tiles; not part of the step) ----
     Pd = bf.make_problem(q, k, v, o) if not w["paged"] else P
+    wsd = bf.alloc_workspace(Pd, None)  # optional for dense: enables dynamic item scheduling
     for _ in range(2):
-        bf.bfla_prefill(Pd, None, None, None)
+        bf.bfla_prefill(Pd, None, None, wsd)
     torch.cuda.synchronize()
     de = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     nd = max(2, min(args.steps, 5))
     de[0].record(st)
     for _ in range(nd):
-        bf.bfla_prefill(Pd, None, None, None)
+        bf.bfla_prefill(Pd, None, None, wsd)
     de[1].record(st)
     torch.cuda.synchronize()
     dense_ms = de[0].elapsed_time(de[1]) / nd

@@ -175,6 +175,9 @@ bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* c
    problem->o (+ lse).  tcgen05/TMEM/TMA kernel, bf16 in, fp32 accumulation, P rounded to bf16. */
 bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                 void* ws, size_t ws_bytes, void* stream);
+/* (ws is optional for bfla_sparse_prefill and for the dense bfla_prefill: when it is given — at least
+   bfla_workspace_size bytes — the kernel schedules its work items dynamically through a counter kept
+   in ws; with ws == NULL it uses a static round-robin order.  Results are identical either way.) */
 
 /* The whole path: Stage 1 -> Stage 2 -> sparse prefill.  config == NULL runs DENSE causal attention
    (Eq. 1, the comparator) with the same kernel.  mask == NULL keeps the mask buffers inside ws. */

@@ -208,7 +208,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
 
 // ---- workspace layout -------------------------------------------------------------------------
 struct WsLayout {
-  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, flagthr, nflag, kgather, total;
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, flagthr, nflag, sched, kgather, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Geom& g) {
@@ -239,6 +239,8 @@ static WsLayout ws_layout(const Geom& g) {
   L.flagthr = o;
   o += al((size_t)g.B * g.Hq * g.Lq * 4);
   L.nflag = o;
+  o += al(16);
+  L.sched = o;  // attention item counter (dynamic scheduling)
   o += al(16);
   L.kgather = o;
   if (g.paged) o += al((size_t)g.B * g.Hkv_real * g.Nkv * g.D * 2);
@@ -374,7 +376,7 @@ static bfla_status run_expand(const Geom& g, const bfla_config* cfg, bfla_mask* 
 }
 
 static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int32_t* list, const int32_t* count,
-                                 int dense, cudaStream_t st) {
+                                 int dense, cudaStream_t st, int32_t* sched = nullptr) {
   AttnMaps maps;
   bfla_status s;
   {
@@ -413,8 +415,15 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     return e && atoi(e) == 1;
   }();
   const int32_t* pt = g.paged ? P->page_table : nullptr;
-  int e = (g.D == 128 && !v1) ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st)
-                              : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st);
+  static const bool no_dyn = [] {
+    const char* e = getenv("BFLA_DYN_SCHED");  // A/B: 0 = static round-robin items
+    return e && atoi(e) == 0;
+  }();
+  if (no_dyn) sched = nullptr;
+  if (sched) cudaMemsetAsync(sched, 0, sizeof(int32_t), st);
+  int e = (g.D == 128 && !v1)
+              ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
+              : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st);
   if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
   return cuda_check("attention launch");
 }
@@ -475,14 +484,16 @@ bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* c
 
 bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                 void* ws, size_t ws_bytes, void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
   if (s != BFLA_OK) return s;
   if (!mask || !mask->tile_list || !mask->tile_count) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask lists are NULL");
-  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream));
+  // the workspace is optional here: with it, items are scheduled dynamically (a counter in ws)
+  const WsLayout L = ws_layout(g);
+  int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
+                                                : nullptr;
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
 }
 
 bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
@@ -491,8 +502,12 @@ bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config,
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
   if (s != BFLA_OK) return s;
-  if (!config) return run_attention(g, problem, nullptr, nullptr, 1, st);  // dense causal (Eq. 1)
   const WsLayout L = ws_layout(g);
+  if (!config) {  // dense causal (Eq. 1); a workspace, if given, enables dynamic item scheduling
+    int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
+                                                  : nullptr;
+    return run_attention(g, problem, nullptr, nullptr, 1, st, sched);
+  }
   if (!ws || ws_bytes < L.total) return fail(BFLA_ERR_WORKSPACE, "workspace too small");
   unsigned char* w = static_cast<unsigned char*>(ws);
   bfla_mask local;
@@ -508,7 +523,8 @@ bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config,
   if ((s = check_mask(g, mask, true, true)) != BFLA_OK) return s;
   if ((s = run_block_mask(g, config, mask, w, problem, st)) != BFLA_OK) return s;
   if ((s = run_expand(g, config, mask, st)) != BFLA_OK) return s;
-  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, st);
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, st,
+                       reinterpret_cast<int32_t*>(w + L.sched));
 }
 
 const char* bfla_status_string(bfla_status status) {

@@ -77,8 +77,9 @@ struct Cfg2 {
   static constexpr int OFF_K = OFF_Q + QS * QBYTES;
   static constexpr int OFF_V = OFF_K + KS * SLOT;
   static constexpr int OFF_BAR = OFF_V + VS * SLOT;
-  static constexpr int NBAR = 2 * QS + 2 * KS + 2 * VS + 4 * NQT;
-  static constexpr int SMEM_TOTAL = OFF_BAR + NBAR * 8 + 16;
+  static constexpr int NBAR = 2 * QS + 2 * KS + 2 * VS + 4 * NQT + 2 * 4;  // + item ring full/empty
+  static constexpr int OFF_RING = OFF_BAR + NBAR * 8 + 16;  // int2 (item index, kept-tile count) x 4
+  static constexpr int SMEM_TOTAL = OFF_RING + 4 * 8;
   static constexpr int THREADS = 128 + 128 * NQT;
   static constexpr int COL_S = 0;    // S_q / P_q at columns [128 q, 128 q + 128)
   static constexpr int COL_O = 256;  // O_q at [256 + 128 q, ...)
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, int otma, Geom g, const int32_t* __restrict__ list,
             const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
-            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC, int opts) {
+            __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC, int opts,
+            int* __restrict__ sched) {
   constexpr bool MAXFIRST = SMX >= 1;
   using C = Cfg2<NQT, PAGED>;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -109,7 +111,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
   uint64_t* p_full = s_full + NQT;     // [NQT]: P_q(s) in TMEM (128 arrivals)
   uint64_t* o_full = p_full + NQT;     // [NQT]: last PV of the item done
   uint64_t* o_free = o_full + NQT;     // [NQT]: epilogue has read O (128 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+  uint64_t* it_full = o_free + NQT;    // [4]: item ring entry published (K producer)
+  uint64_t* it_empty = it_full + 4;    // [4]: entry read by every other role (11 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::QS + 2 * C::KS + 2 * C::VS + 4 * NQT + 8);
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + C::OFF_RING);  // [4][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -130,6 +135,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
       mbar_init(p_full + q, 128);
       mbar_init(o_full + q, 1);
       mbar_init(o_free + q, 128);
+    }
+    for (int e = 0; e < 4; ++e) {
+      mbar_init(it_full + e, 1);
+      mbar_init(it_empty + e, 3 + 4 * NQT);  // warps 1, 2, 3 and the softmax warps
     }
     fence_barrier_init();
   }
@@ -160,11 +169,6 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     if (DENSE) return (int)req_row_count(R, g.T, it.i);
     return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
   };
-  // the next item's kept-tile count, loaded one item ahead so its latency is off the item boundary
-  auto next_count = [&](int idx) -> int {
-    const int nidx = idx + (int)gridDim.x;
-    return nidx < n_items ? row_count(decode_item(g, nidx, NC)) : 0;
-  };
   auto row_list = [&](const Item& it) -> const int32_t* {
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
   };
@@ -172,6 +176,22 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
   // near the diagonal, so the running max settles on the first step and the lazy-max fast path holds
   auto tile_at_c = [&](const int32_t* lst, int cnt, int n) -> int {
     return DENSE ? cnt - 1 - n : __ldg(lst + (cnt - 1 - n));
+  };
+  // Item sequence.  The K producer (furthest ahead) picks items — the CTA's first is blockIdx.x, the
+  // next ones come from a global counter (greedy longest-first list scheduling: items are ordered by
+  // descending row length, so a CTA that finishes early takes the next heaviest item) or, without a
+  // counter, blockIdx.x + k gridDim.x — and publishes (index, kept-tile count) in a 4-entry smem ring;
+  // every other role (one warp at a time) reads the ring in order.  Index -1 ends the sequence.
+  uint32_t ring_n = 0;
+  auto next_item = [&](int& idx, int& cnt) -> bool {
+    const int e = ring_n & 3;
+    mbar_wait(it_full + e, (ring_n >> 2) & 1);
+    idx = ring[2 * e];
+    cnt = ring[2 * e + 1];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(it_empty + e);
+    ++ring_n;
+    return idx >= 0;
   };
 
   // One ring step of K (kvsel = 0) or V (kvsel = 1), issued by a whole warp: lanes fetch the list
@@ -227,18 +247,35 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     // ================================ TMA producer (K) ================================
     {
       uint32_t ks = 0;
-      int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-        const Item it = decode_item(g, idx, NC);
-        const int cnt = cnt_nx;
-        cnt_nx = next_count(idx);
-        if (cnt == 0) continue;
-        const int32_t* lst = DENSE ? nullptr : row_list(it);
-        const int ns = (cnt + 1) / 2;
-        for (int s = 0; s < ns; ++s, ++ks) {
-          load_step(0, ks, lst, cnt, s, it);
-          TRACE(1, 6);
+      int idx = blockIdx.x;
+      for (;;) {
+        const bool live = idx < n_items;
+        const Item it = decode_item(g, live ? idx : 0, NC);
+        const int cnt = live ? row_count(it) : 0;
+        {  // publish (idx, cnt) — or the end marker
+          const int e = ring_n & 3;
+          mbar_wait(it_empty + e, ((ring_n >> 2) & 1) ^ 1);
+          if (lane == 0) {
+            ring[2 * e] = live ? idx : -1;
+            ring[2 * e + 1] = cnt;
+            mbar_arrive(it_full + e);
+          }
+          __syncwarp();
+          ++ring_n;
         }
+        if (!live) break;
+        int nidx = 0;  // the next item, fetched before this one's loads so the atomic's latency hides
+        if (lane == 0) nidx = sched ? (int)gridDim.x + atomicAdd(sched, 1) : idx + (int)gridDim.x;
+        nidx = __shfl_sync(0xffffffffu, nidx, 0);
+        if (cnt > 0) {
+          const int32_t* lst = DENSE ? nullptr : row_list(it);
+          const int ns = (cnt + 1) / 2;
+          for (int s = 0; s < ns; ++s, ++ks) {
+            load_step(0, ks, lst, cnt, s, it);
+            TRACE(1, 6);
+          }
+        }
+        idx = nidx;
       }
     }
   } else if (warp == 2) {
@@ -246,11 +283,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     // Q tile q of the next item is loaded as soon as its smem is free: after the last S_q MMA (STG
     // epilogue) or after O_q, staged through the same smem, has been read by the TMA store.
     uint32_t nit = 0;
-    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int idx, cnt; next_item(idx, cnt);) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = cnt_nx;
-      cnt_nx = next_count(idx);
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
 #pragma unroll
@@ -273,7 +307,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
                         cc * 64, it.i * g.T, it.h * g.m + pl, it.r);
         }
       }
-      if (!(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2 with the next item's Q
+      if (!sched && !(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2: next item's Q
         const Item nx = decode_item(g, idx + gridDim.x, NC);
         for (int q = 0; q < NQT; ++q)
           for (int s = 0; s < hpq; ++s) {
@@ -287,11 +321,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     // ================================ TMA producer (V) ================================
     {
       uint32_t ks = 0;
-      int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      for (int idx, cnt; next_item(idx, cnt);) {
         const Item it = decode_item(g, idx, NC);
-        const int cnt = cnt_nx;
-        cnt_nx = next_count(idx);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const int ns = (cnt + 1) / 2;
@@ -329,11 +360,9 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
       }
       umma_commit_warp(s_full + q);
     };
-    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int idx, cnt; next_item(idx, cnt);) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = cnt_nx;
-      cnt_nx = next_count(idx);
+      (void)it;
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
       const int ns = (cnt + 1) / 2;
@@ -403,11 +432,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     uint32_t st = 0, nit = 0;
-    int cnt_nx = blockIdx.x < n_items ? row_count(decode_item(g, blockIdx.x, NC)) : 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int idx, cnt; next_item(idx, cnt);) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = cnt_nx;
-      cnt_nx = next_count(idx);
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
@@ -693,7 +719,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
 
 template <int NQT, bool PAGED, bool DENSE>
 int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
-              void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st) {
+              void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st, int* sched) {
   static const int smx = [] {
     const char* e = getenv("BFLA_SMX");  // softmax variant (see k_attn2); default 1
     const int v = e ? atoi(e) : 1;
@@ -708,7 +734,7 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
     kern<<<grid, threads, smem, st>>>(maps.q, maps.k, maps.v, maps.o, maps.o_ok, g, list, count, pt,
-                                      static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts);
+                                      static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts, sched);
     count_launch();
     return (int)cudaGetLastError();
   };
@@ -726,14 +752,16 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
 
 // head_dim 128 only (two 32 KB K/V slots per ring stage do not fit next to Q at d = 256).
 int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
-                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st) {
+                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
+                      int* sched) {
   const int hpq = BM / g.T;
   const int nqt = g.m > hpq ? 2 : 1;
   const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
   const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
   if (items == 0) return 0;
   const int n = (int)items;
-#define BFLA_GO2(Q_, P_, X_) return launch2_t<Q_, P_, X_>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
+#define BFLA_GO2(Q_, P_, X_) \
+  return launch2_t<Q_, P_, X_>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st, sched)
   if (nqt == 2) {
     if (g.paged) { if (dense) BFLA_GO2(2, true, true); else BFLA_GO2(2, true, false); }
     else { if (dense) BFLA_GO2(2, false, true); else BFLA_GO2(2, false, false); }
