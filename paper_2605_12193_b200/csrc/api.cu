@@ -423,7 +423,7 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
   if (sched) cudaMemsetAsync(sched, 0, sizeof(int32_t), st);
   int e = (g.D == 128 && !v1)
               ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
-              : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st);
+              : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched);
   if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
   return cuda_check("attention launch");
 }

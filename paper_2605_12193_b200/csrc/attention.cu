@@ -47,9 +47,10 @@ struct Cfg {
   static constexpr int OFF_V = OFF_K + KST * KVBYTES;
   static constexpr int OFF_P = OFF_V + VST * KVBYTES;
   static constexpr int OFF_BAR = OFF_P + 2 * NQT * PBYTES;  // P double buffer per Q tile
-  static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 10 * NQT;
+  static constexpr int NBAR = 2 + 2 * KST + 2 * VST + 10 * NQT + 2 * 4;  // + item ring full/empty
   static constexpr int OFF_RED = OFF_BAR + ((NBAR * 8 + 16 + 127) / 128) * 128;  // row-max exchange
-  static constexpr int SMEM_TOTAL = OFF_RED + (SPL == 2 ? NQT * 2 * 2 * 128 * 4 : 0);  // [NQT][parity][half][row]
+  static constexpr int OFF_RING = OFF_RED + (SPL == 2 ? NQT * 2 * 2 * 128 * 4 : 0);  // [NQT][parity][half][row]
+  static constexpr int SMEM_TOTAL = OFF_RING + 4 * 8;  // item ring: (index, kept-tile count) x 4
   static constexpr int THREADS = 128 + 128 * SPL * NQT;  // 4 control warps + SPL softmax warpgroups per Q tile
   // TMEM columns: S_q double buffer at 128 q + 64 b (d=128) / 64 b (d=256); O_q from column 256
   static constexpr int COL_S = 0;
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     k_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
            const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
-           __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC) {
+           __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC,
+           int* __restrict__ sched) {
   using C = Cfg<D, NQT, SPL>;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
@@ -78,7 +80,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
   uint64_t* p_free = p_full + 2 * NQT;     // [NQT][2]: PV_q(n) done (P buffer n % 2 free, O includes PV(n))
   uint64_t* o_full = p_free + 2 * NQT;     // [NQT]: last PV of the item done
   uint64_t* o_free = o_full + NQT;         // [NQT]: epilogue has read O (128 arrivals)
+  uint64_t* it_full = o_free + NQT;        // [4]: item ring entry published (Q/K producer)
+  uint64_t* it_empty = it_full + 4;        // [4]: entry read by the V producer, the MMA warp, softmax warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
+  volatile int* ring = reinterpret_cast<volatile int*>(smem + C::OFF_RING);  // [4][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -102,6 +107,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       mbar_init(o_full + q, 1);
       mbar_init(o_free + q, 128 * SPL);
     }
+    for (int e = 0; e < 4; ++e) {
+      mbar_init(it_full + e, 1);
+      mbar_init(it_empty + e, 2 + 4 * NQT * SPL);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -121,6 +130,24 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
     if (DENSE) return (int)req_row_count(R, g.T, it.i);
     return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+  };
+  // Item sequence (as attention2.cu): the Q/K producer takes the CTA's first item statically and the
+  // next ones from a global counter (longest-first greedy list scheduling) or round-robin without one,
+  // and publishes (index, kept-tile count) in a 4-entry smem ring that every other role reads in order.
+  uint32_t ring_n = 0;
+  auto next_item = [&](int& idx, int& cnt, bool whole_warp) -> bool {
+    const int e = ring_n & 3;
+    mbar_wait(it_full + e, (ring_n >> 2) & 1);
+    idx = ring[2 * e];
+    cnt = ring[2 * e + 1];
+    if (whole_warp) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(it_empty + e);
+    } else {
+      mbar_arrive(it_empty + e);
+    }
+    ++ring_n;
+    return idx >= 0;
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
@@ -159,10 +186,24 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     // ================================ TMA producer (Q, K) ================================
     if (lane == 0) {
       uint32_t kv = 0, nit = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-        const Item it = decode_item(g, idx, NC);
-        const int cnt = row_count(it);
-        if (cnt == 0) continue;
+      for (int idx = blockIdx.x;;) {
+        const bool live = idx < n_items;
+        const Item it = decode_item(g, live ? idx : 0, NC);
+        const int cnt = live ? row_count(it) : 0;
+        {  // publish (idx, cnt) — or the end marker
+          const int e = ring_n & 3;
+          mbar_wait(it_empty + e, ((ring_n >> 2) & 1) ^ 1);
+          ring[2 * e] = live ? idx : -1;
+          ring[2 * e + 1] = cnt;
+          mbar_arrive(it_full + e);
+          ++ring_n;
+        }
+        if (!live) break;
+        const int nidx = sched ? (int)gridDim.x + atomicAdd(sched, 1) : idx + (int)gridDim.x;
+        if (cnt == 0) {
+          idx = nidx;
+          continue;
+        }
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const uint32_t my_it = nit++;
         // Q: for each tile q and head slot s, D/64 boxes of (64 cols x 64 rows)
@@ -182,8 +223,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
                           cc * 64, it.i * g.T, p, it.r);
           }
         // warm L2 with the next item's Q (it is read from HBM exactly once)
-        if (idx + (int)gridDim.x < n_items) {
-          const Item nx = decode_item(g, idx + gridDim.x, NC);
+        if (nidx < n_items) {
+          const Item nx = decode_item(g, nidx, NC);
           for (int q = 0; q < NQT; ++q)
             for (int s = 0; s < hpq; ++s) {
               const int pl = nx.c * heads_in_chunk + q * hpq + s;
@@ -196,6 +237,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
           const int j = DENSE ? n : lst[n];
           load_kv(0, kv, j, it);
         }
+        idx = nidx;
       }
     }
   } else if (warp == 3) {
@@ -204,9 +246,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     // queue behind a V slot that is still being read.
     if (lane == 0) {
       uint32_t kv = 0;
-      for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+      for (int idx, cnt; next_item(idx, cnt, false);) {
         const Item it = decode_item(g, idx, NC);
-        const int cnt = row_count(it);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         for (int n = 0; n < cnt; ++n, ++kv) load_kv(1, kv, DENSE ? n : lst[n], it);
@@ -237,9 +278,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       }
       umma_commit_warp(s_full + 2 * q + (tcn & 1));
     };
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
-      const Item it = decode_item(g, idx, NC);
-      const int cnt = row_count(it);
+    for (int idx, cnt; next_item(idx, cnt, true);) {
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
       mbar_wait(q_full, my_it & 1);
@@ -313,9 +352,8 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       if (SPL == 2) asm volatile("bar.sync %0, 256;" ::"r"(bar_id) : "memory");
     };
     uint32_t tc = 0, nit = 0;
-    for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    for (int idx, cnt; next_item(idx, cnt, true);) {
       const Item it = decode_item(g, idx, NC);
-      const int cnt = row_count(it);
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
@@ -477,14 +515,14 @@ size_t attn_smem_bytes(int D, int nqt) {
 template <int D, int NQT, bool PAGED, bool DENSE, int SPL>
 static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
                     const int32_t* pt, void* o, float* lse, int n_items, int hpq, int NC, int num_sms,
-                    cudaStream_t st) {
+                    cudaStream_t st, int* sched) {
   using C = Cfg<D, NQT, SPL>;
   auto kern = k_attn<D, NQT, PAGED, DENSE, SPL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;
   kern<<<grid, C::THREADS, C::SMEM_TOTAL, st>>>(maps.q, maps.k, maps.v, g, list, count, pt,
-                                          static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC);
+                                          static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, sched);
   count_launch();
   return (int)cudaGetLastError();
 }
@@ -492,7 +530,8 @@ static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, co
 // Rows of one item: NQT 128-row tiles, each holding hpq = 128/T heads of T rows; NQT = 2 when the
 // group has more than one tile of rows and TMEM allows (d = 128: 2 x (64 S + 128 O) columns).
 int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
-                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st) {
+                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
+                     int* sched) {
   const int hpq = BM / g.T;
   const int nqt = (g.D == 128 && g.m > hpq) ? 2 : 1;
   const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
@@ -505,8 +544,9 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
     return (e && atoi(e) == 2) ? 2 : 1;
   }();
 #define BFLA_GO(D_, Q_, P_, X_)                                                                          \
-  return spl == 2 ? launch_t<D_, Q_, P_, X_, 2>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st) \
-                  : launch_t<D_, Q_, P_, X_, 1>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st)
+  return spl == 2                                                                                        \
+             ? launch_t<D_, Q_, P_, X_, 2>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st, sched) \
+             : launch_t<D_, Q_, P_, X_, 1>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st, sched)
   const bool paged = g.paged != 0;
   if (g.D == 128 && nqt == 2) {
     if (paged) { if (dense) BFLA_GO(128, 2, true, true); else BFLA_GO(128, 2, true, false); }

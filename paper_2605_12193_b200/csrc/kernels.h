@@ -49,7 +49,8 @@ struct AttnMaps {
 };
 size_t attn_smem_bytes(int D, int nqt);
 int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
-                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st);
+                     const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
+                     int* sched = nullptr);
 // head_dim 128: two kept tiles per step, P in TMEM (attention2.cu)
 // sched: optional device int (zeroed by the caller) for dynamic item scheduling; NULL = static
 int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
