@@ -41,9 +41,13 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
                                                           int32_t* __restrict__ list, int32_t* __restrict__ count,
                                                           uint8_t* __restrict__ label,
                                                           unsigned long long* __restrict__ stats) {
+  __shared__ unsigned long long bsum[8];  // block sums of stats[0..7] (one atomic per counter and block)
+  if (threadIdx.x < 8) bsum[threadIdx.x] = 0ull;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long long nrows = (long long)g.B * g.Hkv * g.Tq;
+  auto body = [&]() {
   if (row >= nrows) return;
   const int i = (int)(row % g.Tq);
   const int h = (int)((row / g.Tq) % g.Hkv);
@@ -63,17 +67,22 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
   int d_i = (int)(fr / g.T);
   if (d_i > R.Tkv - 1) d_i = R.Tkv - 1;
   const int band_lo = d_i - n_local > 0 ? d_i - n_local : 0;
-  const uint32_t* crow = coarse + ((long long)(r * g.Hkv + h) * g.Lq + i / g.rb) * g.Lw;
+  const int rbs = __ffs(g.rb) - 1;  // rho_b = b / T is a power of two: j / rho_b = j >> rbs
+  const uint32_t* crow = coarse + ((long long)(r * g.Hkv + h) * g.Lq + (i >> rbs)) * g.Lw;
   int32_t* lrow = list + (long long)(r * g.Hkv + h) * g.causal_per_head + req_row_offset(R, g.T, i);
   const uint64_t hglob = (uint64_t)(g.head_offset + h);
   int nk = 0;
   unsigned cnt[6] = {0, 0, 0, 0, 0, 0};
+  // the coarse row in registers, one word per lane (Lw <= 32, i.e. up to 1024 blocks), read by shuffle
+  const bool creg = g.Lw <= 32;
+  const uint32_t cw = (creg && lane < g.Lw) ? __ldg(crow + lane) : 0u;
   for (int j0 = 0; j0 < g.Tkv; j0 += 32) {
     const int j = j0 + lane;
     int lab = 0;
+    const int J = j >> rbs;
+    const uint32_t word = creg ? __shfl_sync(0xffffffffu, cw, (J >> 5) & 31) : (j <= jmax ? crow[J >> 5] : 0u);
     if (j <= jmax) {
-      const int J = j / g.rb;
-      if ((crow[J >> 5] >> (J & 31)) & 1u) {
+      if ((word >> (J & 31)) & 1u) {
         lab = 1;
       } else if (j < n_sink) {
         lab = 2;
@@ -102,13 +111,17 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
     for (int l = 1; l < 6; ++l) {
       unsigned v = cnt[l];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && v) atomicAdd(stats + 2 + l, (unsigned long long)v);
+      if (lane == 0 && v) atomicAdd(&bsum[2 + l], (unsigned long long)v);
     }
     if (lane == 0) {
-      atomicAdd(stats + 0, (unsigned long long)(jmax + 1));  // causal tiles of this row
-      atomicAdd(stats + 1, (unsigned long long)nk);
+      atomicAdd(&bsum[0], (unsigned long long)(jmax + 1));  // causal tiles of this row
+      atomicAdd(&bsum[1], (unsigned long long)nk);
     }
   }
+  };
+  body();
+  __syncthreads();
+  if (stats && threadIdx.x < 8 && bsum[threadIdx.x]) atomicAdd(stats + threadIdx.x, bsum[threadIdx.x]);
 }
 
 void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int n_local, int eta, double rho,

@@ -204,6 +204,37 @@ def test_keep_ratio_fast_path(ratio):
     print(f"ratio {ratio}: flagged {fast['stats']['rows_flagged']} of {fast['stats']['rows']}")
 
 
+@pytest.mark.parametrize("paged", [0, 16])
+def test_dynamic_and_static_item_order_identical(paged):
+    """The prefill kernels take their work items from a workspace counter when a workspace is given
+    (greedy longest-first scheduling) and round-robin without one: every item is computed the same
+    way whichever CTA takes it, so O and LSE are bitwise identical (sparse and dense)."""
+    prob = workloads.structured(12, B=2, Hq=8, Hkv=2, Nq=3000, Nkv=3000, d=128, block=256)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    if paged:
+        kc, vc, pt = workloads.paged(k, v, paged, seed=4, extra_pages=3)
+    outs = []
+    for use_ws in (True, False):
+        o = torch.empty_like(q)
+        l = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+        P = (bf.make_problem(q, kc, vc, o, l, page_table=pt, n_kv=k.shape[2]) if paged
+             else bf.make_problem(q, k, v, o, l))
+        cfg = bf.Config(b=256, g=64)
+        ws = bf.alloc_workspace(P, cfg)
+        m = bf.alloc_mask(P, cfg)
+        bf.bfla_block_mask(P, cfg, m, ws)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        bf.bfla_sparse_prefill(P, cfg, m, ws if use_ws else None)
+        od = torch.empty_like(q)
+        Pd = (bf.make_problem(q, kc, vc, od, page_table=pt, n_kv=k.shape[2]) if paged
+              else bf.make_problem(q, k, v, od))
+        bf.bfla_prefill(Pd, None, None, bf.alloc_workspace(Pd, None) if use_ws else None)
+        torch.cuda.synchronize()
+        outs.append((o.clone(), l.clone(), od.clone()))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+
+
 def test_mean_pool_and_keep_ratio():
     prob = workloads.gaussian(21, B=1, Hq=4, Hkv=2, Nq=1500, Nkv=1500, d=128, sigma=1.0)
     for cfg in [bf.Config(b=128, g=64, pool=bf.POOL_MEAN, gamma=0.9),
