@@ -235,6 +235,17 @@ def test_dynamic_and_static_item_order_identical(paged):
         assert torch.equal(a, b)
 
 
+def test_whole_path_deterministic():
+    """S:513 / §8(b): identical inputs give identical bits — masks, lists, O and LSE of two runs of the
+    whole path (tensor-core Stage 1 with certification and recompute, dynamic item scheduling)."""
+    prob = workloads.structured(13, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128, block=256)
+    cfg = bf.Config(b=256, g=64, eta=8, rho=0.1, seed=3)
+    a, b = run_gpu(prob, cfg), run_gpu(prob, cfg)
+    for key in ("coarse", "tiles", "labels", "count", "list"):
+        assert np.array_equal(a[key], b[key]), key
+    assert torch.equal(a["o"], b["o"]) and torch.equal(a["lse"], b["lse"])
+
+
 def test_mean_pool_and_keep_ratio():
     prob = workloads.gaussian(21, B=1, Hq=4, Hkv=2, Nq=1500, Nkv=1500, d=128, sigma=1.0)
     for cfg in [bf.Config(b=128, g=64, pool=bf.POOL_MEAN, gamma=0.9),
