@@ -124,8 +124,14 @@ def run_ours(args, w, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     N, Hq, Hkv, d = w["N"], w["Hq"], w["Hkv"], w["d"]
     heads = args.shard == "heads" and dist.is_initialized()
+    bal = args.shard == "balanced" and dist.is_initialized()
+    if bal and w["paged"]:
+        raise SystemExit("--shard balanced: contiguous K/V workloads only")
     head_offset = 0
-    if heads:
+    if bal:  # strong scaling (§8 f2): every rank holds the whole layer; masks by heads, prefill by cost
+        full = make_inputs(w, 303, dev)
+        q, k, v = full.q, full.k, full.v
+    elif heads:
         # strong scaling of ONE layer: every rank builds the same layer and keeps its KV-head group
         full = make_inputs(w, 303, dev)
         q, k, v, head_offset = parallel.shard_views(full.q, full.k, full.v, rank, world)
@@ -147,10 +153,16 @@ def run_ours(args, w, rank, world, local_rank):
         P = bf.make_problem(q, k, v, o, head_offset=head_offset)
     ws = bf.alloc_workspace(P, cfg)
     m = bf.alloc_mask(P, cfg)
+    if bal:
+        layer = parallel.BalancedLayer(q, k, v, o, cfg, rank, world)
+        m = layer.ms  # stats of this rank's head group (Stage 1/2 certification)
     st = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
     def step(record=None):
+        if bal:  # stages: masks (own heads) | list gather + slice | prefill slice, then O all-reduce
+            layer.run(record, st)
+            return
         if record is not None:
             record[0].record(st)
         bf.bfla_block_mask(P, cfg, m, ws)
@@ -247,6 +259,7 @@ def run_ours(args, w, rank, world, local_rank):
         else:
             Pb = bf.make_problem(qd, kd, vd, od, head_offset=rank * Hkv)
         bufs.append((qd, kd, vd, od, Pb))
+    layers_e2e = [parallel.BalancedLayer(b_[0], b_[1], b_[2], b_[3], cfg, rank, world) for b_ in bufs] if bal else None
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     ne = max(2, min(args.steps, 5))
     ev_in = [torch.cuda.Event() for _ in range(ne)]    # inputs of step i resident
@@ -275,9 +288,12 @@ def run_ours(args, w, rank, world, local_rank):
         st.wait_event(ev_in[i])
         if i >= 2:
             st.wait_event(ev_out[i - 2])
-        bf.bfla_block_mask(Pb, cfg, m, ws)
-        bf.bfla_expand_rescue(Pb, cfg, m, ws)
-        bf.bfla_sparse_prefill(Pb, cfg, m, ws)
+        if bal:
+            layers_e2e[i % 2].run(None, st)
+        else:
+            bf.bfla_block_mask(Pb, cfg, m, ws)
+            bf.bfla_expand_rescue(Pb, cfg, m, ws)
+            bf.bfla_sparse_prefill(Pb, cfg, m, ws)
         if heads:
             o_full.copy_(parallel.gather_heads(od, world))
         ev_done[i].record(st)
@@ -299,6 +315,11 @@ def run_ours(args, w, rank, world, local_rank):
     peaks = load_peaks()
     m_ = Hq // Hkv
     kept = stats["kept_tiles"]
+    if bal:  # this rank's prefill ran its slice only
+        r0, r1 = layer.bounds
+        cnt = layer.counts_host.view(-1, layer.counts_host.shape[-1])  # [B*Hkv, Tq]
+        Tq_ = cnt.shape[1]
+        kept = sum(int(cnt[rho // Tq_, Tq_ - 1 - rho % Tq_]) for rho in range(r0, r1))
     retained_flops = 4.0 * d * m_ * 64 * 64 * kept  # per launch: every kept (h, i, j) tile, m heads, QK^T + PV
     achieved_tf = retained_flops / (at * 1e-3) / 1e12
     dense_flops = 4.0 * d * Hq * N * (N + 1) / 2
@@ -365,8 +386,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama8b-32k", choices=sorted(WORKLOADS))
     ap.add_argument("--pool", default="flatten", choices=["flatten", "mean"])
-    ap.add_argument("--shard", default="layers", choices=["layers", "heads"],
-                    help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O all-gather (strong)")
+    ap.add_argument("--shard", default="layers", choices=["layers", "heads", "balanced"],
+                    help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O "
+                         "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
+                         "slices + O all-reduce (strong, SURVEY §8 f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
@@ -379,6 +402,8 @@ def main():
               "inputs": "structured synthetic (sinks+local+scattered heavy blocks), seed 303+rank",
               "l2": "no flush: per-layer inputs Q+K+V+O exceed the 126 MB L2" if w["N"] >= 16384 else "small",
               "parallelism": (f"KV-head groups x{world} + NCCL all-gather of O" if args.shard == "heads" and world > 1
+                              else f"masks by KV-head group, prefill by cost-balanced row slices x{world} + NCCL "
+                                   f"list all-gather and O all-reduce" if args.shard == "balanced" and world > 1
                               else f"independent layer per rank x{world}")}
 
     if args.impl == "reference":
@@ -413,14 +438,16 @@ def main():
     r = run_ours(args, w, rank, world, local_rank)
     if rank == 0:
         peaks = r["peaks"]
-        strong = args.shard == "heads" and dist.is_initialized()
+        strong = args.shard in ("heads", "balanced") and dist.is_initialized()
         value = r["ms_per_step"] if strong else r["ms_per_step"] / world
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": False, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "bf16 (fp32 accumulate; canonical fp32 mask)", "data": "synthetic",
             "config": config,
-            "stages_ms": {"stage1_scores_select": r["s1"], "stage2_expand_rescue": r["s2"], "sparse_prefill": r["at"]},
+            "stages_ms": ({"stage1_stage2_own_heads": r["s1"], "list_gather_and_slice": r["s2"],
+                           "sparse_prefill_slice": r["at"]} if args.shard == "balanced" and world > 1 else
+                          {"stage1_scores_select": r["s1"], "stage2_expand_rescue": r["s2"], "sparse_prefill": r["at"]}),
             "kappa": r["kappa"],
             "stage1_certification": {"head_rows": r["stats"]["rows"], "rows_flagged": r["stats"]["rows_flagged"],
                                      "groups_recomputed": r["stats"]["rows_recomputed"],

@@ -179,6 +179,30 @@ bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* 
    bfla_workspace_size bytes — the kernel schedules its work items dynamically through a counter kept
    in ws; with ws == NULL it uses a static round-robin order.  Results are identical either way.) */
 
+/* Work slice of the sparse prefill (balanced sharding): the same computation as
+   bfla_sparse_prefill restricted to the prefill rows rho in [row_begin, row_end) of the LPT row order
+   rho = (r * h_kv + h) * Tq + (Tq - 1 - i) — (request, head group) major, query tile i DESCENDING
+   (h ranges over mask groups: h_q of them in PER_Q_HEAD mode); inside the slice the rows run in
+   descending i with its (r, h) segments interleaved (longest first).  A row writes the O (+ LSE) rows
+   i*T .. i*T+T-1 of every query head of its group; rows outside the slice are not touched.  Results
+   are bit-identical to the unsliced call on the rows written (every row is computed by one CTA,
+   independently of the schedule).  Errors: BFLA_ERR_INVALID_ARGUMENT unless
+   0 <= row_begin <= row_end <= batch * h_kv * Tq; an empty slice enqueues nothing. */
+bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                     int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes, void* stream);
+
+/* Host-only (no GPU, no CUDA call): cost-balanced contiguous partition of the LPT row order into
+   `parts` slices for bfla_sparse_prefill_rows (§8 f2: per-head kappa differs, so equal head counts per
+   GPU are not equal work; P:443 runs 8 GPUs without naming a scheme).  tile_count is a HOST copy of
+   mask->tile_count ([batch][h_kv][tq], kept tiles per row, Eq. 26); the cost of a row is
+   tile_count + row_overhead (the per-row fixed cost in tile units).  Writes bounds[0..parts]
+   (bounds[0] = 0, bounds[parts] = batch * h_kv * tq, non-decreasing): slice k = [bounds[k],
+   bounds[k+1]).  The bottleneck max_k cost(slice k) is the minimum over all contiguous partitions
+   (bisection on the bottleneck with greedy packing); when there are at least `parts` rows every slice
+   is non-empty.  Errors: BFLA_ERR_INVALID_ARGUMENT on NULL pointers or non-positive sizes. */
+bfla_status bfla_balance_rows(const int32_t* tile_count, int32_t batch, int32_t h_kv, int32_t tq, int32_t row_overhead,
+                              int32_t parts, int64_t* bounds);
+
 /* The whole path: Stage 1 -> Stage 2 -> sparse prefill.  config == NULL runs DENSE causal attention
    (Eq. 1, the comparator) with the same kernel.  mask == NULL keeps the mask buffers inside ws. */
 bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,

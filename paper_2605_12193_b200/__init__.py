@@ -20,8 +20,8 @@ from ._lib import (KV_CONTIGUOUS, KV_PAGED, MASK_PER_KV_HEAD, MASK_PER_Q_HEAD, P
                    bfla_mask, bfla_problem, bfla_stats, check, lib)
 
 __all__ = ["Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
-           "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill", "bfla_prefill",
-           "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
+           "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill",
+           "bfla_sparse_prefill_rows", "bfla_balance_rows", "bfla_prefill", "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
            "SCORES_CANONICAL", "MASK_PER_KV_HEAD", "MASK_PER_Q_HEAD"]
 
 
@@ -207,6 +207,27 @@ def bfla_sparse_prefill(problem: Problem, cfg: Config, mask: Mask, ws: Optional[
     m = mask.c()
     check(lib().bfla_sparse_prefill(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m), _ptr(ws),
                                     0 if ws is None else ws.numel(), _stream(stream)), "bfla_sparse_prefill")
+
+
+def bfla_sparse_prefill_rows(problem: Problem, cfg: Config, mask: Mask, row_begin: int, row_end: int,
+                             ws: Optional[torch.Tensor] = None, stream=None) -> None:
+    """Sparse prefill of the LPT-order rows [row_begin, row_end) only (include/bfla.h, §8 f2)."""
+    m = mask.c()
+    check(lib().bfla_sparse_prefill_rows(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
+                                         int(row_begin), int(row_end), _ptr(ws), 0 if ws is None else ws.numel(),
+                                         _stream(stream)), "bfla_sparse_prefill_rows")
+
+
+def bfla_balance_rows(tile_count, parts: int, row_overhead: int = 3) -> list[int]:
+    """Cost-balanced slice bounds (parts + 1 of them) of the LPT row order; tile_count is a host
+    [batch, h_kv, tq] int32 tensor/array (a copy of mask.tile_count).  Host-only library call."""
+    t = torch.as_tensor(tile_count).to(torch.int32).contiguous().cpu()
+    if t.dim() != 3:
+        raise ValueError("tile_count must be [batch, h_kv, tq]")
+    bounds = (ctypes.c_int64 * (parts + 1))()
+    check(lib().bfla_balance_rows(ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_int32)), t.shape[0], t.shape[1],
+                                  t.shape[2], int(row_overhead), int(parts), bounds), "bfla_balance_rows")
+    return list(bounds)
 
 
 def bfla_prefill(problem: Problem, cfg: Optional[Config], mask: Optional[Mask], ws: Optional[torch.Tensor],

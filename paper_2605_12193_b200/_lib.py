@@ -58,7 +58,8 @@ class bfla_mask(ctypes.Structure):
 _lib = None
 
 ENTRY_POINTS = ["bfla_workspace_size", "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue",
-                "bfla_sparse_prefill", "bfla_prefill", "bfla_status_string", "bfla_last_error",
+                "bfla_sparse_prefill", "bfla_sparse_prefill_rows", "bfla_balance_rows", "bfla_prefill",
+                "bfla_status_string", "bfla_last_error",
                 "bfla_kernel_launches"]
 
 
@@ -79,6 +80,11 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = [P(bfla_problem), P(bfla_config), mask_t, vp, ctypes.c_size_t, vp]
             fn.restype = ctypes.c_int
+        L.bfla_sparse_prefill_rows.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64, vp,
+                                               ctypes.c_size_t, vp]
+        L.bfla_sparse_prefill_rows.restype = ctypes.c_int
+        L.bfla_balance_rows.argtypes = [P(i32), i32, i32, i32, i32, i32, P(i64)]
+        L.bfla_balance_rows.restype = ctypes.c_int
         L.bfla_status_string.argtypes = [ctypes.c_int]
         L.bfla_status_string.restype = ctypes.c_char_p
         L.bfla_last_error.argtypes = []

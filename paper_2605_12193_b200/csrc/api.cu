@@ -496,6 +496,81 @@ bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* 
   return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
 }
 
+bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                     int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes, void* stream) {
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if (!mask || !mask->tile_list || !mask->tile_count) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask lists are NULL");
+  const int64_t rows = (int64_t)g.B * g.Hkv * g.Tq;
+  if (row_begin < 0 || row_end < row_begin || row_end > rows)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                (long long)row_end, (long long)rows);
+  if (row_end == row_begin) return BFLA_OK;  // an empty slice enqueues nothing
+  g.row0 = (int)row_begin;
+  g.nrows = (int)(row_end - row_begin);
+  const WsLayout L = ws_layout(g);
+  int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
+                                                : nullptr;
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
+}
+
+bfla_status bfla_balance_rows(const int32_t* tile_count, int32_t batch, int32_t h_kv, int32_t tq, int32_t row_overhead,
+                              int32_t parts, int64_t* bounds) {
+  if (!tile_count || !bounds || batch < 1 || h_kv < 1 || tq < 1 || parts < 1 || row_overhead < 0)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "balance_rows: bad argument");
+  const int64_t n = (int64_t)batch * h_kv * tq;
+  // cost of LPT row rho = (r * h_kv + h) * tq + (tq - 1 - i): its kept tiles + a per-row overhead
+  auto cost = [&](int64_t rho) -> int64_t {
+    const int64_t seg = rho / tq, i = tq - 1 - rho % tq;
+    const int32_t c = tile_count[seg * tq + i];
+    return (int64_t)(c > 0 ? c : 0) + row_overhead;
+  };
+  int64_t total = 0, lo = 0;
+  for (int64_t rho = 0; rho < n; ++rho) {
+    const int64_t c = cost(rho);
+    total += c;
+    lo = c > lo ? c : lo;
+  }
+  // smallest bottleneck M such that greedy contiguous packing needs <= parts pieces (exact optimum
+  // of the linear partition problem: greedy packing is optimal for a fixed M)
+  auto pieces = [&](int64_t M) -> int64_t {
+    int64_t k = 1, acc = 0;
+    for (int64_t rho = 0; rho < n; ++rho) {
+      const int64_t c = cost(rho);
+      if (acc + c > M) {
+        ++k;
+        acc = 0;
+      }
+      acc += c;
+    }
+    return k;
+  };
+  int64_t hi = total;
+  if (lo < (total + parts - 1) / parts) lo = (total + parts - 1) / parts;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (pieces(mid) <= parts) hi = mid;
+    else lo = mid + 1;
+  }
+  // cut greedily at the optimum M, but never leave fewer rows than parts still to fill: rows are
+  // handed out so that every part gets at least one row when n >= parts
+  int64_t acc = 0, p = 0;
+  bounds[0] = 0;
+  for (int64_t rho = 0; rho < n; ++rho) {
+    const int64_t c = cost(rho);
+    const bool must = (n - rho) <= (parts - 1 - p);  // remaining rows only just cover remaining parts
+    if (p < parts - 1 && rho > bounds[p] && (acc + c > lo || must)) {
+      bounds[++p] = rho;
+      acc = 0;
+    }
+    acc += c;
+  }
+  while (p < parts) bounds[++p] = n;
+  return BFLA_OK;
+}
+
 bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
                          size_t ws_bytes, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -535,7 +535,7 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
   const int hpq = BM / g.T;
   const int nqt = (g.D == 128 && g.m > hpq) ? 2 : 1;
   const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
-  const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
+  const long long items = (g.nrows ? (long long)g.nrows : (long long)g.B * g.Hkv * g.Tq) * NC;
   if (items == 0) return 0;
   const int n = (int)items;
   // softmax warpgroups per Q tile: 1 (default) or 2 (BFLA_SOFTMAX_SPLIT=2, A/B experiments)

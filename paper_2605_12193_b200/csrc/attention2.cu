@@ -757,7 +757,7 @@ int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, 
   const int hpq = BM / g.T;
   const int nqt = g.m > hpq ? 2 : 1;
   const int NC = (g.m + nqt * hpq - 1) / (nqt * hpq);
-  const long long items = (long long)g.B * g.Hkv * NC * g.Tq;
+  const long long items = (g.nrows ? (long long)g.nrows : (long long)g.B * g.Hkv * g.Tq) * NC;
   if (items == 0) return 0;
   const int n = (int)items;
 #define BFLA_GO2(Q_, P_, X_) \

@@ -30,6 +30,9 @@ struct Geom {
   // group h reads KV head h / kvdiv of a tensor with Hkv_real heads (per KV head: kvdiv = 1,
   // Hkv_real = Hkv; per query head: Hkv = Hq, m = 1, kvdiv = the GQA group size)
   int kvdiv, Hkv_real;
+  // prefill work slice (bfla_sparse_prefill_rows, §8 f2): rows [row0, row0 + nrows) of the LPT row
+  // order rho = (r * Hkv + h) * Tq + (Tq - 1 - i); nrows = 0 means every row
+  int row0, nrows;
 };
 
 // Logical dimensions of request r (Eq. 4, 11, 19 with that request's N_q, N_kv).

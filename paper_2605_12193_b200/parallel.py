@@ -53,3 +53,118 @@ def request_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     """Request (batch) slice for request-level sharding: requests are fully independent."""
     per = -(-batch // world)
     return min(batch, rank * per), min(batch, (rank + 1) * per)
+
+
+# ---- §8 f2: cost-balanced row sharding of the prefill ------------------------------------------
+# Head sharding gives every rank h_kv / world heads, but per-head kappa differs (P:443 runs 8 GPUs
+# without naming a scheme), so the rank with the densest heads sets the layer time.  Balanced
+# sharding keeps Stage 1 + Stage 2 head-sharded (their cost is per head and small), gathers the
+# kept-tile lists, and splits the PREFILL by cost: contiguous slices of the LPT row order
+# rho = (r * h_kv + h) * Tq + (Tq - 1 - i) whose kept-tile sums are balanced (bfla_balance_rows),
+# each run with bfla_sparse_prefill_rows.  The output rows are then assembled across ranks.
+
+
+def gather_mask_lists(tile_list: torch.Tensor, tile_count: torch.Tensor, batch: int, world: int, group=None):
+    """All-gather head-sharded Stage-2 lists into the global layout.
+
+    Local tile_count is [batch, h_kv/world, Tq] and tile_list holds batch * (h_kv/world) * C entries
+    (C = causal tiles per (r, h), include/bfla.h); ranks hold consecutive head slices (head_range).
+    Returns (tile_list [batch, h_kv * C], tile_count [batch, h_kv, Tq]) — exactly the layout an unsharded
+    bfla_expand_rescue writes, because Stage 2 rows are independent and psi takes the global head."""
+    out = []
+    for t, last in ((tile_list, None), (tile_count, tile_count.shape[-1])):
+        t = t.reshape(batch, -1).contiguous()  # per request: [hl * X], head-major
+        if dist.get_backend(group) == "nccl":
+            buf = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(buf, t, group=group)
+        else:
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t, group=group)
+            buf = torch.stack(parts)
+        g = buf.permute(1, 0, 2).reshape(batch, -1)  # [B, world * hl * X]: global head order
+        out.append(g if last is None else g.reshape(batch, -1, last))
+    return out[0], out[1]
+
+
+def balanced_slice(tile_count_host: torch.Tensor, world: int, rank: int, row_overhead: int = 3) -> tuple[int, int]:
+    """This rank's LPT row slice [row_begin, row_end) of a cost-balanced partition (bfla_balance_rows).
+    Every rank computes the same bounds from the same gathered counts, so no exchange is needed."""
+    from . import bfla_balance_rows
+
+    b = bfla_balance_rows(tile_count_host, world, row_overhead)
+    return b[rank], b[rank + 1]
+
+
+def slice_rows(row_begin: int, row_end: int, h_kv: int, tq: int):
+    """(r, h, i) of the LPT rows in a slice, in order (host helper for tests and reports)."""
+    out = []
+    for rho in range(row_begin, row_end):
+        seg, j = divmod(rho, tq)
+        out.append((seg // h_kv, seg % h_kv, tq - 1 - j))
+    return out
+
+
+def assemble_rows(o: torch.Tensor, lse: torch.Tensor | None = None, group=None) -> None:
+    """Assemble row-sharded outputs in place: every rank zero-filled O (and LSE) before its slice wrote
+    its rows, so a SUM all-reduce gives every rank the full output exactly (x + 0 = x).  This is the
+    exposed-collective form; the fused form (the epilogue storing O tiles straight into every peer's
+    buffer over NVLink multicast) is the f2 follow-up."""
+    dist.all_reduce(o, group=group)
+    if lse is not None:
+        dist.all_reduce(lse, group=group)
+
+
+class BalancedLayer:
+    """One layer of the f2 strong-scaling path on this rank (all buffers on the rank's GPU):
+
+      1. Stage 1 + Stage 2 on the rank's KV-head group (head-sharded views, global psi offset);
+      2. all-gather of the kept-tile lists and counts into the full-layer mask layout (NCCL);
+      3. cost-balanced LPT row slice from the gathered counts (host, bfla_balance_rows; every rank
+         derives the same bounds, so no exchange);
+      4. bfla_sparse_prefill_rows over the full layer's Q/K/V for that slice, into a zeroed O;
+      5. SUM all-reduce of O (assemble_rows).
+
+    q/k/v are the full layer (head-first, every rank holds them); o is the full-size output."""
+
+    def __init__(self, q, k, v, o, cfg, rank: int, world: int, row_overhead: int = 3, group=None):
+        from . import alloc_mask, alloc_workspace, make_problem
+
+        self.cfg, self.rank, self.world, self.ovh, self.group = cfg, rank, world, row_overhead, group
+        self.B, self.Hkv = q.shape[0], k.shape[1]
+        # zero-copy strided views of the rank's head group; the shard problem only runs the mask
+        # stages, so its O (a view of the full O) is never written through it
+        qs, ks, vs, h0 = shard_views(q, k, v, rank, world)
+        os_ = shard_views(o, k, v, rank, world)[0]
+        self.Ps = make_problem(qs, ks, vs, os_, head_offset=h0)
+        self.ms = alloc_mask(self.Ps, cfg)
+        self.wss = alloc_workspace(self.Ps, cfg)
+        self.o = o
+        self.P = make_problem(q, k, v, o)
+        self.m = alloc_mask(self.P, cfg)
+        self.ws = alloc_workspace(self.P, cfg)
+        self.counts_host = torch.empty(self.m.tile_count.shape, dtype=torch.int32).pin_memory()
+        self.bounds = None
+
+    def run(self, marks=None, stream=None):
+        """One layer; marks (optional) = 4 CUDA events recorded at the stage boundaries
+        (start, masks done, lists gathered + sliced, prefill done)."""
+        from . import bfla_block_mask, bfla_expand_rescue, bfla_sparse_prefill_rows
+
+        st = torch.cuda.current_stream() if stream is None else stream
+        rec = (lambda k: marks[k].record(st)) if marks is not None else (lambda k: None)
+        rec(0)
+        bfla_block_mask(self.Ps, self.cfg, self.ms, self.wss, st)
+        bfla_expand_rescue(self.Ps, self.cfg, self.ms, self.wss, st)
+        rec(1)
+        tl, tc = gather_mask_lists(self.ms.tile_list, self.ms.tile_count, self.B, self.world, self.group)
+        self.m.tile_list[:tl.numel()].copy_(tl.reshape(-1))
+        self.m.tile_count.view(tc.shape).copy_(tc)
+        self.counts_host.copy_(self.m.tile_count, non_blocking=True)
+        st.synchronize()  # the slice bounds are host decisions (a few KB of counts)
+        r0, r1 = balanced_slice(self.counts_host.view(self.B, self.Hkv, -1), self.world, self.rank, self.ovh)
+        self.bounds = (r0, r1)
+        rec(2)
+        self.o.zero_()
+        bfla_sparse_prefill_rows(self.P, self.cfg, self.m, r0, r1, self.ws, st)
+        rec(3)
+        assemble_rows(self.o, None, self.group)

@@ -420,3 +420,104 @@ def test_varlen_dense_and_single_call():
         qf, kf, vf = (f32(t[r])[:, :n] for t, n in ((prob.q, nq), (prob.k, nkv), (prob.v, nkv)))
         O_ref, _ = oracle.masked_attention(qf, kf, vf, 128 ** -0.5)
         compare_o(o[r, :, :nq], O_ref, f"varlen dense r={r}")
+
+
+def _lpt_rows(rho0, rho1, B, H, Tq):
+    """(r, h, i) of the LPT-order rows [rho0, rho1) (include/bfla.h, bfla_sparse_prefill_rows)."""
+    out = []
+    for rho in range(rho0, rho1):
+        seg, i = divmod(rho, Tq)
+        out.append((seg // H, seg % H, Tq - 1 - i))
+    return out
+
+
+@pytest.mark.parametrize("case", [
+    dict(B=2, Hq=8, Hkv=2, N=3000, d=128, paged=0),     # m=4 (NQT=2), two requests
+    dict(B=1, Hq=8, Hkv=2, N=3000, d=128, paged=16),    # paged K/V
+    dict(B=1, Hq=16, Hkv=2, N=2500, d=128, paged=0),    # m=8: two head chunks per row
+    dict(B=1, Hq=4, Hkv=2, N=2000, d=256, paged=0),     # d=256 kernel
+])
+def test_row_slices_compose_to_full_prefill(case):
+    """§8 f2: slicing the prefill by LPT rows (bfla_sparse_prefill_rows) over a cost-balanced partition
+    (bfla_balance_rows) reproduces the unsliced O and LSE bit for bit, and one slice writes exactly its
+    rows' (heads, tokens) and nothing else."""
+    B, Hq, Hkv, N, d, paged = (case[k] for k in ("B", "Hq", "Hkv", "N", "d", "paged"))
+    prob = workloads.structured(14, B=B, Hq=Hq, Hkv=Hkv, Nq=N, Nkv=N, d=d, block=256)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    if paged:
+        kc, vc, pt = workloads.paged(k, v, paged, seed=6, extra_pages=2)
+
+    def problem(o, l):
+        return (bf.make_problem(q, kc, vc, o, l, page_table=pt, n_kv=N) if paged
+                else bf.make_problem(q, k, v, o, l))
+
+    cfg = bf.Config(b=256, g=64, eta=8, rho=0.1, seed=9)
+    o_full = torch.empty_like(q)
+    l_full = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    P = problem(o_full, l_full)
+    ws = bf.alloc_workspace(P, cfg)
+    m = bf.alloc_mask(P, cfg)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    counts = m.tile_count.view(B, Hkv, -1).cpu()
+    Tq = counts.shape[2]
+    bounds = bf.bfla_balance_rows(counts, 3)
+    assert bounds[0] == 0 and bounds[-1] == B * Hkv * Tq
+
+    sentinel_o, sentinel_l = 7.0, -5.0
+    o_s = torch.full_like(q, sentinel_o)
+    l_s = torch.full(q.shape[:3], sentinel_l, dtype=torch.float32, device="cuda")
+    Ps = problem(o_s, l_s)
+    for a, b_ in zip(bounds[:-1], bounds[1:]):
+        bf.bfla_sparse_prefill_rows(Ps, cfg, m, a, b_, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(o_s, o_full) and torch.equal(l_s, l_full)
+
+    # one slice alone: exactly its rows
+    a, b_ = bounds[1], bounds[2]
+    o_1 = torch.full_like(q, sentinel_o)
+    l_1 = torch.full(q.shape[:3], sentinel_l, dtype=torch.float32, device="cuda")
+    bf.bfla_sparse_prefill_rows(problem(o_1, l_1), cfg, m, a, b_, None)
+    torch.cuda.synchronize()
+    want = torch.zeros(q.shape[:3], dtype=torch.bool)
+    mh = Hq // Hkv
+    for r, h, i in _lpt_rows(a, b_, B, Hkv, Tq):
+        want[r, h * mh:(h + 1) * mh, i * 64:(i + 1) * 64] = True
+    want = want.cuda()
+    assert torch.equal(o_1[want], o_full[want]) and torch.equal(l_1[want], l_full[want])
+    assert bool((o_1[~want] == sentinel_o).all()) and bool((l_1[~want] == sentinel_l).all())
+    # empty slices enqueue nothing; out-of-range slices are rejected before any launch
+    bf.bfla_sparse_prefill_rows(Ps, cfg, m, 5, 5, ws)
+    with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
+        bf.bfla_sparse_prefill_rows(Ps, cfg, m, 0, B * Hkv * Tq + 1, ws)
+
+
+def test_balanced_layer_single_rank_nccl():
+    """The f2 strong-scaling layer (parallel.BalancedLayer: head-group masks on strided views, NCCL
+    list all-gather, host slice bounds, sliced prefill into a zeroed O, O all-reduce) through a real
+    one-rank NCCL group equals the unsharded whole path bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+    from paper_2605_12193_b200 import parallel
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        prob = workloads.structured(15, B=2, Hq=8, Hkv=2, Nq=2100, Nkv=2100, d=128, block=256)
+        q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+        cfg = bf.Config(b=256, g=64, eta=8, rho=0.1, seed=4)
+        o_ref, _ = bf.prefill(q, k, v, cfg)
+        o = torch.full_like(q, 3.0)
+        layer = parallel.BalancedLayer(q, k, v, o, cfg, 0, 1)
+        layer.run()
+        torch.cuda.synchronize()
+        assert layer.bounds == (0, 2 * 2 * 33)
+        assert torch.equal(o, o_ref)
+    finally:
+        dist.destroy_process_group()

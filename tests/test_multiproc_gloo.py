@@ -68,3 +68,106 @@ def test_head_range_and_views():
     assert h0 == 2 and qs.shape == (2, 4, 16, 4) and ks.shape == (2, 2, 16, 4)
     assert qs.data_ptr() == q[:, 4].data_ptr()  # zero-copy view
     assert parallel.request_range(5, 2, 1) == (3, 5)
+
+
+def _worker_balanced(rank, world, port, out_dir):
+    """§8 f2 flow on CPU: head-sharded masks -> gathered lists/counts -> cost-balanced row slices ->
+    each rank's rows only -> SUM all-reduce.  The per-slice compute is the oracle restricted to the
+    slice's rows (the GPU path runs bfla_sparse_prefill_rows on the same slice)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import workloads
+    from paper_2605_12193_b200 import parallel
+
+    T = 64
+    prob = workloads.gaussian(6, 1, 8, 4, 512, 512, 128, sigma=0.8)
+    q, k, v, h0 = parallel.shard_views(prob.q, prob.k, prob.v, rank, world)
+    f = lambda t: t[0].float().numpy()
+    res = oracle.mask_pipeline(f(q), f(k), b=128, g=64, T=T, gamma=0.95, eta=4, rho=0.3, seed=9, head_offset=h0)
+    labels = res["labels"]  # [hl, Tq, Tkv]
+    hl, tq, tkv = labels.shape
+    causal = np.tril(np.ones((tq, tkv), dtype=bool))
+    C = int(causal.sum())
+    lists = np.full((hl, C), -1, np.int32)
+    for h in range(hl):  # compacted rows at the closed-form offsets c_i (include/bfla.h)
+        off = 0
+        for i in range(tq):
+            js = np.nonzero(labels[h, i] > 0)[0]
+            lists[h, off:off + len(js)] = js
+            off += i + 1
+    counts = (labels > 0).sum(-1).astype(np.int32)
+    g_list, g_count = parallel.gather_mask_lists(torch.from_numpy(lists).reshape(-1), torch.from_numpy(counts)[None],
+                                                 1, world)
+    r0, r1 = parallel.balanced_slice(g_count, world, rank)
+    # this rank's rows only: the oracle over all heads with the gathered labels, rows outside zeroed
+    full_labels = parallel.gather_heads(torch.from_numpy(labels.astype(np.int32))[None], world)[0].numpy()
+    O, lse = oracle.masked_attention(f(prob.q), f(prob.k), f(prob.v), 128 ** -0.5, full_labels, T)
+    own = np.zeros(O.shape[:2], dtype=bool)
+    m = 2  # heads per group (Hq=8, Hkv=4)
+    for _, h, i in parallel.slice_rows(r0, r1, 4, tq):
+        own[h * m:(h + 1) * m, i * T:(i + 1) * T] = True
+    o_t = torch.from_numpy(np.where(own[..., None], O, 0.0))
+    l_t = torch.from_numpy(np.where(own, lse, 0.0))
+    parallel.assemble_rows(o_t, l_t)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "list.npy"), g_list[0].numpy().reshape(4, -1))
+        np.save(os.path.join(out_dir, "count.npy"), g_count[0].numpy())
+        np.save(os.path.join(out_dir, "o.npy"), o_t.numpy())
+        np.save(os.path.join(out_dir, "slices.npy"), np.array([r0, r1]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_balanced_row_sharding_equals_unsharded(tmp_path, orc):
+    world = 2
+    mp.spawn(_worker_balanced, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    import workloads
+
+    prob = workloads.gaussian(6, 1, 8, 4, 512, 512, 128, sigma=0.8)
+    f = lambda t: t[0].float().numpy()
+    full = orc.mask_pipeline(f(prob.q), f(prob.k), b=128, g=64, T=64, gamma=0.95, eta=4, rho=0.3, seed=9)
+    labels = full["labels"]
+    counts = (labels > 0).sum(-1)
+    assert np.array_equal(np.load(tmp_path / "count.npy"), counts)
+    lst = np.load(tmp_path / "list.npy")
+    for h in range(labels.shape[0]):
+        off = 0
+        for i in range(labels.shape[1]):
+            assert np.array_equal(lst[h, off:off + counts[h, i]], np.nonzero(labels[h, i] > 0)[0])
+            off += i + 1
+    O, _ = orc.masked_attention(f(prob.q), f(prob.k), f(prob.v), 128 ** -0.5, labels, 64)
+    assert np.array_equal(np.load(tmp_path / "o.npy"), O)
+    r0, r1 = np.load(tmp_path / "slices.npy")
+    assert r0 == 0 and 0 < r1 < labels.shape[0] * labels.shape[1]
+
+
+def _worker_gather_b2(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_12193_b200 import parallel
+
+    B, hl, C, Tq = 3, 2, 5, 4
+    h = torch.arange(hl) + rank * hl  # global heads of this rank
+    lst = (torch.arange(B)[:, None, None] * 1000 + h[None, :, None] * 100 + torch.arange(C)[None, None, :]).int()
+    cnt = (torch.arange(B)[:, None, None] * 1000 + h[None, :, None] * 100 + torch.arange(Tq)[None, None, :]).int()
+    gl, gc = parallel.gather_mask_lists(lst.reshape(-1), cnt, B, world)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "gl.npy"), gl.numpy())
+        np.save(os.path.join(out_dir, "gc.npy"), gc.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_mask_lists_multi_request(tmp_path):
+    """Global layout of the gathered lists with batch > 1: request-major, then global head (the layout
+    an unsharded bfla_expand_rescue writes, include/bfla.h)."""
+    world = 2
+    mp.spawn(_worker_gather_b2, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    B, H, C, Tq = 3, 4, 5, 4
+    gl, gc = np.load(tmp_path / "gl.npy"), np.load(tmp_path / "gc.npy")
+    want_l = (np.arange(B)[:, None, None] * 1000 + np.arange(H)[None, :, None] * 100 + np.arange(C)).reshape(B, -1)
+    want_c = np.arange(B)[:, None, None] * 1000 + np.arange(H)[None, :, None] * 100 + np.arange(Tq)
+    assert np.array_equal(gl, want_l) and np.array_equal(gc, want_c)
