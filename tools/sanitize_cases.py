@@ -1,6 +1,7 @@
 """Small end-to-end cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel of the
 path — tensor-core Stage 1 with forced recompute (TMA-staged units), canonical SIMT Stage 1, MEAN,
-keep-ratio, per-query-head masks, paged K/V, Stage 2, both attention kernels (d = 128 / 256), dense.
+keep-ratio, per-query-head masks, paged K/V, Stage 2, both attention kernels (d = 128 / 256), dense,
+and the row-sliced prefill over a balanced partition (§8 f2).
 Run on a GPU box:  compute-sanitizer --tool memcheck python tools/sanitize_cases.py"""
 import os
 import sys
@@ -13,7 +14,7 @@ import paper_2605_12193_b200 as bf  # noqa: E402
 import workloads  # noqa: E402
 
 
-def run(prob, cfg, paged=0):
+def run(prob, cfg, paged=0, slices=0):
     q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
     o = torch.empty_like(q)
     lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
@@ -29,7 +30,12 @@ def run(prob, cfg, paged=0):
         m = bf.alloc_mask(P, cfg, labels=True)
         bf.bfla_block_mask(P, cfg, m, ws)
         bf.bfla_expand_rescue(P, cfg, m, ws)
-        bf.bfla_sparse_prefill(P, cfg, m, ws)
+        if slices:
+            bounds = bf.bfla_balance_rows(m.tile_count.cpu(), slices)
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                bf.bfla_sparse_prefill_rows(P, cfg, m, a, b, ws)
+        else:
+            bf.bfla_sparse_prefill(P, cfg, m, ws)
     torch.cuda.synchronize()
     return o
 
@@ -47,8 +53,13 @@ def main():
         ("d=256", workloads.gaussian(7, B=1, Hq=4, Hkv=2, Nq=1024, Nkv=1024, d=256, sigma=0.8), bf.Config(b=256, g=64), 0),
         ("dense", g1, None, 0),
     ]
-    for name, prob, cfg, paged in cases:
-        o = run(prob, cfg, paged)
+    cases = [c + (0,) for c in cases] + [
+        ("row slices (3-way balanced), d=128", g1, bf.Config(b=256, g=64), 0, 3),
+        ("row slices (5-way balanced), d=256",
+         workloads.gaussian(8, B=2, Hq=4, Hkv=2, Nq=1000, Nkv=1000, d=256, sigma=0.8), bf.Config(b=256, g=64), 0, 5),
+    ]
+    for name, prob, cfg, paged, slices in cases:
+        o = run(prob, cfg, paged, slices)
         print(f"{name}: ok, |O| max {o.float().abs().max().item():.3f}", flush=True)
 
 
