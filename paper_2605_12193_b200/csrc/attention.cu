@@ -58,7 +58,7 @@ struct Cfg {
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 
-template <int D, int NQT, bool PAGED, bool DENSE, int SPL>
+template <int D, int NQT, bool PAGED, bool DENSE, int SPL, bool SLICE = false>
 __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     k_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, Geom g, const int32_t* __restrict__ list,
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       uint32_t kv = 0, nit = 0;
       for (int idx = blockIdx.x;;) {
         const bool live = idx < n_items;
-        const Item it = decode_item(g, live ? idx : 0, NC);
+        const Item it = decode_item<SLICE>(g, live ? idx : 0, NC);
         const int cnt = live ? row_count(it) : 0;
         {  // publish (idx, cnt) — or the end marker
           const int e = ring_n & 3;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
           }
         // warm L2 with the next item's Q (it is read from HBM exactly once)
         if (nidx < n_items) {
-          const Item nx = decode_item(g, nidx, NC);
+          const Item nx = decode_item<SLICE>(g, nidx, NC);
           for (int q = 0; q < NQT; ++q)
             for (int s = 0; s < hpq; ++s) {
               const int pl = nx.c * heads_in_chunk + q * hpq + s;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     if (lane == 0) {
       uint32_t kv = 0;
       for (int idx, cnt; next_item(idx, cnt, false);) {
-        const Item it = decode_item(g, idx, NC);
+        const Item it = decode_item<SLICE>(g, idx, NC);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         for (int n = 0; n < cnt; ++n, ++kv) load_kv(1, kv, DENSE ? n : lst[n], it);
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
     };
     uint32_t tc = 0, nit = 0;
     for (int idx, cnt; next_item(idx, cnt, true);) {
-      const Item it = decode_item(g, idx, NC);
+      const Item it = decode_item<SLICE>(g, idx, NC);
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
@@ -518,6 +518,8 @@ static int launch_t(const Geom& g, const AttnMaps& maps, const int32_t* list, co
                     cudaStream_t st, int* sched) {
   using C = Cfg<D, NQT, SPL>;
   auto kern = k_attn<D, NQT, PAGED, DENSE, SPL>;
+  if constexpr (!DENSE && SPL == 1)
+    if (g.nrows) kern = k_attn<D, NQT, PAGED, false, 1, true>;  // work slice (bfla_sparse_prefill_rows)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return (int)e;
   const int grid = n_items < num_sms ? n_items : num_sms;

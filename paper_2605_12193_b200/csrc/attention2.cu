@@ -89,7 +89,7 @@ struct Cfg2 {
 // SMX: softmax variant — 0 fused single pass with exact redo, 1 max-first whole row per thread
 // (MAXFIRST, default).  (Splitting a Q tile's 128 columns over two warpgroups with a row-max
 // exchange was measured 10% slower: the exponential phases of all softmax warps then coincide.)
-template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY>
+template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY, bool SLICE = false>
 __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, int otma, Geom g, const int32_t* __restrict__ list,
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
       int idx = blockIdx.x;
       for (;;) {
         const bool live = idx < n_items;
-        const Item it = decode_item(g, live ? idx : 0, NC);
+        const Item it = decode_item<SLICE>(g, live ? idx : 0, NC);
         const int cnt = live ? row_count(it) : 0;
         {  // publish (idx, cnt) — or the end marker
           const int e = ring_n & 3;
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     // epilogue) or after O_q, staged through the same smem, has been read by the TMA store.
     uint32_t nit = 0;
     for (int idx, cnt; next_item(idx, cnt);) {
-      const Item it = decode_item(g, idx, NC);
+      const Item it = decode_item<SLICE>(g, idx, NC);
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
 #pragma unroll
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
         }
       }
       if (!sched && !(opts & 1) && lane == 0 && idx + (int)gridDim.x < n_items) {  // warm L2: next item's Q
-        const Item nx = decode_item(g, idx + gridDim.x, NC);
+        const Item nx = decode_item<SLICE>(g, idx + gridDim.x, NC);
         for (int q = 0; q < NQT; ++q)
           for (int s = 0; s < hpq; ++s) {
             const int pl = nx.c * heads_in_chunk + q * hpq + s;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     {
       uint32_t ks = 0;
       for (int idx, cnt; next_item(idx, cnt);) {
-        const Item it = decode_item(g, idx, NC);
+        const Item it = decode_item<SLICE>(g, idx, NC);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
         const int ns = (cnt + 1) / 2;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
       umma_commit_warp(s_full + q);
     };
     for (int idx, cnt; next_item(idx, cnt);) {
-      const Item it = decode_item(g, idx, NC);
+      const Item it = decode_item<SLICE>(g, idx, NC);
       (void)it;
       if (cnt == 0) continue;
       const uint32_t my_it = nit++;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
     uint32_t st = 0, nit = 0;
     for (int idx, cnt; next_item(idx, cnt);) {
-      const Item it = decode_item(g, idx, NC);
+      const Item it = decode_item<SLICE>(g, idx, NC);
       const int slot = row / g.T;
       const int pl = it.c * heads_in_chunk + q * hpq + slot;
       const int t = it.i * g.T + (row % g.T);
@@ -744,6 +744,8 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
 #endif
   constexpr int PM = BFLA_POLY_MASK;
   using C = Cfg2<NQT, PAGED>;
+  if constexpr (!DENSE)
+    if (g.nrows) return go(k_attn2<NQT, PAGED, false, 1, PM, true>, C::SMEM_TOTAL, C::THREADS);  // work slice
   if (smx == 0) return go(k_attn2<NQT, PAGED, DENSE, 0, PM>, C::SMEM_TOTAL, C::THREADS);
   return go(k_attn2<NQT, PAGED, DENSE, 1, PM>, C::SMEM_TOTAL, C::THREADS);
 }

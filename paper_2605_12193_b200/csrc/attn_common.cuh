@@ -31,41 +31,47 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                      __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
+// Work slice [row0, row0 + nrows) of the item order (bfla_sparse_prefill_rows): executed in descending i
+// with the slice's (r, h) segments interleaved, so the longest rows still go first.  Compiled only into
+// the SLICE kernel instances: a runtime branch in the unsliced kernels cost them 1.5 % (measured).
+__device__ __forceinline__ Item decode_slice(const Geom& g, int idx, int NC) {
+  Item it;
+  it.c = idx % NC;
+  const int k = idx / NC, Tq = g.Tq;
+  const int r0 = g.row0, r1 = g.row0 + g.nrows - 1;
+  const int s_lo = r0 / Tq, s_hi = r1 / Tq, nmid = s_hi - s_lo > 1 ? s_hi - s_lo - 1 : 0;
+  const int i_start = Tq - 1 - r0 % Tq, i_end = Tq - 1 - r1 % Tq;
+  const int lo0 = s_lo == s_hi ? i_end : 0;  // segment s_lo holds i in [lo0, i_start]
+  // F(i) = slice rows with query tile >= i
+  auto F = [&](int i) {
+    int n = max(0, i_start - max(i, lo0) + 1) + nmid * (Tq - i);
+    if (s_hi != s_lo) n += Tq - max(i, i_end);
+    return n;
+  };
+  int lo = 0, hi = Tq - 1;  // largest i with F(i) > k
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (F(mid) > k) lo = mid;
+    else hi = mid - 1;
+  }
+  int j = k - (lo + 1 < Tq ? F(lo + 1) : 0);  // rank of the row among the segments holding tile lo
+  int seg;
+  if (lo >= lo0 && lo <= i_start && j == 0) seg = s_lo;
+  else {
+    if (lo >= lo0 && lo <= i_start) --j;
+    seg = j < nmid ? s_lo + 1 + j : s_hi;
+  }
+  it.i = lo;
+  it.h = seg % g.Hkv;
+  it.r = seg / g.Hkv;
+  return it;
+}
+
+template <bool SLICE>
 __device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
   // order: (r, h) major, query tile descending (longest rows first: LPT proxy), chunk inner
+  if constexpr (SLICE) return decode_slice(g, idx, NC);
   Item it;
-  if (g.nrows) {  // work slice [row0, row0 + nrows) of that order: executed in descending i with the
-                  // slice's (r, h) segments interleaved, so the longest rows still go first
-    it.c = idx % NC;
-    const int k = idx / NC, Tq = g.Tq;
-    const int r0 = g.row0, r1 = g.row0 + g.nrows - 1;
-    const int s_lo = r0 / Tq, s_hi = r1 / Tq, nmid = s_hi - s_lo > 1 ? s_hi - s_lo - 1 : 0;
-    const int i_start = Tq - 1 - r0 % Tq, i_end = Tq - 1 - r1 % Tq;
-    const int lo0 = s_lo == s_hi ? i_end : 0;  // segment s_lo holds i in [lo0, i_start]
-    // F(i) = slice rows with query tile >= i
-    auto F = [&](int i) {
-      int n = max(0, i_start - max(i, lo0) + 1) + nmid * (Tq - i);
-      if (s_hi != s_lo) n += Tq - max(i, i_end);
-      return n;
-    };
-    int lo = 0, hi = Tq - 1;  // largest i with F(i) > k
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (F(mid) > k) lo = mid;
-      else hi = mid - 1;
-    }
-    int j = k - (lo + 1 < Tq ? F(lo + 1) : 0);  // rank of the row among the segments holding tile lo
-    int seg;
-    if (lo >= lo0 && lo <= i_start && j == 0) seg = s_lo;
-    else {
-      if (lo >= lo0 && lo <= i_start) --j;
-      seg = j < nmid ? s_lo + 1 + j : s_hi;
-    }
-    it.i = lo;
-    it.h = seg % g.Hkv;
-    it.r = seg / g.Hkv;
-    return it;
-  }
   it.c = idx % NC;
   int rest = idx / NC;
   it.i = g.Tq - 1 - rest % g.Tq;
