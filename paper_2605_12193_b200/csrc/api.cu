@@ -236,8 +236,8 @@ static WsLayout ws_layout(const Geom& g) {
   o += al((size_t)g.B * g.Hkv * g.Lkv * 4);
   L.flagged = o;
   o += al((size_t)g.B * g.Hq * g.Lq * 4);
-  L.flagthr = o;
-  o += al((size_t)g.B * g.Hq * g.Lq * 4);
+  L.flagthr = o;  // [flagged row][2]: score band (lo, hi) of the blocks the recompute must redo
+  o += al((size_t)g.B * g.Hq * g.Lq * 8);
   L.nflag = o;
   o += al(16);
   L.sched = o;  // attention item counter (dynamic scheduling)

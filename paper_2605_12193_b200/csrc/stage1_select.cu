@@ -252,10 +252,17 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
         if (lane == 0) {
           const int f = atomicAdd(n_flagged, 1);
           flagged[f] = (int32_t)rowid;
-          // MASS: blocks below thr have canonical logit < -127 (exact zero probability); RATIO: blocks
-          // below thr rank below the canonical k-th score (only the cut's neighbourhood is recomputed)
-          flag_thr[f] = select == 1 ? res.s_cut - 2.0f * res.dmax * (1.0f + 0x1p-10f) - 0x1p-20f * fabsf(res.s_cut)
-                                    : res.M - 2.0f * res.dmax - 127.0f / c_alpha;
+          // Recompute band [lo, hi] of fast scores.  MASS: blocks below lo have canonical logit < -127
+          // (exact zero probability); every block above matters to the mass, so hi = +inf.  RATIO (top-k
+          // by score): with |S_f - S_canon| <= d per block, the canonical k-th score c* lies within d of
+          // s_cut (the fast k-th score), so a block with S_f > s_cut + 2d ranks above c* and one with
+          // S_f < s_cut - 2d below it, canonically as well: only the band between is recomputed, and
+          // the mixed row (fast scores outside, canonical inside) has the same top-k set, the same
+          // k-th key and the same tie at the cut as the all-canonical row.  (kept_mass, which needs
+          // every score canonical, always takes the canonical path: api.cu use_fast_scores.)
+          const float wband = 2.0f * res.dmax * (1.0f + 0x1p-10f) + 0x1p-20f * fabsf(res.s_cut);
+          flag_thr[2 * f] = select == 1 ? res.s_cut - wband : res.M - 2.0f * res.dmax - 127.0f / c_alpha;
+          flag_thr[2 * f + 1] = select == 1 ? res.s_cut + wband : INFINITY;
         }
       }
       __syncwarp();

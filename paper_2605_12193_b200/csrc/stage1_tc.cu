@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 
 // ---- canonical recompute of flagged head rows (DESIGN.md §4 item 2 order).  Work unit = (flagged head
 // row (r,p,i), KV block j) for every causal j whose score can still carry canonical probability
-// (S_f >= flag_thr: below it 2^t underflows to an exact 0 whatever the rounding).  The unit's G x G
+// (S_f inside the row's band flag_thr[2f .. 2f+1]: MASS — below it 2^t underflows to an exact 0 whatever
+// the rounding; RATIO — outside it the rank against the canonical k-th score is certain).  The unit's G x G
 // group dots are G*G*g independent token-pair chains (C-long fp32 FMA chains, channel ascending): a
 // thread runs four of them side by side straight from global memory (16-byte loads, L1/L2-resident
 // rows), the token dots land in smem, and G*G threads add them in ascending token order — the
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * g.b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
+    if (!(srow[j] >= flag_thr[2 * fidx] && srow[j] <= flag_thr[2 * fidx + 1])) continue;  // outside the band
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
     const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     // chains c = (u, v, t), t fastest: four per thread per pass
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    if (srow[j] < flag_thr[fidx]) continue;  // exactly-zero canonical probability either way
+    if (!(srow[j] >= flag_thr[2 * fidx] && srow[j] <= flag_thr[2 * fidx + 1])) continue;  // outside the band
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
     const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     const int kt0 = j * b, nkt = min(b, R.Nkv - kt0);  // valid key tokens of the block
@@ -482,7 +483,8 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
     long long e_i = (long long)R.Nc + (long long)(i + 1) * b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * b > e_i || j >= R.Lkv) return false;
-    return S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] >= flag_thr[fidx];
+    const float sf = S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j];
+    return sf >= flag_thr[2 * fidx] && sf <= flag_thr[2 * fidx + 1];
   };
   auto next_live = [&](long long from) -> long long {
     while (from < u1 && !live(from)) ++from;

@@ -204,6 +204,22 @@ def test_keep_ratio_fast_path(ratio):
     print(f"ratio {ratio}: flagged {fast['stats']['rows_flagged']} of {fast['stats']['rows']}")
 
 
+@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("ratio", [0.05, 0.3])
+def test_keep_ratio_recompute_band(monkeypatch, ratio, d):
+    """Keep-ratio rows that fail certification recompute only the blocks whose fast score lies in the
+    band s_cut -/+ 2d around the cut (stage1_select.cu): outside it the rank against the canonical
+    k-th score is already certain.  A widened error bound (BFLA_TAU_SCALE) flags most rows and widens
+    every band, so rows mix fast and canonical scores; the mask must still equal the oracle's bit for
+    bit (d = 128: TMA recompute kernel; d = 256: the global-load one)."""
+    monkeypatch.setenv("BFLA_TAU_SCALE", "3000")
+    prob = workloads.structured(10, B=1, Hq=4, Hkv=2, Nq=3072, Nkv=3072, d=d, block=256)
+    kw = dict(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=ratio)
+    fast = run_gpu(prob, bf.Config(**kw, scores=bf.SCORES_AUTO), lse=False)
+    assert fast["stats"]["rows_flagged"] >= 8, fast["stats"]
+    _check_masks(fast, oracle_masks(prob, bf.Config(**kw)), None)
+
+
 @pytest.mark.parametrize("paged", [0, 16])
 def test_dynamic_and_static_item_order_identical(paged):
     """The prefill kernels take their work items from a workspace counter when a workspace is given
