@@ -208,7 +208,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
 
 // ---- workspace layout -------------------------------------------------------------------------
 struct WsLayout {
-  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, flagthr, nflag, sched, kgather, total;
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, units, nflag, sched, kgather, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Geom& g) {
@@ -236,8 +236,8 @@ static WsLayout ws_layout(const Geom& g) {
   o += al((size_t)g.B * g.Hkv * g.Lkv * 4);
   L.flagged = o;
   o += al((size_t)g.B * g.Hq * g.Lq * 4);
-  L.flagthr = o;  // [flagged row][2]: score band (lo, hi) of the blocks the recompute must redo
-  o += al((size_t)g.B * g.Hq * g.Lq * 8);
+  L.units = o;  // recompute units (flagged row, KV block) of every flagged row's band, int32
+  o += al((size_t)g.B * g.Hq * g.Lq * g.Lkv * 4);
   L.nflag = o;
   o += al(16);
   L.sched = o;  // attention item counter (dynamic scheduling)
@@ -293,7 +293,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     float* kn = reinterpret_cast<float*>(ws + L.kn);
     int32_t* flagged = reinterpret_cast<int32_t*>(ws + L.flagged);
     int32_t* nflag = reinterpret_cast<int32_t*>(ws + L.nflag);
-    float* fthr = reinterpret_cast<float*>(ws + L.flagthr);
+    int32_t* ulist = reinterpret_cast<int32_t*>(ws + L.units);
     const void* kc = P->k;
     Geom gk = g;  // geometry of the K operand as the score kernels see it (gathered = contiguous)
     if (g.paged) {
@@ -336,11 +336,11 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     }
     if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st))
       return fail(BFLA_ERR_CUDA, "tc scores launch failed");
-    cudaMemsetAsync(nflag, 0, sizeof(int32_t), st);
+    cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);
     const int sms = num_sms_current();
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
-                  1, qn, kn, certify_tau(g), flagged, nflag, sms, fthr);
+                  1, qn, kn, certify_tau(g), flagged, nflag, sms, ulist);
     CUtensorMap rq, rk;  // token-row maps (64 x 64 SW128 boxes) for the TMA-staged recompute
     bool rmaps;
     {
@@ -351,7 +351,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, 64, 1, 1};
       rmaps = encode_4d_quiet(&rq, P->q, dq, sq, box) && encode_4d_quiet(&rk, kc, dk, sk, box);
     }
-    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, fthr, S, sms, st, rmaps ? &rq : nullptr,
+    if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, ulist, nflag + 1, S, sms, st, rmaps ? &rq : nullptr,
                               rmaps ? &rk : nullptr))
       return fail(BFLA_ERR_CUDA, "recompute launch failed");
     launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,

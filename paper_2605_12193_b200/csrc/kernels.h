@@ -21,7 +21,7 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
                    uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st, int mode = 0,
                    const float* qn = nullptr, const float* kn = nullptr, float tau = 0.f,
                    int32_t* flagged = nullptr, int32_t* n_flagged = nullptr, int num_sms = 148,
-                   float* flag_thr = nullptr);
+                   int32_t* ulist = nullptr);
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
 constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
@@ -33,7 +33,8 @@ void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, 
                         bool with_q = true);
 // tmQ / tmK (optional): {D, N, H, B} maps with 64 x 64 SW128 boxes for the TMA-staged variant
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st,
+                          const int32_t* n_flagged, const int32_t* ulist, const int32_t* n_units, float* S,
+                          int num_sms, cudaStream_t st,
                           const CUtensorMap* tmQ = nullptr, const CUtensorMap* tmK = nullptr);
 void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, void* kout, cudaStream_t st);
 // Stage 2 (Eq. 19-26)

@@ -55,7 +55,33 @@ struct RowResult {
   bool tie, certified;
   float M, dmax;  // fast row max and largest score-error bound (mode 1)
   float s_cut;    // RATIO: fast score of the last kept block (mode 1)
+  float band_lo, band_hi;  // RATIO, uncertified row: fast-score band that needs canonical scores
 };
+
+// Order-preserving uint32 key of a float (larger float -> larger key).
+__device__ __forceinline__ uint32_t okey(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float okey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+// k-th largest of f(j), j < nc, over a warp (bisection on the order-preserving keys: 32 rounds).
+template <class F>
+__device__ float warp_kth_largest(int nc, int k, F f) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0u, hi = 0xffffffffu;  // largest key t with #{j : key_j >= t} >= k
+  while (lo < hi) {
+    const uint32_t mid = lo + (uint32_t)(((unsigned long long)hi - lo + 1ull) >> 1);
+    int cnt = 0;
+    for (int j = lane; j < nc; j += 32) cnt += okey(f(j)) >= mid;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (cnt >= k) lo = mid;
+    else hi = mid - 1u;
+  }
+  return okey_inv(lo);
+}
 
 __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int nc, float c_alpha, int select,
                                 float gamma, float keep_ratio, unsigned long long* keys, bool certify, float qnorm,
@@ -129,7 +155,7 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     if (keep_all) continue;
     if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
   }
-  RowResult res{nsel, P, false, true, M, 0.f, 0.f};
+  RowResult res{nsel, P, false, true, M, 0.f, 0.f, 0.f, 0.f};
   if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
@@ -172,6 +198,26 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     res.certified = ok;
     res.dmax = dmax;
     res.s_cut = s_last;
+    if (select == 1 && !ok) {
+      // Recompute band of an uncertified RATIO row.  Canonical scores c_j lie in [S_j - d_j, S_j + d_j]
+      // (d_j = tau |q| |k_j|), so the canonical k-th score c* lies in [L, U] with L / U the k-th largest
+      // of S_j - d_j / S_j + d_j (order statistics are monotone).  With d_b = max d_j over the blocks
+      // whose S_j lies in [L - dmax, U + dmax]: S_j > U + d_b implies c_j > c* and S_j < L - d_b implies
+      // c_j < c* (a block with d_j > d_b lies outside [L - dmax, U + dmax]), so only [L - d_b, U + d_b]
+      // needs canonical scores; outside it the mixed row ranks exactly like the canonical one (c* is
+      // attained inside the band, every outside value is strictly above or below it).  The per-block d_j
+      // keeps one large-norm block (an attention sink) from widening every row's band.
+      const float U = warp_kth_largest(nc, nsel, [&](int j) { return s[j] + tau * qnorm * knrow[j]; });
+      const float L = warp_kth_largest(nc, nsel, [&](int j) { return s[j] - tau * qnorm * knrow[j]; });
+      float db = 0.f;
+      for (int j = lane; j < nc; j += 32)
+        if (s[j] >= L - dmax && s[j] <= U + dmax) db = fmaxf(db, tau * qnorm * knrow[j]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) db = fmaxf(db, __shfl_xor_sync(0xffffffffu, db, o));
+      db *= 1.0f + 0x1p-10f;  // fp32 rounding of S_j -/+ d_j and of the products
+      res.band_lo = L - db - 0x1p-20f * fabsf(L);
+      res.band_hi = U + db + 0x1p-20f * fabsf(U);
+    }
   }
   return res;
 }
@@ -198,7 +244,7 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
                                                    unsigned long long* __restrict__ stats, int mode,
                                                    const float* __restrict__ qn, const float* __restrict__ kn,
                                                    float tau, int32_t* __restrict__ flagged,
-                                                   int32_t* __restrict__ n_flagged, float* __restrict__ flag_thr) {
+                                                   int32_t* __restrict__ n_flagged, int32_t* __restrict__ ulist) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -247,22 +293,34 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
         if (kept_mass && lane == 0) kept_mass[rowid] = res.P;
       } else {
         unc++;
-        // blocks with S_f < thr have canonical logit < -127 (exp2_canon = 0 exactly): only the others
-        // need canonical scores (k_s1_recompute_rows skips the rest)
+        // Recompute band [lo, hi] of fast scores.  MASS: blocks below lo have canonical logit < -127
+        // (exact zero probability); every block above matters to the mass, so hi = +inf.  RATIO (top-k
+        // by score): the band of select_row — outside it the rank against the canonical k-th score is
+        // certain, and the mixed row (fast scores outside, canonical inside) has the same top-k set,
+        // k-th key and tie at the cut as the all-canonical row.  (kept_mass, which needs every score
+        // canonical, always takes the canonical path: api.cu use_fast_scores.)  The row's band blocks
+        // are listed contiguously in ulist as fidx * Lkv + j (n_flagged[1] counts them), so the
+        // recompute kernels never scan dead units.
+        const float lo = select == 1 ? res.band_lo : res.M - 2.0f * res.dmax - 127.0f / c_alpha;
+        const float hi = select == 1 ? res.band_hi : INFINITY;
+        int cnt = 0;
+        for (int j = lane; j < nc; j += 32) cnt += s[j] >= lo && s[j] <= hi;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        int f = 0, base = 0;
         if (lane == 0) {
-          const int f = atomicAdd(n_flagged, 1);
+          f = atomicAdd(n_flagged, 1);
+          base = atomicAdd(n_flagged + 1, cnt);
           flagged[f] = (int32_t)rowid;
-          // Recompute band [lo, hi] of fast scores.  MASS: blocks below lo have canonical logit < -127
-          // (exact zero probability); every block above matters to the mass, so hi = +inf.  RATIO (top-k
-          // by score): with |S_f - S_canon| <= d per block, the canonical k-th score c* lies within d of
-          // s_cut (the fast k-th score), so a block with S_f > s_cut + 2d ranks above c* and one with
-          // S_f < s_cut - 2d below it, canonically as well: only the band between is recomputed, and
-          // the mixed row (fast scores outside, canonical inside) has the same top-k set, the same
-          // k-th key and the same tie at the cut as the all-canonical row.  (kept_mass, which needs
-          // every score canonical, always takes the canonical path: api.cu use_fast_scores.)
-          const float wband = 2.0f * res.dmax * (1.0f + 0x1p-10f) + 0x1p-20f * fabsf(res.s_cut);
-          flag_thr[2 * f] = select == 1 ? res.s_cut - wband : res.M - 2.0f * res.dmax - 127.0f / c_alpha;
-          flag_thr[2 * f + 1] = select == 1 ? res.s_cut + wband : INFINITY;
+        }
+        f = __shfl_sync(0xffffffffu, f, 0);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int j0 = 0; j0 < nc; j0 += 32) {
+          const int j = j0 + lane;
+          const bool in = j < nc && s[j] >= lo && s[j] <= hi;
+          const uint32_t bal = __ballot_sync(0xffffffffu, in);
+          if (in) ulist[base + __popc(bal & ((1u << lane) - 1u))] = f * g.Lkv + j;
+          base += __popc(bal);
         }
       }
       __syncwarp();
@@ -287,14 +345,14 @@ size_t select_smem_bytes(const Geom& g, int nwarps) {
 void launch_select(const Geom& g, const float* S, float c_alpha, int select, float gamma, float keep_ratio,
                    uint32_t* coarse, float* kept_mass, unsigned long long* stats, cudaStream_t st, int mode,
                    const float* qn, const float* kn, float tau, int32_t* flagged, int32_t* n_flagged, int num_sms,
-                   float* flag_thr) {
+                   int32_t* ulist) {
   const int nwarps = g.m < 4 ? g.m : 4;
   const size_t smem = select_smem_bytes(g, nwarps);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_s1_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int rows = g.B * g.Hkv * g.Lq;
   const int grid = mode == 2 ? num_sms : rows;
   k_s1_select<<<grid, nwarps * 32, smem, st>>>(g, S, c_alpha, select, gamma, keep_ratio, coarse, kept_mass, stats,
-                                               mode, qn, kn, tau, flagged, n_flagged, flag_thr);
+                                               mode, qn, kn, tau, flagged, n_flagged, ulist);
   count_launch();
 }
 

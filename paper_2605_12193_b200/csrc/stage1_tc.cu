@@ -239,8 +239,8 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 
 // ---- canonical recompute of flagged head rows (DESIGN.md §4 item 2 order).  Work unit = (flagged head
 // row (r,p,i), KV block j) for every causal j whose score can still carry canonical probability
-// (S_f inside the row's band flag_thr[2f .. 2f+1]: MASS — below it 2^t underflows to an exact 0 whatever
-// the rounding; RATIO — outside it the rank against the canonical k-th score is certain).  The unit's G x G
+// (S_f inside the row's band, listed by k_s1_select: MASS — below it 2^t underflows to an exact 0
+// whatever the rounding; RATIO — outside it the rank against the canonical k-th score is certain).  The unit's G x G
 // group dots are G*G*g independent token-pair chains (C-long fp32 FMA chains, channel ascending): a
 // thread runs four of them side by side straight from global memory (16-byte loads, L1/L2-resident
 // rows), the token dots land in smem, and G*G threads add them in ascending token order — the
@@ -262,15 +262,17 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
                                                                    const __nv_bfloat16* __restrict__ k,
                                                                    const int32_t* __restrict__ flagged,
                                                                    const int32_t* __restrict__ n_flagged,
-                                                                   const float* __restrict__ flag_thr,
+                                                                   const int32_t* __restrict__ ulist,
+                                                                   const int32_t* __restrict__ n_units,
                                                                    float* __restrict__ S) {
   extern __shared__ float tokdot[];  // [G*G][g] token dots of the current unit
-  const int nf = *n_flagged;
+  (void)n_flagged;
   const int G = g.G, gg = g.g, nch = G * G * gg;
-  const long long units = (long long)nf * g.Lkv;
-  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
-    const int j = (int)(unit % g.Lkv);
-    const int fidx = (int)(unit / g.Lkv);
+  const int nunits = *n_units;
+  for (int uidx = blockIdx.x; uidx < nunits; uidx += gridDim.x) {
+    const int unit = ulist[uidx];  // fidx * Lkv + j (k_s1_select: the row's recompute band)
+    const int j = unit % g.Lkv;
+    const int fidx = unit / g.Lkv;
     const int row = flagged[fidx];  // (r * Hq + p) * Lq + i
     const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
     const int h = p / g.m;
@@ -279,7 +281,6 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * g.b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    if (!(srow[j] >= flag_thr[2 * fidx] && srow[j] <= flag_thr[2 * fidx + 1])) continue;  // outside the band
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
     const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     // chains c = (u, v, t), t fastest: four per thread per pass
@@ -350,7 +351,8 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const
                                                                    const __nv_bfloat16* __restrict__ k,
                                                                    const int32_t* __restrict__ flagged,
                                                                    const int32_t* __restrict__ n_flagged,
-                                                                   const float* __restrict__ flag_thr,
+                                                                   const int32_t* __restrict__ ulist,
+                                                                   const int32_t* __restrict__ n_units,
                                                                    float* __restrict__ S) {
   constexpr int PITCH = D * 2 + 16;  // bytes per staged token row
   extern __shared__ __align__(16) unsigned char rs[];
@@ -366,11 +368,12 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const
   }
   __syncthreads();
   uint32_t ph[3] = {0, 0, 0};
-  const int nf = *n_flagged;
-  const long long units = (long long)nf * g.Lkv;
-  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
-    const int j = (int)(unit % g.Lkv);
-    const int fidx = (int)(unit / g.Lkv);
+  (void)n_flagged;
+  const int nunits = *n_units;
+  for (int uidx = blockIdx.x; uidx < nunits; uidx += gridDim.x) {
+    const int unit = ulist[uidx];  // fidx * Lkv + j (k_s1_select: the row's recompute band)
+    const int j = unit % g.Lkv;
+    const int fidx = unit / g.Lkv;
     const int row = flagged[fidx];  // (r * Hq + p) * Lq + i
     const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
     const int h = p / g.m;
@@ -379,7 +382,6 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_smem(Geom g, const
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    if (!(srow[j] >= flag_thr[2 * fidx] && srow[j] <= flag_thr[2 * fidx + 1])) continue;  // outside the band
     const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
     const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
     const int kt0 = j * b, nkt = min(b, R.Nkv - kt0);  // valid key tokens of the block
@@ -453,7 +455,8 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
                                                                   const __grid_constant__ CUtensorMap tmK, Geom g,
                                                                   const int32_t* __restrict__ flagged,
                                                                   const int32_t* __restrict__ n_flagged,
-                                                                  const float* __restrict__ flag_thr,
+                                                                  const int32_t* __restrict__ ulist,
+                                                                  const int32_t* __restrict__ n_units,
                                                                   float* __restrict__ S) {
   constexpr int NCH = D / 64;  // 64-column chunks per token row
   extern __shared__ __align__(1024) unsigned char rs_raw[];
@@ -470,35 +473,22 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
     fence_barrier_init();
   }
   __syncthreads();
-  const int nf = *n_flagged;
-  const long long units = (long long)nf * g.Lkv;
+  // the units (flagged row, KV block) of every row's recompute band, listed row by row by k_s1_select:
+  // an even contiguous share per CTA, no scanning of dead units
+  const long long units = *n_units;
   const long long per = (units + gridDim.x - 1) / gridDim.x;
   const long long u0 = (long long)blockIdx.x * per, u1 = min(units, u0 + per);
-  // a unit is live if causal and its score can still carry canonical probability (uniform test)
-  auto live = [&](long long unit) -> bool {
-    const int j = (int)(unit % g.Lkv), fidx = (int)(unit / g.Lkv);
-    const int row = flagged[fidx];
-    const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
-    const Req R = req_of(g, r);
-    long long e_i = (long long)R.Nc + (long long)(i + 1) * b - 1;
-    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
-    if ((long long)j * b > e_i || j >= R.Lkv) return false;
-    const float sf = S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j];
-    return sf >= flag_thr[2 * fidx] && sf <= flag_thr[2 * fidx + 1];
-  };
-  auto next_live = [&](long long from) -> long long {
-    while (from < u1 && !live(from)) ++from;
-    return from;
-  };
+  auto next_live = [&](long long from) -> long long { return from; };
   auto load_block = [&](unsigned char* dst, const CUtensorMap* map, uint64_t* br, int t0, int hh, int r) {
     mbar_arrive_expect_tx(br, (uint32_t)blk_bytes);
     for (int rt = 0; rt < nrt; ++rt)
       for (int cc = 0; cc < NCH; ++cc)
         tma_load_4d(dst + (rt * NCH + cc) * 8192, map, br, cc * 64, t0 + rt * 64, hh, r);
   };
-  auto decode = [&](long long unit, int& j, int& i, int& p, int& r, int& fidx) {
-    j = (int)(unit % g.Lkv);
-    fidx = (int)(unit / g.Lkv);
+  auto decode = [&](long long uidx, int& j, int& i, int& p, int& r, int& fidx) {
+    const int unit = ulist[uidx];
+    j = unit % g.Lkv;
+    fidx = unit / g.Lkv;
     const int row = flagged[fidx];
     i = row % g.Lq;
     p = (row / g.Lq) % g.Hq;
@@ -637,7 +627,8 @@ void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, 
 }
 
 int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int32_t* pt, const int32_t* flagged,
-                          const int32_t* n_flagged, const float* flag_thr, float* S, int num_sms, cudaStream_t st,
+                          const int32_t* n_flagged, const int32_t* ulist, const int32_t* n_units, float* S,
+                          int num_sms, cudaStream_t st,
                           const CUtensorMap* tmQ, const CUtensorMap* tmK) {
   (void)pt;
   if (g.G * g.G > kRecThreads) return -1;
@@ -652,7 +643,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
     if (mode == 0 && tmQ && tmK && g.D == 128 && g.G <= 8 && g.b % 64 == 0 && smem_t <= 226 * 1024) {
       auto kern = k_s1_recompute_tma<128>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
-      kern<<<num_sms, kRecThreads, smem_t, st>>>(*tmQ, *tmK, g, flagged, n_flagged, flag_thr, S);
+      kern<<<num_sms, kRecThreads, smem_t, st>>>(*tmQ, *tmK, g, flagged, n_flagged, ulist, n_units, S);
       count_launch();
       return (int)cudaGetLastError();
     }
@@ -665,7 +656,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRecThreads, smem_s);
-      kern<<<num_sms * (per_sm > 0 ? per_sm : 1), kRecThreads, smem_s, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
+      kern<<<num_sms * (per_sm > 0 ? per_sm : 1), kRecThreads, smem_s, st>>>(g, qq, kk, flagged, n_flagged, ulist, n_units, S);
     };
     if (g.D == 128) gs(k_s1_recompute_smem<128>);
     else if (g.D == 256) gs(k_s1_recompute_smem<256>);
@@ -676,7 +667,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
   const int smem = (g.G * g.G * g.g + g.G * g.G) * 4;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<num_sms * 4, kRecThreads, smem, st>>>(g, qq, kk, flagged, n_flagged, flag_thr, S);
+    kern<<<num_sms * 4, kRecThreads, smem, st>>>(g, qq, kk, flagged, n_flagged, ulist, n_units, S);
   };
   if (g.D == 128) go(k_s1_recompute_rows<128>);
   else if (g.D == 256) go(k_s1_recompute_rows<256>);

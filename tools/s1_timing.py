@@ -13,14 +13,16 @@ import workloads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=32768)
 ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--hkv", type=int, default=8)
+ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--ratio", type=float, default=0.0, help="keep-ratio selection (R9) instead of gamma")
 a = ap.parse_args()
-prob = workloads.structured(303, 1, a.hq, 8, a.n, a.n, 128, block=256, theta=5e5, device="cuda")
+prob = workloads.structured(303, 1, a.hq, a.hkv, a.n, a.n, a.d, block=256, theta=5e5, device="cuda")
 o = torch.empty_like(prob.q)
 cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, n_local=8, eta=16, rho=0.0)
 if a.ratio > 0:
-    cfg = bf.Config(b=256, g=64, T=64, select=bf.SELECT_RATIO, keep_ratio=a.ratio, n_local=8, eta=16)
+    cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, select=bf.SELECT_RATIO, keep_ratio=a.ratio, n_local=8, eta=16)
 P = bf.make_problem(prob.q, prob.k, prob.v, o)
 ws = bf.alloc_workspace(P, cfg)
 m = bf.alloc_mask(P, cfg)
