@@ -144,7 +144,7 @@ def run_ours(args, w, rank, world, local_rank):
         q, k, v = prob.q, prob.k, prob.v
         head_offset = rank * Hkv
     o = torch.empty_like(q)
-    cfg = bf.Config(b=w["b"], g=w["g"], T=64, gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"],
+    cfg = bf.Config(b=w["b"], g=w["g"], T=w["T"], gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"],
                     pool=bf.POOL_MEAN if args.pool == "mean" else bf.POOL_FLATTEN)
     if w["paged"]:
         kc, vc, pt = workloads.paged(k, v, w["paged"], seed=404 + rank)
@@ -320,7 +320,7 @@ def run_ours(args, w, rank, world, local_rank):
         cnt = layer.counts_host.view(-1, layer.counts_host.shape[-1])  # [B*Hkv, Tq]
         Tq_ = cnt.shape[1]
         kept = sum(int(cnt[rho // Tq_, Tq_ - 1 - rho % Tq_]) for rho in range(r0, r1))
-    retained_flops = 4.0 * d * m_ * 64 * 64 * kept  # per launch: every kept (h, i, j) tile, m heads, QK^T + PV
+    retained_flops = 4.0 * d * m_ * w["T"] * w["T"] * kept  # per launch: every kept (h, i, j) tile, m heads, QK^T + PV
     achieved_tf = retained_flops / (at * 1e-3) / 1e12
     dense_flops = 4.0 * d * Hq * N * (N + 1) / 2
     dense_tf = dense_flops / (dense_ms * 1e-3) / 1e12
@@ -357,14 +357,14 @@ def cpu_baseline(w, small: bool = False, prob=None):
         v = prob.v[0].float().numpy()
     oracle.build()
     t0 = time.perf_counter()
-    r = oracle.mask_pipeline(q, k, b=w["b"], g=w["g"], T=64, gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"],
+    r = oracle.mask_pipeline(q, k, b=w["b"], g=w["g"], T=w["T"], gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"],
                              rho=w["rho"])
     t_mask = time.perf_counter() - t0
     N, Hq = w["N"], q.shape[0]
     stride = 64 if small else 2
     rows = np.array([[p, t] for p in range(Hq) for t in range(0, N, stride)], np.int32)
     t0 = time.perf_counter()
-    oracle.masked_attention(q, k, v, 1 / math.sqrt(w["d"]), r["labels"], 64, rows)
+    oracle.masked_attention(q, k, v, 1 / math.sqrt(w["d"]), r["labels"], w["T"], rows)
     t_attn = time.perf_counter() - t0
     heads = w["Hkv"] if small else 1
     layer_ms = (t_mask + t_attn * stride) * heads * 1e3
@@ -386,18 +386,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama8b-32k", choices=sorted(WORKLOADS))
     ap.add_argument("--pool", default="flatten", choices=["flatten", "mean"])
+    ap.add_argument("--tile", type=int, default=64, choices=[64, 128], help="mask tile T (Eq. 19)")
     ap.add_argument("--shard", default="layers", choices=["layers", "heads", "balanced"],
                     help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O "
                          "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
                          "slices + O all-reduce (strong, SURVEY §8 f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    w = WORKLOADS[args.workload]
+    w = dict(WORKLOADS[args.workload], T=args.tile)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     config = {"workload": args.workload, "h_q": w["Hq"], "h_kv": w["Hkv"], "head_dim": w["d"], "n": w["N"],
-              "b": w["b"], "g": w["g"], "T": 64, "gamma": w["gamma"], "n_local": w["n_local"], "eta": w["eta"],
+              "b": w["b"], "g": w["g"], "T": w["T"], "gamma": w["gamma"], "n_local": w["n_local"], "eta": w["eta"],
               "rho": w["rho"], "pool": args.pool, "kv": f"paged{w['paged']}" if w["paged"] else "contiguous",
               "inputs": "structured synthetic (sinks+local+scattered heavy blocks), seed 303+rank",
               "l2": "no flush: per-layer inputs Q+K+V+O exceed the 126 MB L2" if w["N"] >= 16384 else "small",
@@ -459,7 +460,7 @@ def main():
             "roofline": {"bound": "tensor", "achieved": r["achieved_tf"], "peak": peaks["bf16"], "unit": "TFLOP/s",
                          "frac": r["achieved_tf"] / peaks["bf16"], "traffic": r["traffic"],
                          "kernel": "k_attn (sparse prefill)", "peak_src": peaks["src"] + " burst bf16",
-                         "algorithmic": "4*d*m*64*64 flop per kept (r,h,i,j) tile"},
+                         "algorithmic": f"4*d*m*{w['T']}*{w['T']} flop per kept (r,h,i,j) tile"},
             "e2e": {"value": r["e2e_ms"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
                     "d2h_bytes_per_step": r["d2h"]},
             "gpu_launches": r["launches"],

@@ -104,7 +104,7 @@ typedef struct {
 typedef struct {
     int32_t block_b;    /* b: coarse block size (Eq. 4), power of two                                   */
     int32_t group_g;    /* g: flattening group (Eq. 6), power of two dividing b; G = b/g <= 8 built    */
-    int32_t tile_t;     /* T: attention tile (Eq. 19), divides b; 64 built                              */
+    int32_t tile_t;     /* T: attention tile (Eq. 19), divides b; 64 and 128 built                      */
     int32_t pool;       /* BFLA_POOL_*                                                                  */
     int32_t select;     /* BFLA_SELECT_*                                                                */
     float gamma;        /* mass threshold (Eq. 17), (0, 1]; 1 keeps every causal block (R7)           */

@@ -175,7 +175,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
     if (!(cfg->rho >= 0.f && cfg->rho <= 1.f)) return fail(BFLA_ERR_INVALID_ARGUMENT, "rho must be in [0, 1] (Eq. 25)");
     if (cfg->eta < 0 || cfg->n_local < 0 || cfg->n_sink < 0)
       return fail(BFLA_ERR_INVALID_ARGUMENT, "eta, n_local, n_sink must be >= 0");
-    if (T != 64) return fail(BFLA_ERR_UNSUPPORTED, "tile_t %d not built (64)", T);
+    if (T != 64 && T != 128) return fail(BFLA_ERR_UNSUPPORTED, "tile_t %d not built (64, 128)", T);
     if (cfg->pool == BFLA_POOL_FLATTEN && b / gg > 8)
       return fail(BFLA_ERR_UNSUPPORTED, "G = b/g = %d > 8 not built for FLATTEN", b / gg);
     if (cfg->mask_groups != BFLA_MASK_PER_KV_HEAD && cfg->mask_groups != BFLA_MASK_PER_Q_HEAD)

@@ -125,11 +125,17 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int heads_in_chunk = NQT * hpq;
 
+  // 64-key tiles (BN); a T = 128 mask tile is two of them (see attention2.cu)
+  const int TR = g.T / BN;
   auto row_count = [&](const Item& it) -> int {
     const Req R = req_of(g, it.r);
     if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
-    if (DENSE) return (int)req_row_count(R, g.T, it.i);
-    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+    if (DENSE) return (int)req_row_count(R, g.T, it.i) * TR;
+    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i] * TR;
+  };
+  auto tile64 = [&](const int32_t* lst, int n) -> int {  // n-th 64-key tile of the row, ascending
+    if (DENSE) return n;
+    return TR == 1 ? __ldg(lst + n) : 2 * __ldg(lst + (n >> 1)) + (n & 1);
   };
   // Item sequence (as attention2.cu): the Q/K producer takes the CTA's first item statically and the
   // next ones from a global counter (longest-first greedy list scheduling) or round-robin without one,
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         for (int q = 0; q < NQT; ++q)
           for (int s = 0; s < hpq; ++s)
             if (it.c * heads_in_chunk + q * hpq + s < g.m) nq_boxes += D / 64;
-        mbar_arrive_expect_tx(q_full, nq_boxes * 64 * 64 * 2);
+        mbar_arrive_expect_tx(q_full, nq_boxes * 64 * g.T * 2);
         for (int q = 0; q < NQT; ++q)
           for (int s = 0; s < hpq; ++s) {
             const int pl = it.c * heads_in_chunk + q * hpq + s;
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
             }
         }
         for (int n = 0; n < cnt; ++n, ++kv) {
-          const int j = DENSE ? n : lst[n];
+          const int j = tile64(lst, n);
           load_kv(0, kv, j, it);
         }
         idx = nidx;
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         const Item it = decode_item<SLICE>(g, idx, NC);
         if (cnt == 0) continue;
         const int32_t* lst = DENSE ? nullptr : row_list(it);
-        for (int n = 0; n < cnt; ++n, ++kv) load_kv(1, kv, DENSE ? n : lst[n], it);
+        for (int n = 0; n < cnt; ++n, ++kv) load_kv(1, kv, tile64(lst, n), it);
       }
     }
   } else if (warp == 1) {
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
       const int32_t* lst = DENSE ? nullptr : row_list(it);
       float m_run = -INFINITY, l_run = 0.0f;
       for (int n = 0; n < cnt; ++n, ++tc) {
-        const int j = DENSE ? n : __ldg(lst + n);
+        const int j = tile64(lst, n);
         mbar_wait(s_full + 2 * q + (tc & 1), (tc >> 1) & 1);
         tc_fence_after();
         float s[NCOL];

@@ -163,11 +163,14 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
   int tr_n[kTraceRoles] = {0, 0, 0, 0, 0, 0};
 #endif
 
+  // The kernel works in 64-key tiles (BN); a mask tile of T = 128 is two of them,
+  // so counts scale by TR = T / 64 and the n-th 64-key tile of a row is half (n & 1) of list entry n / 2
+  const int TR = g.T / BN;
   auto row_count = [&](const Item& it) -> int {
     const Req R = req_of(g, it.r);
     if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
-    if (DENSE) return (int)req_row_count(R, g.T, it.i);
-    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+    if (DENSE) return (int)req_row_count(R, g.T, it.i) * TR;
+    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i] * TR;
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
     return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
@@ -175,7 +178,9 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
   // tiles are visited in DESCENDING j (diagonal / local band first): the largest scores usually sit
   // near the diagonal, so the running max settles on the first step and the lazy-max fast path holds
   auto tile_at_c = [&](const int32_t* lst, int cnt, int n) -> int {
-    return DENSE ? cnt - 1 - n : __ldg(lst + (cnt - 1 - n));
+    const int pos = cnt - 1 - n;  // ascending position among the row's 64-key tiles
+    if (DENSE) return pos;
+    return TR == 1 ? __ldg(lst + pos) : 2 * __ldg(lst + (pos >> 1)) + (pos & 1);
   };
   // Item sequence.  The K producer (furthest ahead) picks items — the CTA's first is blockIdx.x, the
   // next ones come from a global counter (greedy longest-first list scheduling: items are ordered by
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
           int nb = 0;
           for (int s = 0; s < hpq; ++s)
             if (it.c * heads_in_chunk + q * hpq + s < g.m) nb += D / 64;
-          mbar_arrive_expect_tx(q_full + qsl, nb * 64 * 64 * 2);
+          mbar_arrive_expect_tx(q_full + qsl, nb * 64 * g.T * 2);
         }
         __syncwarp();
         {  // lane = (head slot, d-chunk)

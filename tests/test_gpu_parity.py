@@ -190,6 +190,29 @@ def test_per_query_head_masks(case):
     assert np.abs(gpu["lse"][0].cpu().numpy() - lse_ref).max() <= 1e-3
 
 
+@pytest.mark.parametrize("case", [
+    dict(B=2, Hq=8, Hkv=2, Nq=1000, Nkv=1000, d=128, b=256, g=64, paged=0),   # m=4: 2 chunks of 1 head x 128 rows
+    dict(B=1, Hq=8, Hkv=1, Nq=700, Nkv=1500, d=128, b=256, g=64, paged=16),   # chunked prefill, paged, m=8
+    dict(B=1, Hq=2, Hkv=2, Nq=1111, Nkv=1111, d=128, b=128, g=64, paged=0),   # m=1, T = b
+    dict(B=1, Hq=4, Hkv=2, Nq=900, Nkv=900, d=256, b=256, g=64, paged=0),     # d=256 kernel
+])
+def test_tile_128(case):
+    """T = 128 mask tiles: Stage 2 at T = 128 and the prefill kernels, which run
+    each kept 128-key tile as two 64-key halves and 128-row Q tiles of one head; bit-exact masks and O
+    within tolerance against the oracle at the same T, ragged tails included."""
+    c = dict(case)
+    b, g, d, paged = c.pop("b"), c.pop("g"), c.pop("d"), c.pop("paged")
+    prob = workloads.gaussian(21, d=d, sigma=0.8, **c)
+    cfg = bf.Config(b=b, g=g, T=128, gamma=0.95, eta=4, rho=0.2, seed=7)
+    gpu = run_gpu(prob, cfg, paged_page=paged)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    check_lists(gpu, labels, c["Nq"], c["Nkv"], 128)
+    for r, (o_ref, lse_ref) in enumerate(oracle_attention(prob, labels, 128)):
+        compare_o(gpu["o"][r], o_ref, str(case))
+        assert np.abs(gpu["lse"][r].cpu().numpy() - lse_ref).max() <= 1e-3
+
+
 @pytest.mark.parametrize("ratio", [0.05, 0.2, 0.6])
 def test_keep_ratio_fast_path(ratio):
     """Keep-ratio (R9, ranked by score) on the tensor-core path: certification by the score gap at the
