@@ -3,7 +3,7 @@
   c2  Llama-3.1-8B layer at 32K: gamma in {0.9, 0.95, 0.99, 0.999} x eta in {off, 16}
   c5  Gemma-like global layer (16 Q / 8 KV heads, d = 256): N in {4K ... 128K} x sparsity knobs —
       eta in {off, 32, 16, 8} (rho 0), rho in {0.1, 0.2} (eta 16), keep_ratio in {0.05, 0.1, 0.2, 0.4}
-      (T = 64: T = 128 is not built)
+      (--tile 64 or 128)
 
 For every point: kappa (kept / causal tiles, R20), layer ms = Stage 1 + Stage 2 + sparse prefill
 (median with p10 / p90 of --reps back-to-back layers; inputs exceed L2 from 32K up), the stage split,
@@ -87,6 +87,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=None)
     ap.add_argument("--max-n", type=int, default=131072)
+    ap.add_argument("--tile", type=int, default=64, choices=[64, 128], help="mask tile T")
     a = ap.parse_args()
     rows = []
     if a.set == "c2":
@@ -94,7 +95,7 @@ def main():
         dm = dense_ms(P)
         for eta in (0, 16):
             for gamma in (0.9, 0.95, 0.99, 0.999):
-                cfg = bf.Config(b=256, g=64, T=64, gamma=gamma, n_local=8, eta=eta, rho=0.0)
+                cfg = bf.Config(b=256, g=64, T=a.tile, gamma=gamma, n_local=8, eta=eta, rho=0.0)
                 r = run_point(P, cfg, a.reps)
                 r.update(set="c2", N=32768, knob=f"gamma={gamma} eta={eta or 'off'}", dense_ms=dm,
                          speedup=dm / r["ms"])
@@ -111,14 +112,15 @@ def main():
             knobs += [(f"keep_ratio={kr}", dict(eta=16, rho=0.0, select=bf.SELECT_RATIO, keep_ratio=kr))
                       for kr in (0.05, 0.1, 0.2, 0.4)]
             for name, kw in knobs:
-                cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, n_local=8, **kw)
+                cfg = bf.Config(b=256, g=64, T=a.tile, gamma=0.99, n_local=8, **kw)
                 r = run_point(P, cfg, a.reps)
                 r.update(set="c5", N=N, knob=name, dense_ms=dm, speedup=dm / r["ms"])
                 rows.append(r)
                 print(json.dumps(r), flush=True)
             del prob, P, o
             torch.cuda.empty_cache()
-    lines = [f"# §8(d) sweep {a.set} (B200, synthetic structured inputs; median of {a.reps} layers, p10/p90)", "",
+    lines = [f"# §8(d) sweep {a.set}, T = {a.tile} (B200, synthetic structured inputs; median of {a.reps} layers, "
+             "p10/p90)", "",
              "| N | knob | κ | layer ms (p10–p90) | Stage 1 | Stage 2 | prefill | dense ms | speedup | rows flagged |",
              "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
