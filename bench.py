@@ -183,7 +183,20 @@ def run_ours(args, w, rank, world, local_rank):
     stats = m.stats_dict()
     kappa = stats["kept_tiles"] / max(1, stats["causal_tiles"])
 
-    # ---- timed region: exactly K steps, per-stage events on the launching stream ----
+    # ---- CUDA graph of one step (no collective / host decision inside the step): the library never
+    # synchronises or allocates, so the whole layer captures; replays remove the host launch gaps ----
+    graph, per_step = None, 0
+    if args.graph and not heads and not bal:
+        graph = torch.cuda.CUDAGraph()
+        n0 = bf.kernel_launches()
+        with torch.cuda.graph(graph):
+            step()
+        per_step = bf.kernel_launches() - n0  # kernel nodes of the captured step
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps (graph replays, or eager with per-stage events) ----
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -194,13 +207,20 @@ def run_ours(args, w, rank, world, local_rank):
     with Clocks(local_rank) as clk:
         t_start.record(st)
         for s in range(args.steps):
-            step(evs[s])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(evs[s])
         t_end.record(st)
         torch.cuda.synchronize()
-    launches = bf.kernel_launches() - l0
+    launches = per_step * args.steps if graph is not None else bf.kernel_launches() - l0
     if world > 1:
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
+    if graph is not None:  # stage split from an instrumented eager pass over the same K steps
+        for s in range(args.steps):
+            step(evs[s])
+        torch.cuda.synchronize()
     s1 = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
     s2 = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
     at = statistics.median(e[2].elapsed_time(e[3]) for e in evs)
@@ -329,7 +349,7 @@ def run_ours(args, w, rank, world, local_rank):
     if os.path.exists(prof):
         tr = json.load(open(prof)).get(args.workload, {})
         traffic = tr.get("attention_bytes")
-    res = dict(ms_per_step=ms_per_step, s1=s1, s2=s2, at=at, dense_ms=dense_ms, sdpa_ms=sdpa_ms, kappa=kappa, stats=stats,
+    res = dict(graph=graph is not None, ms_per_step=ms_per_step, s1=s1, s2=s2, at=at, dense_ms=dense_ms, sdpa_ms=sdpa_ms, kappa=kappa, stats=stats,
                launches=launches, clk=clk.summary(), e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, peaks=peaks,
                achieved_tf=achieved_tf, dense_tf=dense_tf, traffic=traffic, retained_flops=retained_flops)
     return res
@@ -392,6 +412,8 @@ def main():
                          "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
                          "slices + O all-reduce (strong, SURVEY §8 f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", type=int, default=1, choices=[0, 1],
+                    help="1: time CUDA-graph replays of the captured step (layers sharding); 0: eager launches")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload], T=args.tile)
     rank = int(os.environ.get("RANK", 0))
@@ -464,6 +486,8 @@ def main():
             "e2e": {"value": r["e2e_ms"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
                     "d2h_bytes_per_step": r["d2h"]},
             "gpu_launches": r["launches"],
+            "launch": ("CUDA graph replay of the captured step (stages_ms from an eager pass)" if r["graph"]
+                       else "eager launches"),
             "clocks": r["clk"],
         }
         if not args.no_cpu_baseline and world == 1:

@@ -560,3 +560,45 @@ def test_balanced_layer_single_rank_nccl():
         assert torch.equal(o, o_ref)
     finally:
         dist.destroy_process_group()
+
+
+def test_cuda_graph_capture_of_whole_path():
+    """The library never synchronises or allocates, so one layer (Stage 1 with the side-stream norms and
+    the recompute, Stage 2, sparse prefill with its dynamic-scheduling counter) captures into a CUDA
+    graph; replays on new inputs written into the captured buffers give the eager results bit for bit."""
+    prob = workloads.structured(16, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128, block=256)
+    prob2 = workloads.structured(17, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128, block=256)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o = torch.empty_like(q)
+    cfg = bf.Config(b=256, g=64, eta=8, rho=0.1, seed=3)
+    P = bf.make_problem(q, k, v, o)
+    ws = bf.alloc_workspace(P, cfg)
+    m = bf.alloc_mask(P, cfg)
+
+    def layer():
+        bf.bfla_block_mask(P, cfg, m, ws)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        bf.bfla_sparse_prefill(P, cfg, m, ws)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        layer()  # warm-up outside capture (function attributes, tensor maps)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    n0 = bf.kernel_launches()
+    with torch.cuda.graph(graph):
+        layer()
+    assert bf.kernel_launches() - n0 >= 5
+    outs = []
+    for src in (prob, prob2):
+        q.copy_(src.q.cuda()), k.copy_(src.k.cuda()), v.copy_(src.v.cuda())
+        graph.replay()
+        torch.cuda.synchronize()
+        got = (o.clone(), m.tile_count.clone(), m.coarse_bits.clone())
+        layer()
+        torch.cuda.synchronize()
+        assert torch.equal(got[0], o) and torch.equal(got[1], m.tile_count) and torch.equal(got[2], m.coarse_bits)
+        outs.append(got[0])
+    assert not torch.equal(outs[0], outs[1])

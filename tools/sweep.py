@@ -6,7 +6,8 @@
       (--tile 64 or 128)
 
 For every point: kappa (kept / causal tiles, R20), layer ms = Stage 1 + Stage 2 + sparse prefill
-(median with p10 / p90 of --reps back-to-back layers; inputs exceed L2 from 32K up), the stage split,
+(CUDA-graph replays of the captured layer: median with p10 / p90 of --reps layers; inputs exceed L2
+from 32K up), the stage split (eager pass),
 the dense causal comparator (same kernel, median of 3) and speedup = dense / layer.  Writes a
 markdown table and one JSON line per point.
 
@@ -55,6 +56,23 @@ def run_point(P, cfg, reps):
         tot.append(ev[0].elapsed_time(ev[3]))
     st = m.stats_dict()
     kappa = st["kept_tiles"] / max(1, st["causal_tiles"])
+    # layer time from CUDA-graph replays of the captured layer (no host launch gaps: they dominate
+    # below ~8K); the stage split above is from the eager pass
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        bf.bfla_block_mask(P, cfg, m, ws)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        bf.bfla_sparse_prefill(P, cfg, m, ws)
+    graph.replay()
+    torch.cuda.synchronize()
+    tot = []
+    for _ in range(reps):
+        ev[0].record()
+        graph.replay()
+        ev[1].record()
+        torch.cuda.synchronize()
+        tot.append(ev[0].elapsed_time(ev[1]))
+    del graph
     return dict(kappa=kappa, ms=statistics.median(tot), p10=pct(tot, 0.1), p90=pct(tot, 0.9),
                 stage1_ms=statistics.median(s1), stage2_ms=statistics.median(s2), prefill_ms=statistics.median(at),
                 rows_flagged=st["rows_flagged"])
