@@ -208,7 +208,7 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
 
 // ---- workspace layout -------------------------------------------------------------------------
 struct WsLayout {
-  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, units, nflag, sched, kgather, total;
+  size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, units, nflag, sched, kgather, tcpart, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Geom& g) {
@@ -244,6 +244,8 @@ static WsLayout ws_layout(const Geom& g) {
   o += al(16);
   L.kgather = o;
   if (g.paged) o += al((size_t)g.B * g.Hkv_real * g.Nkv * g.D * 2);
+  L.tcpart = o;  // split-K partial accumulators of the tensor-core scores (small tile grids only)
+  o += al(tc_part_bytes(g));
   L.total = o;
   return L;
 }
@@ -263,7 +265,8 @@ static bfla_status cuda_check(const char* what) {
 // sum|x_k y_k| <= ||x|| ||y||.  The tests measure the observed ratio — it sits far below tau.
 static float certify_tau(const Geom& g) {
   const double n = (double)g.g * g.D, u = std::ldexp(1.0, -24);
-  double tau = u * (10.0 * std::sqrt((double)g.D + g.g) + n / 8.0);
+  // + 2 u per split-K partial added in fp32 (k_s1_tc_reduce), on top of the n/16 MMA steps
+  double tau = u * (10.0 * std::sqrt((double)g.D + g.g) + n / 8.0 + 2.0 * tc_splits(g));
   if (const char* e = getenv("BFLA_TAU_SCALE")) tau *= atof(e);  // calibration experiments only
   return (float)tau;
 }
@@ -334,7 +337,8 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, (uint32_t)kTcTileN / 2, 1, 1};  // two boxes per stage (one on diagonal tiles)
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
-    if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st))
+    float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
+    if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart))
       return fail(BFLA_ERR_CUDA, "tc scores launch failed");
     cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);

@@ -27,7 +27,9 @@ constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 size_t tc_scores_smem();
 // qn (optional): the scores kernel also writes the query-group norm bounds (Gram diagonal)
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st);
+                     cudaStream_t st, float* part = nullptr);
+int tc_splits(const Geom& g);
+size_t tc_part_bytes(const Geom& g);
 // with_q = false: key-group norms only (the scores kernel wrote the query norms)
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st,
                         bool with_q = true);

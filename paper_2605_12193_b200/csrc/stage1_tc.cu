@@ -113,10 +113,25 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
 // M128 x N128, into TMEM columns 256-383) from the A stages already in shared memory — no extra bytes
 // from L2 — and read its diagonal ||x_u||^2 (fp32 tensor-core sum of exact bf16 squares: relative
 // error <= 2(n/16)u, far inside the 2^-10 slack).  Only the K norms remain for k_s1_block_norms.
+//
+// Split-K (splits > 1, few tiles: short prompts, and the 1.3-wave grid at 32K): CTA (tile, split) runs
+// k-steps [k0, k1) and writes its raw fp32 partial accumulators, column-major [col][row], to `part`
+// (and the Gram diagonal to `qpart`); k_s1_tc_reduce adds the splits in ascending order and runs the
+// same max-pool epilogue.  The certification bound counts the extra additions (api.cu certify_tau).
+__device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& R, int mt, int nt, int* nlive) {
+  const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
+  long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
+  if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
+  if ((long long)nt * BK * g.b > e_last || mt * BQ >= R.Lq) return false;
+  *nlive = ((long long)(nt * BK + BK / 2) * g.b > e_last) ? TN / 2 : TN;
+  return true;
+}
+
 __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, Geom g,
                                                          float* __restrict__ S, int n_mt, int n_nt,
-                                                         float* __restrict__ qn) {
+                                                         float* __restrict__ qn, int splits,
+                                                         float* __restrict__ part, float* __restrict__ qpart) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ABYTES + BBYTES));
@@ -124,22 +139,19 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   uint64_t* done = empty + ST;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int t = blockIdx.x;
+  int t = blockIdx.x / splits;
+  const int split = blockIdx.x % splits;
+  const long long tile = t;
   const int nt = t % n_nt;
   t /= n_nt;
   const int mt = t % n_mt;
   const int rp = t / n_mt;  // r * Hq + p
   const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
-  const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
   const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
-  int nlive = TN;  // key-group columns with any causal block for this M tile: 256, or 128 when the
-                   // tile's second half lies entirely past the causal frontier (diagonal tiles)
-  {  // causal skip (Eq. 11-13): smallest j of the N tile vs the largest i of the M tile
-    long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
-    if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
-    if ((long long)nt * BK * g.b > e_last || mt * BQ >= R.Lq) return;
-    if ((long long)(nt * BK + BK / 2) * g.b > e_last) nlive = TN / 2;
-  }
+  // key-group columns with any causal block for this M tile: 256, or 128 when the tile's second half
+  // lies entirely past the causal frontier (diagonal tiles); causally dead tiles exit (Eq. 11-13)
+  int nlive = TN;
+  if (!tc_tile_live(g, R, mt, nt, &nlive)) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(full + s, 1);
@@ -158,10 +170,11 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int nk = g.g * g.D / TK;
+  const int k0 = (int)((long long)nk * split / splits), k1 = (int)((long long)nk * (split + 1) / splits);
   if (warp == 0 && lane == 0) {
-    for (int kk = 0; kk < nk; ++kk) {
-      const int s = kk % ST;
-      mbar_wait(empty + s, ((kk / ST) & 1) ^ 1);
+    for (int kk = k0; kk < k1; ++kk) {
+      const int s = (kk - k0) % ST;
+      mbar_wait(empty + s, (((kk - k0) / ST) & 1) ^ 1);
       mbar_arrive_expect_tx(full + s, ABYTES + (nlive == TN ? BBYTES : BBYTES / 2));
       unsigned char* a = smem + s * (ABYTES + BBYTES);
       tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
@@ -172,18 +185,19 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     const uint32_t idesc = nlive == TN ? idesc_bf16(TM, TN, 0, 0) : idesc_bf16(TM, TN / 2, 0, 0);
     constexpr uint32_t idesc_g = idesc_bf16(TM, TM, 0, 0);  // Gram A A^T
     const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
-    for (int kk = 0; kk < nk; ++kk) {
-      const int s = kk % ST;
-      mbar_wait(full + s, (kk / ST) & 1);
+    for (int kk = k0; kk < k1; ++kk) {
+      const int s = (kk - k0) % ST;
+      mbar_wait(full + s, ((kk - k0) / ST) & 1);
       tc_fence_after();
       const uint64_t a = d0 + (uint64_t)((s * (ABYTES + BBYTES)) >> 4), b = a + (uint64_t)(ABYTES >> 4);
 #pragma unroll
       for (int k16 = 0; k16 < TK / 16; ++k16)
-        umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk | k16) ? 1u : 0u);
+        umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk > k0 || k16) ? 1u : 0u);
       if (qduty) {
 #pragma unroll
         for (int k16 = 0; k16 < TK / 16; ++k16)
-          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_g, (kk | k16) ? 1u : 0u);
+          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_g,
+                           (kk > k0 || k16) ? 1u : 0u);
       }
       umma_commit_warp(empty + s);
     }
@@ -193,6 +207,26 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     const int row = lg * 32 + lane;  // query group within the tile
     mbar_wait(done, 0);
     tc_fence_after();
+    if (splits > 1) {  // raw partials; k_s1_tc_reduce finishes the tile
+      if (qduty) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
+        tmem_wait_ld();
+        float sq = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e == lane) sq = v[e];
+        qpart[(((long long)rp * n_mt + mt) * splits + split) * TM + row] = sq;
+      }
+      float* pp = part + (tile * splits + split) * (long long)(TN * TM);
+      for (int c0 = 0; c0 < nlive; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) pp[(c0 + e) * TM + row] = v[e];  // lanes = consecutive rows
+      }
+    } else {
     const int grow = mt * TM + row;           // global query group of head p
     const int ib = grow / g.G, u = grow % g.G;
     if (qduty) {
@@ -227,6 +261,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
         if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
       }
     }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -234,6 +269,65 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     tc_fence_after();
     if (qduty) tmem_dealloc<2 * TN>(tmem);
     else tmem_dealloc<TN>(tmem);
+  }
+}
+
+// Split-K finish: four CTAs (128 threads, thread = query-group row) per tile, one per 64-column
+// group; sums the splits in ascending order, then the epilogue of k_s1_tc_scores (Gram diagonal ->
+// query norms; G x G max).  Loads are column-major partials: a warp reads 128 contiguous bytes, and
+// the G x splits loads of a block column are independent (in flight together).
+constexpr int kRedCols = 64;
+__global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict__ S, int n_mt, int n_nt,
+                                                      float* __restrict__ qn, int splits,
+                                                      const float* __restrict__ part,
+                                                      const float* __restrict__ qpart) {
+  const int cg = blockIdx.x % (TN / kRedCols);
+  int t = blockIdx.x / (TN / kRedCols);
+  const long long tile = t;
+  const int nt = t % n_nt;
+  t /= n_nt;
+  const int mt = t % n_mt;
+  const int rp = t / n_mt;
+  const int p = rp % g.Hq, r = rp / g.Hq;
+  const Req R = req_of(g, r);
+  int nlive;
+  if (!tc_tile_live(g, R, mt, nt, &nlive)) return;
+  const int row = threadIdx.x;
+  const int grow = mt * TM + row;
+  const int ib = grow / g.G, u = grow % g.G;
+  if (qn != nullptr && nt == 0 && cg == 0) {
+    float sq = 0.f;
+    for (int sp = 0; sp < splits; ++sp) sq += qpart[(((long long)rp * n_mt + mt) * splits + sp) * TM + row];
+    float mx = sqrtf(fmaxf(sq, 0.f));
+    for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
+  }
+  const bool uvalid = (long long)grow * g.g < R.Nq;
+  long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
+  if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+  float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
+  const float* pp = part + tile * splits * (long long)(TN * TM) + row;
+  const int c_end = min(nlive, (cg + 1) * kRedCols);
+  for (int jb0 = cg * kRedCols; jb0 < c_end; jb0 += g.G) {
+    const int gcol = nt * TN + jb0;
+    float a[8];
+#pragma unroll
+    for (int vv = 0; vv < 8; ++vv) a[vv] = vv < g.G ? __ldg(pp + (long long)(jb0 + vv) * TM) : 0.f;
+    for (int sp = 1; sp < splits; ++sp) {
+      float b[8];
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv) b[vv] = vv < g.G ? __ldg(pp + ((long long)sp * TN + jb0 + vv) * TM) : 0.f;
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv) a[vv] += b[vv];
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int vv = 0; vv < 8; ++vv)
+      if (vv < g.G && (long long)(gcol + vv) * g.g < R.Nkv) mx = fmaxf(mx, a[vv]);
+    if (!uvalid) mx = -INFINITY;
+    for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int jb = gcol / g.G;
+    if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
   }
 }
 
@@ -605,16 +699,47 @@ void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, v
 
 size_t tc_scores_smem() { return SMEM; }
 
+// Split-K factor: enough CTAs for about two waves of 148 SMs when the tile grid is small, at most 8
+// and at least 16 k-steps per split; BFLA_TC_SPLITS overrides (A/B).  Deterministic in the geometry,
+// so bfla_workspace_size can reserve the partials.
+int tc_splits(const Geom& g) {
+  const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
+  const long long tiles = (long long)g.B * g.Hq * ((ngq + TM - 1) / TM) * ((ngk + TN - 1) / TN);
+  const int nk = g.g * g.D / TK;
+  static const int forced = [] {
+    const char* e = getenv("BFLA_TC_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  int s = forced > 0 ? forced : (tiles >= 2 * 148 ? 1 : (int)((2 * 148 + tiles - 1) / tiles));
+  if (s > 8) s = 8;
+  while (s > 1 && nk / s < 16) --s;
+  return s < 1 ? 1 : s;
+}
+
+size_t tc_part_bytes(const Geom& g) {
+  const int s = tc_splits(g);
+  if (s == 1) return 0;
+  const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
+  const long long n_mt = (ngq + TM - 1) / TM, tiles = (long long)g.B * g.Hq * n_mt * ((ngk + TN - 1) / TN);
+  return (size_t)(tiles * s * TN * TM + (long long)g.B * g.Hq * n_mt * s * TM) * 4;
+}
+
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st) {
+                     cudaStream_t st, float* part) {
   const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
   const int n_mt = (ngq + TM - 1) / TM, n_nt = (ngk + TN - 1) / TN;
   const long long ctas = (long long)g.B * g.Hq * n_mt * n_nt;
-  if (ctas <= 0 || ctas > 0x7fffffff) return -1;
+  const int splits = part ? tc_splits(g) : 1;
+  if (ctas <= 0 || ctas * splits > 0x7fffffff) return -1;
   cudaError_t e = cudaFuncSetAttribute(k_s1_tc_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return (int)e;
-  k_s1_tc_scores<<<(int)ctas, 256, SMEM, st>>>(tmA, tmB, g, S, n_mt, n_nt, qn);
+  float* qpart = part ? part + ctas * splits * (long long)(TN * TM) : nullptr;
+  k_s1_tc_scores<<<(int)(ctas * splits), 256, SMEM, st>>>(tmA, tmB, g, S, n_mt, n_nt, qn, splits, part, qpart);
   count_launch();
+  if (splits > 1) {
+    k_s1_tc_reduce<<<(int)(ctas * (TN / kRedCols)), 128, 0, st>>>(g, S, n_mt, n_nt, qn, splits, part, qpart);
+    count_launch();
+  }
   return (int)cudaGetLastError();
 }
 
