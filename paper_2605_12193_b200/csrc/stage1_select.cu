@@ -85,20 +85,24 @@ __device__ float warp_kth_largest(int nc, int k, F f) {
 
 __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int nc, float c_alpha, int select,
                                 float gamma, float keep_ratio, unsigned long long* keys, bool certify, float qnorm,
-                                const float* __restrict__ knrow, float tau) {
+                                const float* __restrict__ knrow, float tau, bool need_p = true) {
   const int lane = threadIdx.x & 31;
+  // the block softmax (Eq. 15) is needed for MASS and for the kept mass; RATIO without it ranks by S
+  const bool soft = select == 0 || need_p;
   float M = -INFINITY;
   for (int j = lane; j < nc; j += 32) M = fmaxf(M, s[j]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float* e = reinterpret_cast<float*>(keys);  // reuse the key area for e_j (nc floats)
-  for (int j = lane; j < nc; j += 32) e[j] = exp2_canon(__fmul_rn(__fsub_rn(s[j], M), c_alpha));
-  __syncwarp();
   float Z = 0.0f;
-  if (lane == 0)
-    for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
-  Z = __shfl_sync(0xffffffffu, Z, 0);
-  __syncwarp();
+  if (soft) {
+    for (int j = lane; j < nc; j += 32) e[j] = exp2_canon(__fmul_rn(__fsub_rn(s[j], M), c_alpha));
+    __syncwarp();
+    if (lane == 0)
+      for (int j = 0; j < nc; ++j) Z = __fadd_rn(Z, e[j]);
+    Z = __shfl_sync(0xffffffffu, Z, 0);
+    __syncwarp();
+  }
   // keys: (A bits << 32) | ~j — larger key = larger A, then smaller j (MASS, R6).  RATIO (R9) ranks
   // by the score instead — the block softmax is monotone in S, so this is the top-k by probability
   // without the ties fp32 underflow of A would create: (order-preserving bits of S << 32) | ~j.
@@ -132,7 +136,47 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
   float P = 0.0f, a_last = 0.0f, P_prev = 0.0f, kept_lo = INFINITY, t_last = 0.0f, s_last = 0.0f;
   uint32_t key_last = 0u;
   int nsel = 0;
-  while (nsel < nc) {
+  bool tie_fast = false, fast = false;
+  if (select == 1 && !need_p) {
+    // RATIO without the kept mass: the top-k set directly (no extraction loop).  The k-th largest
+    // score key by bisection, every block above it, then the smallest-j blocks at that key — the
+    // (S desc, j asc) order of the extraction; a block left at that key is the tie at the cut.
+    fast = true;
+    const float kth = warp_kth_largest(nc, target, [&](int j) { return s[j]; });
+    const uint32_t kk = okey(kth);
+    int gt = 0, eq = 0;
+    for (int j = lane; j < nc; j += 32) {
+      const uint32_t kj = okey(s[j]);
+      gt += kj > kk;
+      eq += kj == kk;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      gt += __shfl_xor_sync(0xffffffffu, gt, o);
+      eq += __shfl_xor_sync(0xffffffffu, eq, o);
+    }
+    int need = target - gt;  // blocks taken at the cut key, smallest j first
+    for (int j0 = 0; j0 < nc; j0 += 32) {
+      const int j = j0 + lane;
+      const uint32_t kj = j < nc ? okey(s[j]) : 0u;
+      const uint32_t at = __ballot_sync(0xffffffffu, j < nc && kj == kk);
+      const int rank = __popc(at & ((1u << lane) - 1u));
+      const bool take = j < nc && (kj > kk || (kj == kk && rank < need));
+      need -= __popc(at) < need ? __popc(at) : need;
+      if (take) {
+        keys[j] = 0ull;
+        if (certify) kept_lo = fminf(kept_lo, s[j] - tau * qnorm * knrow[j]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) kept_lo = fminf(kept_lo, __shfl_xor_sync(0xffffffffu, kept_lo, o));
+    __syncwarp();
+    nsel = target;
+    key_last = kk;
+    tie_fast = eq > target - gt;
+    s_last = kth;
+  }
+  while (!fast && nsel < nc) {
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
     best = warp_max_u64(best);
@@ -156,7 +200,9 @@ __device__ RowResult select_row(const Geom& g, const float* __restrict__ s, int 
     if (select == 0 ? (P >= gamma) : (nsel >= target)) break;
   }
   RowResult res{nsel, P, false, true, M, 0.f, 0.f, 0.f, 0.f};
-  if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
+  if (fast) {
+    res.tie = tie_fast;
+  } else if (nsel < nc) {  // a tie at the cut (R6): the next block in order has the same probability
     unsigned long long best = 0ull;
     for (int j = lane; j < nc; j += 32) best = keys[j] > best ? keys[j] : best;
     best = warp_max_u64(best);
@@ -261,7 +307,8 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
       const long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
       const int nc = (int)((e_i < R.Nkv - 1 ? e_i : (long long)R.Nkv - 1) / g.b) + 1;
       const float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-      const RowResult res = select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, false, 0.f, nullptr, 0.f);
+      const RowResult res =
+          select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, false, 0.f, nullptr, 0.f, false);
       or_kept(keys, nc, coarse + ((long long)(r * g.Hkv + h) * g.Lq + i) * g.Lw);
       rows++, recomputed++;
       ties += res.tie;
@@ -284,7 +331,8 @@ __global__ void __launch_bounds__(128) k_s1_select(Geom g, const float* __restri
       const bool cert = mode == 1;
       const RowResult res = select_row(g, s, nc, c_alpha, select, gamma, keep_ratio, keys, cert,
                                        cert ? qn[rowid] : 0.f, cert ? kn + ((long long)r * g.Hkv + h) * g.Lkv : nullptr,
-                                       tau);
+                                       tau,
+                                       kept_mass != nullptr);
       if (res.certified) {
         or_kept(keys, nc, row_bits);
         rows++;
