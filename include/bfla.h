@@ -2,7 +2,7 @@
  * bfla.h — C ABI of the B200 (sm_100a) BFLA hot path.  ABI version 1.
  *
  * Block-Filtered Long-Context Attention (arXiv 2605.12193).  Citations "P:n" are lines of the
- * paper's text; "Eq. k" its equations; R1..R21 the readings listed in DESIGN.md §3.
+ * paper's text; "Eq. k" its equations; R1..R22 the readings listed in DESIGN.md §3.
  *
  * Conventions (all entry points):
  *  - Tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA tensors) unless stated.
@@ -38,7 +38,7 @@ typedef enum {
                                       (Eq. 6), T does not divide b (Eq. 19), gamma not in (0,1] (Eq. 17),
                                       keep_ratio not in (0,1], rho not in [0,1] (Eq. 25), eta < 0, n_local < 0,
                                       n_sink < 0, NULL required pointer                                       */
-    BFLA_ERR_UNSUPPORTED = 2,      /* valid but not built: head_dim not in {128, 256}, T != 64, G = b/g > 8,
+    BFLA_ERR_UNSUPPORTED = 2,      /* valid but not built: head_dim not in {128, 256}, T not in {64, 128}, G = b/g > 8,
                                       FLATTEN with non-contiguous tokens, page_size not in {16, 32, 64}     */
     BFLA_ERR_MISALIGNED = 3,       /* TMA rules: base address % 16 B, strides % 16 B                         */
     BFLA_ERR_WORKSPACE = 4,        /* ws_bytes < bfla_workspace_size(...) or ws == NULL                       */
