@@ -669,6 +669,146 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
   }
 }
 
+// D = 256 variant of k_s1_recompute_tma: the row's query block (b x 256 bf16, 128 KB at b = 256) stays
+// resident as before, but K arrives one 64-column chunk per stage (double-buffered, 32 KB at b = 256),
+// so a unit takes D/64 stages and each thread's G chains carry their accumulators across them — the
+// channel order of every chain is unchanged (chunk ascending, then k16, then element).  Thread =
+// (query group u, token t); needs G*g <= the block size.
+template <int D>
+__global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma_kc(const __grid_constant__ CUtensorMap tmQ,
+                                                                     const __grid_constant__ CUtensorMap tmK, Geom g,
+                                                                     const int32_t* __restrict__ flagged,
+                                                                     const int32_t* __restrict__ n_flagged,
+                                                                     const int32_t* __restrict__ ulist,
+                                                                     const int32_t* __restrict__ n_units,
+                                                                     float* __restrict__ S) {
+  constexpr int NCH = D / 64;
+  (void)n_flagged;
+  extern __shared__ __align__(1024) unsigned char rk_raw[];
+  unsigned char* rs = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(rk_raw) + 1023) & ~uintptr_t(1023));
+  const int G = g.G, gg = g.g, b = g.b, nrt = b / 64;
+  unsigned char* qs = rs;                                              // query block, all chunks
+  unsigned char* kb[2] = {rs + b * D * 2, rs + b * D * 2 + b * 128};  // one K chunk per buffer
+  float* tokdot = reinterpret_cast<float*>(rs + b * D * 2 + 2 * b * 128);
+  float* pairtot = tokdot + G * G * gg;
+  __shared__ __align__(8) uint64_t bar[3];
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < 3; ++e) mbar_init(bar + e, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long units = *n_units;
+  const long long per = (units + gridDim.x - 1) / gridDim.x;
+  const long long u0 = (long long)blockIdx.x * per, u1 = min(units, u0 + per);
+  auto decode = [&](long long uidx, int& j, int& i, int& p, int& r, int& fidx) {
+    const int unit = ulist[uidx];
+    j = unit % g.Lkv;
+    fidx = unit / g.Lkv;
+    const int row = flagged[fidx];
+    i = row % g.Lq;
+    p = (row / g.Lq) % g.Hq;
+    r = row / (g.Lq * g.Hq);
+  };
+  auto load_q = [&](int t0, int p, int r) {
+    mbar_arrive_expect_tx(bar, (uint32_t)(b * D * 2));
+    for (int rt = 0; rt < nrt; ++rt)
+      for (int cc = 0; cc < NCH; ++cc) tma_load_4d(qs + (rt * NCH + cc) * 8192, &tmQ, bar, cc * 64, t0 + rt * 64, p, r);
+  };
+  auto load_kc = [&](int bi, int t0, int hh, int r, int cc) {
+    mbar_arrive_expect_tx(bar + 1 + bi, (uint32_t)(b * 128));
+    for (int rt = 0; rt < nrt; ++rt) tma_load_4d(kb[bi] + rt * 8192, &tmK, bar + 1 + bi, cc * 64, t0 + rt * 64, hh, r);
+  };
+  const long long s0 = u0 * NCH, s1 = u1 * NCH;
+  if (s0 < s1 && threadIdx.x == 0) {
+    int j, i, p, r, f;
+    decode(u0, j, i, p, r, f);
+    load_q(i * b, p, r);
+    load_kc(0, j * b, p / g.m / g.kvdiv, r, 0);
+  }
+  uint32_t qph = 0, kph[2] = {0, 0};
+  int buf = 0, qrow = -1;
+  const int idx = threadIdx.x;
+  const bool act = idx < G * gg;
+  const int t = act ? idx % gg : 0, u = act ? idx / gg : 0;
+  float acc[8];
+  for (long long sg = s0; sg < s1; ++sg) {
+    const long long uidx = sg / NCH;
+    const int cc = (int)(sg % NCH);
+    int j, i, p, r, fidx;
+    decode(uidx, j, i, p, r, fidx);
+    bool new_q = false;
+    int ni = 0, np = 0, nr = 0;
+    if (sg + 1 < s1) {
+      int nj, nfi;
+      decode((sg + 1) / NCH, nj, ni, np, nr, nfi);
+      new_q = cc == NCH - 1 && nfi != fidx;
+      if (threadIdx.x == 0) load_kc(buf ^ 1, nj * b, np / g.m / g.kvdiv, nr, (int)((sg + 1) % NCH));
+    }
+    if (qrow != fidx) {
+      mbar_wait(bar, qph);
+      qph ^= 1;
+      qrow = fidx;
+    }
+    mbar_wait(bar + 1 + buf, kph[buf]);
+    kph[buf] ^= 1;
+    const Req R = req_of(g, r);
+    const int qtok = u * gg + t;
+    const bool qok = act && i * b + qtok < R.Nq;
+    if (cc == 0) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[v] = 0.f;
+    }
+    if (qok) {
+      const unsigned char* kbuf = kb[buf];
+#pragma unroll 2
+      for (int k16 = 0; k16 < 8; ++k16) {
+        float xf[8];
+        {
+          const int rt = qtok >> 6, row = qtok & 63;
+          bf16x8_f32(*reinterpret_cast<const uint4*>(qs + (rt * NCH + cc) * 8192 + row * 128 + ((k16 ^ (row & 7)) << 4)),
+                     xf);
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          if (v >= G) break;
+          const int ktok = v * gg + t, rt = ktok >> 6, row = ktok & 63;
+          float yf[8];
+          bf16x8_f32(*reinterpret_cast<const uint4*>(kbuf + rt * 8192 + row * 128 + ((k16 ^ (row & 7)) << 4)), yf);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[v] = __fmaf_rn(xf[e], yf[e], acc[v]);
+        }
+      }
+    }
+    __syncthreads();  // K buffer `buf` (and, after the last chunk, the query block) no longer read
+    if (cc == NCH - 1) {
+      if (act) {
+        const int kt0 = j * b;
+        for (int v = 0; v < G; ++v) {
+          const bool ok = qok && kt0 + v * gg + t < R.Nkv;  // padding tokens: exact zero dot
+          tokdot[(u * G + v) * gg + t] = ok ? acc[v] : 0.0f;
+        }
+      }
+      if (new_q && threadIdx.x == 0) load_q(ni * b, np, nr);
+      __syncthreads();
+      if (threadIdx.x < G * G) {
+        const int uv = threadIdx.x, uu = uv / G, vv = uv % G;
+        float a = 0.0f;
+        for (int tt = 0; tt < gg; ++tt) a = __fadd_rn(a, tokdot[uv * gg + tt]);  // ascending t
+        const bool valid = i * b + uu * gg < R.Nq && j * b + vv * gg < R.Nkv;   // padding-only groups (R3)
+        pairtot[uv] = valid ? a : -INFINITY;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float mx = -INFINITY;  // Eq. 10
+        for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
+        S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = mx;
+      }
+      __syncthreads();
+    }
+    buf ^= 1;
+  }
+}
+
 // vLLM pages -> contiguous [B][Hkv][Nkv][D] (Stage-1 FLATTEN groups span several pages; the gathered
 // copy lets one TMA box cover a whole group row).  One thread per 16 bytes.
 __global__ void __launch_bounds__(256) k_paged_gather(Geom g, const uint4* __restrict__ kc, const int32_t* __restrict__ pt,
@@ -769,6 +909,16 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
       auto kern = k_s1_recompute_tma<128>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
       kern<<<num_sms, kRecThreads, smem_t, st>>>(*tmQ, *tmK, g, flagged, n_flagged, ulist, n_units, S);
+      count_launch();
+      return (int)cudaGetLastError();
+    }
+    const size_t smem_kc = (size_t)g.b * g.D * 2 + (size_t)2 * g.b * 128 + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4 +
+                           1024;
+    if (mode == 0 && tmQ && tmK && g.D == 256 && g.G <= 8 && g.b % 64 == 0 && g.G * g.g <= kRecThreads &&
+        smem_kc <= 226 * 1024) {
+      auto kern = k_s1_recompute_tma_kc<256>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_kc);
+      kern<<<num_sms, kRecThreads, smem_kc, st>>>(*tmQ, *tmK, g, flagged, n_flagged, ulist, n_units, S);
       count_launch();
       return (int)cudaGetLastError();
     }
