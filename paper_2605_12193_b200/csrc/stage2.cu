@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(256) k_s2_expand_rescue(Geom g, const uint32_t
   // the coarse row in registers, one word per lane (Lw <= 32, i.e. up to 1024 blocks), read by shuffle
   const bool creg = g.Lw <= 32;
   const uint32_t cw = (creg && lane < g.Lw) ? __ldg(crow + lane) : 0u;
-  for (int j0 = 0; j0 < g.Tkv; j0 += 32) {
+  // words wholly past the causal frontier are zero: written lane-parallel below, not walked here
+  const int jend = label ? g.Tkv : ((jmax >> 5) + 1) << 5;
+  for (int w = (jmax >> 5) + 1 + lane; !label && w < g.Tw; w += 32) tile_bits[row * g.Tw + w] = 0u;
+  for (int j0 = 0; j0 < jend; j0 += 32) {
     const int j = j0 + lane;
     int lab = 0;
     const int J = j >> rbs;

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/s2_tests.txt 2>&1
-echo "rc=$?" >> gpurun_out/s2_tests.txt
-python tools/stats_cost.py > gpurun_out/s2_cost.txt 2>&1; python tools/stats_cost.py 131072 >> gpurun_out/s2_cost.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s2_tests.txt 2>&1; echo "exit $?" >> gpurun_out/s2_tests.txt
+if grep -q "exit 0" gpurun_out/s2_tests.txt; then
+bash tools/runs/gpu_launches.sh s2_llama128k --workload llama8b-128k
+bash tools/runs/gpu_launches.sh s2_llama32k
+fi
