@@ -167,25 +167,28 @@ def test_certification_norms(m):
         assert (got <= want * (1 + 2 ** -9) + 1e-6).all(), "norm bound loose"
 
 
+@pytest.mark.parametrize("T", [64, 128])
 @pytest.mark.parametrize("case", [
     dict(Nq=1000, Nkv=1500, b=128, paged=0),      # chunked, ragged: canonical SIMT scores
     dict(Nq=2048, Nkv=2048, b=256, paged=0),      # tensor-core scores + certification + recompute
     dict(Nq=2048, Nkv=2048, b=256, paged=16),     # paged K/V
 ])
-def test_per_query_head_masks(case):
+def test_per_query_head_masks(case, T):
     """§8 f3: BFLA_MASK_PER_Q_HEAD keeps Eq. 18 literal (one mask per query head, Stage 2 per query
     head, psi by query head).  Reference: the oracle on K/V repeated per query head, where the OR over
     a one-head group is that head's own mask; masks bit-exact, O within tolerance."""
     m = 4
     prob = workloads.gaussian(41, B=1, Hq=8, Hkv=2, Nq=case["Nq"], Nkv=case["Nkv"], d=128, sigma=0.8)
-    cfg = bf.Config(b=case["b"], g=64, T=64, gamma=0.95, eta=4, rho=0.2, seed=5, mask_groups=bf.MASK_PER_Q_HEAD)
+    if case["b"] % T:
+        pytest.skip("T must divide b")
+    cfg = bf.Config(b=case["b"], g=64, T=T, gamma=0.95, eta=4, rho=0.2, seed=5, mask_groups=bf.MASK_PER_Q_HEAD)
     gpu = run_gpu(prob, cfg, paged_page=case["paged"])
     rep = workloads.Problem(q=prob.q, k=prob.k.repeat_interleave(m, dim=1), v=prob.v.repeat_interleave(m, dim=1))
     ref = oracle_masks(rep, cfg)
     labels = _check_masks(gpu, ref, cfg)
     assert labels.shape[1] == 8
-    check_lists(gpu, labels, case["Nq"], case["Nkv"], 64)
-    (o_ref, lse_ref), = oracle_attention(rep, labels, 64)
+    check_lists(gpu, labels, case["Nq"], case["Nkv"], T)
+    (o_ref, lse_ref), = oracle_attention(rep, labels, T)
     compare_o(gpu["o"][0], o_ref, str(case))
     assert np.abs(gpu["lse"][0].cpu().numpy() - lse_ref).max() <= 1e-3
 
@@ -394,11 +397,12 @@ def _varlen_case(seed, lens, Hq=4, Hkv=2, d=128):
     return workloads.Problem(q, k, v), torch.tensor(lens, dtype=torch.int32)
 
 
+@pytest.mark.parametrize("T", [64, 128])
 @pytest.mark.parametrize("paged", [0, 16])
-def test_varlen_batch(paged):
+def test_varlen_batch(paged, T):
     lens = [(700, 1500), (300, 300), (129, 1000), (64, 64)]
     prob, sl = _varlen_case(81, lens)
-    cfg = bf.Config(b=128, g=64, gamma=0.95, eta=4, rho=0.2, seed=3)
+    cfg = bf.Config(b=128, g=64, T=T, gamma=0.95, eta=4, rho=0.2, seed=3)
     q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
     B, Hq, Nq, d = q.shape
     Nkv = k.shape[2]
@@ -420,7 +424,7 @@ def test_varlen_batch(paged):
     Tq_max, Tkv_max = labels.shape[2], labels.shape[3]
     for r, (nq, nkv) in enumerate(lens):
         qf, kf, vf = (f32(t[r])[:, :n] for t, n in ((prob.q, nq), (prob.k, nkv), (prob.v, nkv)))
-        ref = oracle.mask_pipeline(qf, kf, b=128, g=64, T=64, gamma=0.95, eta=4, rho=0.2, seed=3)
+        ref = oracle.mask_pipeline(qf, kf, b=128, g=64, T=T, gamma=0.95, eta=4, rho=0.2, seed=3)
         Lq, Lkv = ref["coarse"].shape[1:]
         assert np.array_equal(coarse[r, :, :Lq, :Lkv], ref["coarse"]), r
         assert not coarse[r, :, Lq:].any() and not coarse[r, :, :, Lkv:].any()
@@ -428,7 +432,7 @@ def test_varlen_batch(paged):
         assert np.array_equal(labels[r, :, :Tq, :Tkv], ref["labels"]), r
         assert not labels[r, :, Tq:].any() and not labels[r, :, :, Tkv:].any()
         # lists: row (r, h, i) at (r*Hkv + h) * Tq_max*Tkv_max + causal prefix of request r
-        rc = np.array([sum(oracle.causal(i, j, 64, nq, nkv) for j in range(Tkv)) for i in range(Tq)])
+        rc = np.array([sum(oracle.causal(i, j, T, nq, nkv) for j in range(Tkv)) for i in range(Tq)])
         offs = np.concatenate([[0], np.cumsum(rc)])
         for h in range(2):
             for i in range(Tq):
@@ -437,7 +441,7 @@ def test_varlen_batch(paged):
                 assert counts[r, h, i] == len(want)
                 assert np.array_equal(lists[base:base + len(want)], want)
             assert not counts[r, h, Tq:].any()
-        O_ref, lse_ref = oracle.masked_attention(qf, kf, vf, 128 ** -0.5, ref["labels"], 64)
+        O_ref, lse_ref = oracle.masked_attention(qf, kf, vf, 128 ** -0.5, ref["labels"], T)
         compare_o(o[r, :, :nq], O_ref, f"varlen r={r}")
         assert np.abs(l[r, :, :nq].cpu().numpy() - lse_ref).max() <= 1e-3
         assert not o[r, :, nq:].float().abs().sum().item()  # padding rows untouched (zeros)
