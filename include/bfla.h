@@ -15,8 +15,11 @@
  *    next synchronisation as a CUDA error.
  *  - Identical inputs give identical output bits (masks, lists, O, LSE): no atomics decide any
  *    value (atomics only accumulate integer statistics).
- *  - Calls are reentrant; there is no global mutable state except the thread-local detail
- *    string of bfla_last_error().
+ *  - Calls are reentrant and may come from several host threads at once: the only state kept
+ *    between calls is per host thread (the detail string of bfla_last_error(), and the side stream
+ *    + events bfla_block_mask forks its key-norm kernel onto, created on a thread's first call per
+ *    device and joined back into `stream` before the call returns) plus a process-wide atomic
+ *    launch counter.
  *  - Element strides are in ELEMENTS (bf16 = 2 bytes); the head_dim axis must be contiguous.
  */
 #ifndef BFLA_H_
@@ -116,6 +119,11 @@ typedef struct {
     uint64_t seed;      /* s of Eq. 24-25                                                               */
     int32_t scores_path; /* BFLA_SCORES_* (FLATTEN only; MEAN is always canonical)                      */
     int32_t mask_groups; /* BFLA_MASK_* (0 = per KV head, the default)                                  */
+    float certify_slack; /* AUTO scores: factor >= 1 applied to the certification bound tau;
+                            a wider bound only sends more rows to the canonical recompute — the mask
+                            is the same bit for bit — so tests use it to exercise the recompute.
+                            0 = 1 (default); values in (0, 1) or negative are INVALID_ARGUMENT, so no
+                            setting can weaken the certification.                                     */
 } bfla_config;
 
 /* Statistics, accumulated with integer atomics (values are order independent). */
@@ -148,10 +156,12 @@ typedef struct {
     bfla_stats* stats;      /* optional device bfla_stats (zeroed by bfla_block_mask)                */
 } bfla_mask;
 
-/* Bytes of device scratch the entry points need for (problem, config). */
+/* Bytes of device scratch the entry points need for (problem, config); 0 if the pair is invalid.
+   config == NULL (the dense comparator of bfla_prefill) needs only the 256-byte scheduling counter. */
 size_t bfla_workspace_size(const bfla_problem* problem, const bfla_config* config);
 /* Entries tile_list must hold: batch * h_kv * (causal tiles per (r,h)); with seqlens, batch * h_kv *
-   ceil(n_q/T) * ceil(n_kv/T). */
+   ceil(n_q/T) * ceil(n_kv/T).  On invalid (problem, config) it returns the NEGATED bfla_status
+   (e.g. -BFLA_ERR_UNSUPPORTED) with the detail in bfla_last_error(). */
 int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* config);
 
 /* Stage 1 (Eq. 4-18 + GQA OR): pooling, block scores (Eq. 9-10), causal mask (Eq. 11-14),

@@ -42,10 +42,12 @@ class Config:
     seed: int = 0
     scores: int = SCORES_AUTO
     mask_groups: int = MASK_PER_KV_HEAD  # MASK_PER_Q_HEAD: Eq. 18 literal, one mask per query head
+    certify_slack: float = 0.0  # >= 1 widens the certification bound (tests: forces the recompute)
 
     def c(self) -> bfla_config:
         return bfla_config(self.b, self.g, self.T, self.pool, self.select, self.gamma, self.keep_ratio,
-                           self.n_sink, self.n_local, self.eta, self.rho, self.seed, self.scores, self.mask_groups)
+                           self.n_sink, self.n_local, self.eta, self.rho, self.seed, self.scores, self.mask_groups,
+                           self.certify_slack)
 
 
 @dataclasses.dataclass
@@ -142,8 +144,8 @@ class Mask:
         Lq, Lkv, Tq, Tkv = cd(Nq, cfg.b), cd(Nkv, cfg.b), cd(Nq, cfg.T), cd(Nkv, cfg.T)
         self.Lq, self.Lkv, self.Tq, self.Tkv = Lq, Lkv, Tq, Tkv
         cap = bfla_tile_list_capacity(problem, cfg)
-        if cap < 0:
-            check(1, "bfla_tile_list_capacity")
+        if cap < 0:  # the negated bfla_status of the invalid (problem, config)
+            check(-cap, "bfla_tile_list_capacity")
         self.coarse_bits = torch.zeros(B, Hkv, Lq, cd(Lkv, 32), dtype=torch.int32, device=dev)
         self.tile_bits = torch.zeros(B, Hkv, Tq, cd(Tkv, 32), dtype=torch.int32, device=dev)
         self.tile_list = torch.zeros(max(1, cap), dtype=torch.int32, device=dev)

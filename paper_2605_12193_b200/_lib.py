@@ -12,10 +12,16 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbfla.so")
-if os.environ.get("BFLA_TRACE_LIB") == "1":  # timeline-instrumented build (tools/attn_trace.py only)
-    LIB_PATH = os.path.join(_HERE, "libbfla_trace.so")
-if os.environ.get("BFLA_LIB_VARIANT"):  # A/B experiments: libbfla_<variant>.so built by tools/ab_build.py
-    LIB_PATH = os.path.join(_HERE, f"libbfla_{os.environ['BFLA_LIB_VARIANT']}.so")
+
+
+def use_variant(name: str) -> None:
+    """Tools and debug tests only: load libbfla_<name>.so (build.py variants: debug, exp, trace, or an
+    A/B build of tools/ab_build.py) instead of the product library.  Must precede the first lib()."""
+    global LIB_PATH
+    path = os.path.join(_HERE, f"libbfla_{name}.so") if name else os.path.join(_HERE, "libbfla.so")
+    if _lib is not None and path != LIB_PATH:
+        raise RuntimeError(f"{LIB_PATH} is already loaded")
+    LIB_PATH = path
 
 BFLA_OK = 0
 STATUS = {0: "BFLA_OK", 1: "BFLA_ERR_INVALID_ARGUMENT", 2: "BFLA_ERR_UNSUPPORTED", 3: "BFLA_ERR_MISALIGNED",
@@ -41,7 +47,8 @@ class bfla_problem(ctypes.Structure):
 class bfla_config(ctypes.Structure):
     _fields_ = [("block_b", i32), ("group_g", i32), ("tile_t", i32), ("pool", i32), ("select", i32),
                 ("gamma", f32), ("keep_ratio", f32), ("n_sink", i32), ("n_local", i32), ("eta", i32),
-                ("rho", f32), ("seed", u64), ("scores_path", i32), ("mask_groups", i32)]
+                ("rho", f32), ("seed", u64), ("scores_path", i32), ("mask_groups", i32),
+                ("certify_slack", f32)]
 
 
 class bfla_stats(ctypes.Structure):

@@ -42,43 +42,48 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+# Library variants.  The product library (libbfla.so) has no switches.  The others are built on
+# demand for tools only: debug (mbarrier-timeout traps, build.py --debug), exp (experiment switches
+# read from the environment, tools/ab_build.py) and trace (attention timeline, tools/attn_trace.py).
+VARIANTS = {"": [], "debug": ["-DBFLA_DEBUG"], "exp": ["-DBFLA_EXPERIMENTS"], "trace": ["-DBFLA_TRACE"]}
+
+
+def lib_path(variant: str = "") -> str:
+    return LIB if not variant else os.path.join(HERE, f"libbfla_{variant}.so")
+
+
+def build(force: bool = False, verbose: bool = False, variant: str = "", extra=()) -> str:
+    """Compile every unit for sm_100a and link libbfla[_variant].so; returns its path."""
+    flags = list(VARIANTS.get(variant, ["-DBFLA_EXPERIMENTS"])) + list(extra)
+    objdir = BUILD if not variant else BUILD + "_" + variant
+    os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "bfla.h"))
     objs = []
-    for unit, extra in UNITS.items():
+    for unit, unit_flags in UNITS.items():
         src = os.path.join(CSRC, unit)
-        obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
+        obj = os.path.join(objdir, unit.replace(".cu", ".o"))
         objs.append(obj)
-        if force or _stale(obj, [src, *headers, __file__]):
-            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", src, "-o", obj]
+        if force or extra or _stale(obj, [src, *headers, __file__]):
+            cmd = [nvcc(), *ARCH, *COMMON, *flags, *unit_flags, "-c", src, "-o", obj]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)
-    if force or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    out = lib_path(variant)
+    if force or extra or _stale(out, objs):
+        tmp = out + f".tmp{os.getpid()}"
         subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs])
-        os.replace(tmp, LIB)
-    return LIB
-
-
-def build_trace() -> str:
-    """libbfla_trace.so: the same library with the attention timeline instrumentation compiled in
-    (-DBFLA_TRACE; tools/attn_trace.py).  Never loaded by the product path or the tests."""
-    build()
-    out = os.path.join(HERE, "libbfla_trace.so")
-    obj = os.path.join(BUILD, "attention2_trace.o")
-    src = os.path.join(CSRC, "attention2.cu")
-    subprocess.check_call([nvcc(), *ARCH, *COMMON, "-DBFLA_TRACE", "-c", src, "-o", obj])
-    objs = [os.path.join(BUILD, u.replace(".cu", ".o")) for u in UNITS if u != "attention2.cu"]
-    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", out, *objs, obj])
+        os.replace(tmp, out)
     return out
 
 
+def build_trace() -> str:
+    """libbfla_trace.so: the attention timeline instrumentation compiled in (-DBFLA_TRACE;
+    tools/attn_trace.py).  Never loaded by the product path or the tests."""
+    return build(variant="trace")
+
+
 if __name__ == "__main__":
-    if "--trace" in sys.argv:
-        print(build_trace())
-    else:
-        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    var = "trace" if "--trace" in sys.argv else "debug" if "--debug" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var))

@@ -48,22 +48,26 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-// Side stream + events for fork/join inside one call (created once per device, then read-only).
+// Side stream + fork/join events for the concurrent key-norm kernel inside one bfla_block_mask call.
+// One set per (host thread, device): a call records its fork and join and waits on them before it
+// returns to the caller, all from its own thread, so concurrent calls from different threads never
+// see each other's events (cudaStreamWaitEvent takes the record made by the same thread just before).
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 static SideStream* side_stream() {
-  static std::mutex mu;
-  static SideStream per_dev[64];
+  static thread_local SideStream per_dev[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
   SideStream& ss = per_dev[dev];
   if (!ss.s) {
     if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-    cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+    if (cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;  // run the norms on the caller's stream instead
+    }
   }
   return &ss;
 }
@@ -180,6 +184,8 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
       return fail(BFLA_ERR_UNSUPPORTED, "G = b/g = %d > 8 not built for FLATTEN", b / gg);
     if (cfg->mask_groups != BFLA_MASK_PER_KV_HEAD && cfg->mask_groups != BFLA_MASK_PER_Q_HEAD)
       return fail(BFLA_ERR_INVALID_ARGUMENT, "mask_groups");
+    if (cfg->certify_slack != 0.f && !(cfg->certify_slack >= 1.f))
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "certify_slack must be 0 or >= 1 (it can only widen tau)");
     if (cfg->mask_groups == BFLA_MASK_PER_Q_HEAD) {
       // one mask group per query head (Eq. 18 literal): groups of size 1 over KV head p / m
       g->kvdiv = g->m;
@@ -203,6 +209,11 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
   // list capacity per (r, h): the closed-form causal count (uniform batch) or the full tile rectangle
   // (varlen: every request's causal set fits inside it)
   g->causal_per_head = g->lens ? (long long)g->Tq * g->Tkv : causal_row_offset(*g, g->Tq);
+  // int32 indices inside the kernels: recompute units (head row, KV block) and the prefill items
+  if (cfg && (long long)g->B * g->Hq * g->Lq * g->Lkv >= (1LL << 31))
+    return fail(BFLA_ERR_UNSUPPORTED, "batch * h_q * L_q * L_kv = %lld >= 2^31 (int32 unit indices)",
+                (long long)g->B * g->Hq * g->Lq * g->Lkv);
+  if ((long long)g->B * g->Hq * g->Tq >= (1LL << 31)) return fail(BFLA_ERR_UNSUPPORTED, "too many query tiles");
   return BFLA_OK;
 }
 
@@ -211,9 +222,15 @@ struct WsLayout {
   size_t S, qbar, kbar, coarse, tbits, list, count, stats, qn, kn, flagged, units, nflag, sched, kgather, tcpart, total;
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
-static WsLayout ws_layout(const Geom& g) {
+static WsLayout ws_layout(const Geom& g, bool dense = false) {
   WsLayout L;
   size_t o = 0;
+  if (dense) {  // the dense comparator (config == NULL) uses only the item counter
+    memset(&L, 0, sizeof(L));
+    L.sched = 0;
+    L.total = al(16);
+    return L;
+  }
   L.S = o;
   o += al((size_t)g.B * g.Hq * g.Lq * g.Lkv * 4);
   L.qbar = o;
@@ -256,19 +273,21 @@ static bfla_status cuda_check(const char* what) {
   return BFLA_OK;
 }
 
-// tau: |S_tc - S_canonical| <= tau * ||x|| * ||y|| for one g*C-long group dot product.  Model: the
-// canonical order (g token chains of C FMAs, then g - 1 adds; DESIGN.md §4 item 2) makes C + g
-// round-to-nearest errors per product path, each at most u times a partial sum bounded by
-// sum|x_k y_k|; as independent mean-zero terms they stay within 10 sqrt(C + g) u sum|x_k y_k| (Hoeffding;
-// exceeding it has probability < 2 exp(-50)); the tensor-core chain of n/16 MMA steps stays within
-// 2 (n/16) u even if every internal step truncated (biased, so no square root).  Cauchy-Schwarz:
-// sum|x_k y_k| <= ||x|| ||y||.  The tests measure the observed ratio — it sits far below tau.
-static float certify_tau(const Geom& g) {
+// tau: |S_tc - S_canonical| <= tau * ||x|| * ||y|| for one g*C-long group dot product.
+// Canonical side, worst case (no probabilistic model): every product x_k y_k of the canonical order
+// (g token chains of C FMAs, then g - 1 adds, §4 item 2) passes through at most C + g - 1
+// round-to-nearest operations, so |S_c - S_exact| <= gamma_{C+g-1} sum|x_k y_k| with
+// gamma_n = n u / (1 - n u) <= (C + g) u here (the classical recursive-summation bound; the tests
+// pin it on adversarial inputs).  Tensor-core side: n/16 K=16 MMA steps into an fp32 accumulator,
+// bounded by 2 (n/16) u even if every step truncated; + 2 u per split-K partial added in fp32
+// (k_s1_tc_reduce).  Cauchy-Schwarz: sum|x_k y_k| <= ||x|| ||y||.  `slack` >= 1 (bfla_config
+// certify_slack) only widens tau: more rows are recomputed, the mask cannot change.
+static float certify_tau(const Geom& g, float slack) {
   const double n = (double)g.g * g.D, u = std::ldexp(1.0, -24);
-  // + 2 u per split-K partial added in fp32 (k_s1_tc_reduce), on top of the n/16 MMA steps
-  double tau = u * (10.0 * std::sqrt((double)g.D + g.g) + n / 8.0 + 2.0 * tc_splits(g));
-  if (const char* e = getenv("BFLA_TAU_SCALE")) tau *= atof(e);  // calibration experiments only
-  return (float)tau;
+  const double canon = ((double)g.D + g.g) * u / (1.0 - ((double)g.D + g.g) * u);
+  double tau = canon + u * (n / 8.0 + 2.0 * tc_splits(g));
+  if (slack > 1.0f) tau *= slack;
+  return (float)(tau * (1.0 + 1e-6));  // rounding the bound to fp32 must not shrink it
 }
 
 static bool tc_eligible(const Geom& g, const bfla_problem* P, const bfla_config* cfg, const bfla_mask* mask) {
@@ -286,7 +305,6 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
   const WsLayout L = ws_layout(g);
   float* S = reinterpret_cast<float*>(ws + L.S);
   unsigned long long* stats = reinterpret_cast<unsigned long long*>(mask->stats);
-  if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
   const int32_t* pt = g.paged ? P->page_table : nullptr;
   // c_alpha = log2(e) / sqrt(C) rounded once to fp32 (DESIGN.md §4 item 4; alpha = 1/sqrt(C), Eq. 15)
   const float c_alpha = (float)(1.4426950408889634 / std::sqrt((double)g.D));
@@ -297,32 +315,15 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     int32_t* flagged = reinterpret_cast<int32_t*>(ws + L.flagged);
     int32_t* nflag = reinterpret_cast<int32_t*>(ws + L.nflag);
     int32_t* ulist = reinterpret_cast<int32_t*>(ws + L.units);
-    const void* kc = P->k;
+    const void* kc = g.paged ? static_cast<const void*>(ws + L.kgather) : P->k;  // paged K: gathered copy
     Geom gk = g;  // geometry of the K operand as the score kernels see it (gathered = contiguous)
     if (g.paged) {
-      void* kg = ws + L.kgather;
-      launch_paged_gather(g, P->k, P->page_table, kg, st);
-      kc = kg;
       gk.paged = 0;
       gk.kvs2 = g.D;
       gk.kvs1 = (long long)g.Nkv * g.D;
       gk.kvs0 = (long long)g.Hkv_real * g.Nkv * g.D;
     }
-    // query-group norms come from the scores kernel (Gram diagonal, no extra HBM bytes); key-group
-    // norms (HBM-bound, K only) run on a side stream concurrently; joined before the selection
-    static const bool q_norms_separate = [] {
-      const char* e = getenv("BFLA_QNORM_KERNEL");  // A/B: 1 = query norms in the norm kernel
-      return e && atoi(e) == 1;
-    }();
-    SideStream* ss = side_stream();
-    if (ss) {
-      cudaEventRecord(ss->fork, st);
-      cudaStreamWaitEvent(ss->s, ss->fork, 0);
-      launch_block_norms(gk, P->q, kc, qn, kn, ss->s, q_norms_separate);
-      cudaEventRecord(ss->join, ss->s);
-    } else {
-      launch_block_norms(gk, P->q, kc, qn, kn, st, q_norms_separate);
-    }
+    // every tensor map is encoded before the first enqueue: a failure leaves the stream untouched
     CUtensorMap tmA, tmB;
     bfla_status s;
     {
@@ -337,14 +338,6 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, (uint32_t)kTcTileN / 2, 1, 1};  // two boxes per stage (one on diagonal tiles)
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
-    float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
-    if (launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart))
-      return fail(BFLA_ERR_CUDA, "tc scores launch failed");
-    cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
-    if (ss) cudaStreamWaitEvent(st, ss->join, 0);
-    const int sms = num_sms_current();
-    launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
-                  1, qn, kn, certify_tau(g), flagged, nflag, sms, ulist);
     CUtensorMap rq, rk;  // token-row maps (64 x 64 SW128 boxes) for the TMA-staged recompute
     bool rmaps;
     {
@@ -355,6 +348,28 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, 64, 1, 1};
       rmaps = encode_4d_quiet(&rq, P->q, dq, sq, box) && encode_4d_quiet(&rk, kc, dk, sk, box);
     }
+    if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
+    if (g.paged) launch_paged_gather(g, P->k, P->page_table, ws + L.kgather, st);
+    // query-group norms come from the scores kernel (Gram diagonal, no extra HBM bytes); key-group
+    // norms (HBM-bound, K only) run on this thread's side stream concurrently, joined before the selection
+    static const bool q_norms_separate = experiment_knob("BFLA_QNORM_KERNEL", 0) == 1;  // A/B builds only
+    SideStream* ss = side_stream();
+    if (ss) {
+      cudaEventRecord(ss->fork, st);
+      cudaStreamWaitEvent(ss->s, ss->fork, 0);
+      launch_block_norms(gk, P->q, kc, qn, kn, ss->s, q_norms_separate);
+      cudaEventRecord(ss->join, ss->s);
+    } else {
+      launch_block_norms(gk, P->q, kc, qn, kn, st, q_norms_separate);
+    }
+    float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
+    const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart);
+    cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
+    if (ss) cudaStreamWaitEvent(st, ss->join, 0);  // joined even on failure: never leave a fork open
+    if (tc_err) return fail(BFLA_ERR_CUDA, "tc scores launch failed (%d)", tc_err);
+    const int sms = num_sms_current();
+    launch_select(g, S, c_alpha, cfg->select, cfg->gamma, cfg->keep_ratio, mask->coarse_bits, nullptr, stats, st,
+                  1, qn, kn, certify_tau(g, cfg->certify_slack), flagged, nflag, sms, ulist);
     if (launch_recompute_rows(gk, P->q, kc, nullptr, flagged, nflag, ulist, nflag + 1, S, sms, st, rmaps ? &rq : nullptr,
                               rmaps ? &rk : nullptr))
       return fail(BFLA_ERR_CUDA, "recompute launch failed");
@@ -362,6 +377,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
                   2, nullptr, nullptr, 0.f, flagged, nflag, sms);
     return cuda_check("bfla_block_mask launch");
   }
+  if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
   if (cfg->pool == BFLA_POOL_FLATTEN) {
     if (launch_flatten_scores(g, P->q, P->k, pt, S, st)) return fail(BFLA_ERR_UNSUPPORTED, "G not built");
   } else {
@@ -392,10 +408,7 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     // varlen padding (those must stay untouched); otherwise the kernel stores rows directly
     const uint64_t ostr[3] = {(uint64_t)g.os2 * 2, (uint64_t)g.os1 * 2, (uint64_t)g.os0 * 2};
     const bool oal = ((uintptr_t)P->o % 16 == 0) && ostr[0] % 16 == 0 && ostr[1] % 16 == 0 && ostr[2] % 16 == 0;
-    static const bool no_otma = [] {
-      const char* e = getenv("BFLA_OTMA");
-      return e && atoi(e) == 0;
-    }();
+    static const bool no_otma = experiment_knob("BFLA_OTMA", 1) == 0;  // A/B builds only
     maps.o_ok = 0;
     if (oal && !g.lens && !no_otma && encode_4d_quiet(&maps.o, P->o, dims, ostr, box)) maps.o_ok = 1;
   }
@@ -414,15 +427,9 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     if ((s = encode_4d(&maps.v, P->v, dims, str, box)) != BFLA_OK) return s;
   }
   // d = 128: the paired-tile kernel (attention2.cu); d = 256 (or BFLA_ATTN=1): one tile per step
-  static const bool v1 = [] {
-    const char* e = getenv("BFLA_ATTN");
-    return e && atoi(e) == 1;
-  }();
+  static const bool v1 = experiment_knob("BFLA_ATTN", 0) == 1;  // A/B builds only
   const int32_t* pt = g.paged ? P->page_table : nullptr;
-  static const bool no_dyn = [] {
-    const char* e = getenv("BFLA_DYN_SCHED");  // A/B: 0 = static round-robin items
-    return e && atoi(e) == 0;
-  }();
+  static const bool no_dyn = experiment_knob("BFLA_DYN_SCHED", 1) == 0;  // A/B builds: static round-robin
   if (no_dyn) sched = nullptr;
   if (sched) cudaMemsetAsync(sched, 0, sizeof(int32_t), st);
   int e = (g.D == 128 && !v1)
@@ -454,12 +461,13 @@ extern "C" {
 size_t bfla_workspace_size(const bfla_problem* problem, const bfla_config* config) {
   Geom g;
   if (make_geom(problem, config, &g) != BFLA_OK) return 0;
-  return ws_layout(g).total;
+  return ws_layout(g, config == nullptr).total;
 }
 
 int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* config) {
   Geom g;
-  if (make_geom(problem, config, &g) != BFLA_OK) return -1;
+  const bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return -(int64_t)s;
   return (int64_t)g.B * g.Hkv * g.causal_per_head;
 }
 
@@ -581,12 +589,13 @@ bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config,
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
   if (s != BFLA_OK) return s;
-  const WsLayout L = ws_layout(g);
   if (!config) {  // dense causal (Eq. 1); a workspace, if given, enables dynamic item scheduling
-    int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
-                                                  : nullptr;
+    const WsLayout Ld = ws_layout(g, true);
+    int32_t* sched = (ws && ws_bytes >= Ld.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + Ld.sched)
+                                                   : nullptr;
     return run_attention(g, problem, nullptr, nullptr, 1, st, sched);
   }
+  const WsLayout L = ws_layout(g);
   if (!ws || ws_bytes < L.total) return fail(BFLA_ERR_WORKSPACE, "workspace too small");
   unsigned char* w = static_cast<unsigned char*>(ws);
   bfla_mask local;

@@ -547,10 +547,7 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
   if (items == 0) return 0;
   const int n = (int)items;
   // softmax warpgroups per Q tile: 1 (default) or 2 (BFLA_SOFTMAX_SPLIT=2, A/B experiments)
-  static const int spl = [] {
-    const char* e = getenv("BFLA_SOFTMAX_SPLIT");
-    return (e && atoi(e) == 2) ? 2 : 1;
-  }();
+  static const int spl = experiment_knob("BFLA_SOFTMAX_SPLIT", 1) == 2 ? 2 : 1;
 #define BFLA_GO(D_, Q_, P_, X_)                                                                          \
   return spl == 2                                                                                        \
              ? launch_t<D_, Q_, P_, X_, 2>(g, maps, list, count, page_table, o, lse, n, hpq, NC, num_sms, st, sched) \

@@ -58,6 +58,14 @@ constexpr int BN = 64;    // mask tile T
 constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
 // lazy-rescale headroom (log2 units): p = 2^(x - m_run) <= 2^24; O <= 2^24 * N_kv * |V| << fp32 max
 constexpr float kLazy = 24.0f;
+// PINGPONG: the two softmax warpgroups take turns for the exponential phase of a step (named barriers
+// 3 / 4, 256 threads), so each runs its MUFU-heavy phase with the SM's exponential units to itself
+// instead of both phases stretching over each other while the tensor pipe waits on both
+#ifndef BFLA_PINGPONG
+#define BFLA_PINGPONG 0
+#endif
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int NQT, bool PAGED = false>
 struct Cfg2 {
@@ -436,6 +444,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     const uint32_t tS = tmem + lane_addr + C::COL_S + q * 128;
     const uint32_t tO = tmem + lane_addr + C::COL_O + q * D;
     const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
+    constexpr bool PP = BFLA_PINGPONG && NQT == 2 && SMX == 1;
+    if (PP && q == 1) named_bar_arrive(3, 256);  // tile 0 takes the first turn
     uint32_t st = 0, nit = 0;
     for (int idx, cnt; next_item(idx, cnt);) {
       const Item it = decode_item<SLICE>(g, idx, NC);
@@ -520,6 +530,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
           }
           tmem_wait_ld();
           if (lg == 0) TRACE(3 + q, 16);
+          if (PP && BFLA_PINGPONG == 2) named_bar_sync(3 + q, 256);  // my turn (max + exponentials)
           if (la < BN - 1) {
 #pragma unroll
             for (int c = 0; c < BN; ++c)
@@ -543,14 +554,18 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
           }
           const float msub = m_run == -INFINITY ? 0.0f : m_run;
           ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+          if (PP && BFLA_PINGPONG == 1) named_bar_sync(3 + q, 256);  // my turn: the other tile's exps are done
           exps64(v, 0, msub);
           tmem_st16(tS, pk);
           tmem_st16(tS + 16, pk + 16);
           if (lg == 0) TRACE(3 + q, 17);
           if (two) {
             exps64(v + BN, 1, msub);
+            if (PP) named_bar_arrive(4 - q, 256);  // hand the turn over
             tmem_st16(tS + 32, pk + 32);
             tmem_st16(tS + 48, pk + 48);
+          } else if (PP) {
+            named_bar_arrive(4 - q, 256);
           }
           if (lg == 0) TRACE(3 + q, 9);
           if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
@@ -725,15 +740,9 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
 template <int NQT, bool PAGED, bool DENSE>
 int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count, const int32_t* pt,
               void* o, float* lse, int n_items, int hpq, int NC, int num_sms, cudaStream_t st, int* sched) {
-  static const int smx = [] {
-    const char* e = getenv("BFLA_SMX");  // softmax variant (see k_attn2); default 1
-    const int v = e ? atoi(e) : 1;
-    return v == 0 ? 0 : 1;
-  }();
-  static const int opts = [] {
-    const char* e = getenv("BFLA_ATTN_OPTS");  // experiment switches (bit 0: no Q prefetch)
-    return e ? atoi(e) : 0;
-  }();
+  // softmax variant (see k_attn2; default 1) and experiment switches (bit 0: no Q prefetch): A/B builds only
+  static const int smx = experiment_knob("BFLA_SMX", 1) == 0 ? 0 : 1;
+  static const int opts = experiment_knob("BFLA_ATTN_OPTS", 0);
   const int grid = n_items < num_sms ? n_items : num_sms;
   auto go = [&](auto kern, int smem, int threads) -> int {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

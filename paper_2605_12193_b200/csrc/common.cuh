@@ -2,10 +2,24 @@
 // (mbarrier, TMA, tcgen05/TMEM).  Product path only: the CPU oracle shares nothing with this.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace bfla {
+
+// Experiment switches for same-box A/B measurements.  They exist only in builds compiled with
+// -DBFLA_EXPERIMENTS (tools/ab_build.py); the product library never reads the environment and
+// always takes the default, so no variable can change its results or weaken the certification.
+inline int experiment_knob(const char* name, int dflt) {
+#ifdef BFLA_EXPERIMENTS
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
 
 // ------------------------------------------------------------------------------------------
 // Geometry of one call (computed once on the host, passed by value to every kernel).
@@ -115,8 +129,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef BFLA_DEBUG
+  // debug builds (build.py --debug -> libbfla_debug.so): a wait that never completes — a lost TMA
+  // transaction, a bad list entry or descriptor — traps after ~2 s instead of hanging the GPU
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1LL << 32)) {
+      printf("bfla: mbarrier timeout: block %d thread %d bar smem 0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // TMA: 4-D tiled load global -> shared, completion on an mbarrier (transaction bytes).

@@ -846,10 +846,7 @@ int tc_splits(const Geom& g) {
   const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
   const long long tiles = (long long)g.B * g.Hq * ((ngq + TM - 1) / TM) * ((ngk + TN - 1) / TN);
   const int nk = g.g * g.D / TK;
-  static const int forced = [] {
-    const char* e = getenv("BFLA_TC_SPLITS");
-    return e ? atoi(e) : 0;
-  }();
+  static const int forced = experiment_knob("BFLA_TC_SPLITS", 0);  // A/B builds only
   int s = forced > 0 ? forced : (tiles >= 2 * 148 ? 1 : (int)((2 * 148 + tiles - 1) / tiles));
   if (s > 8) s = 8;
   while (s > 1 && nk / s < 16) --s;
@@ -899,10 +896,8 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
   if (g.G * g.G > kRecThreads) return -1;
   auto qq = static_cast<const __nv_bfloat16*>(q);
   auto kk = static_cast<const __nv_bfloat16*>(k);
-  static const int mode = [] {
-    const char* e = getenv("BFLA_RECOMPUTE");  // experiments: 0 auto (TMA), 1 global loads, 2 bulk rows
-    return e ? atoi(e) : 0;
-  }();
+  // A/B builds only: 0 auto (TMA), 1 global loads, 2 bulk rows
+  static const int mode = experiment_knob("BFLA_RECOMPUTE", 0);
   {
     const size_t smem_t = (size_t)3 * g.b * g.D * 2 + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4 + 1024;
     if (mode == 0 && tmQ && tmK && g.D == 128 && g.G <= 8 && g.b % 64 == 0 && smem_t <= 226 * 1024) {

@@ -152,19 +152,22 @@ class BalancedLayer:
 
         st = torch.cuda.current_stream() if stream is None else stream
         rec = (lambda k: marks[k].record(st)) if marks is not None else (lambda k: None)
-        rec(0)
-        bfla_block_mask(self.Ps, self.cfg, self.ms, self.wss, st)
-        bfla_expand_rescue(self.Ps, self.cfg, self.ms, self.wss, st)
-        rec(1)
-        tl, tc = gather_mask_lists(self.ms.tile_list, self.ms.tile_count, self.B, self.world, self.group)
-        self.m.tile_list[:tl.numel()].copy_(tl.reshape(-1))
-        self.m.tile_count.view(tc.shape).copy_(tc)
-        self.counts_host.copy_(self.m.tile_count, non_blocking=True)
-        st.synchronize()  # the slice bounds are host decisions (a few KB of counts)
-        r0, r1 = balanced_slice(self.counts_host.view(self.B, self.Hkv, -1), self.world, self.rank, self.ovh)
-        self.bounds = (r0, r1)
-        rec(2)
-        self.o.zero_()
-        bfla_sparse_prefill_rows(self.P, self.cfg, self.m, r0, r1, self.ws, st)
-        rec(3)
-        assemble_rows(self.o, None, self.group)
+        # every op of the layer — library calls, collectives, copies, the zero-fill — goes to `st`,
+        # so a non-current stream orders them exactly like the current one
+        with torch.cuda.stream(st):
+            rec(0)
+            bfla_block_mask(self.Ps, self.cfg, self.ms, self.wss, st)
+            bfla_expand_rescue(self.Ps, self.cfg, self.ms, self.wss, st)
+            rec(1)
+            tl, tc = gather_mask_lists(self.ms.tile_list, self.ms.tile_count, self.B, self.world, self.group)
+            self.m.tile_list[:tl.numel()].copy_(tl.reshape(-1))
+            self.m.tile_count.view(tc.shape).copy_(tc)
+            self.counts_host.copy_(self.m.tile_count, non_blocking=True)
+            st.synchronize()  # the slice bounds are host decisions (a few KB of counts)
+            r0, r1 = balanced_slice(self.counts_host.view(self.B, self.Hkv, -1), self.world, self.rank, self.ovh)
+            self.bounds = (r0, r1)
+            rec(2)
+            self.o.zero_()
+            bfla_sparse_prefill_rows(self.P, self.cfg, self.m, r0, r1, self.ws, st)
+            rec(3)
+            assemble_rows(self.o, None, self.group)

@@ -26,21 +26,37 @@ CASES = {
     # Qwen3-32B-like, 64K, vLLM pages of 16, all rescues (BASELINE.json configs[3])
     "qwen32b-64k-paged": dict(Hq=64, Hkv=8, d=128, N=65536, b=256, g=64, gamma=0.99, eta=16, rho=0.1, paged=16,
                               theta=1e6, seed=404),
-    # Gemma-like d=256 GQA shape (BASELINE.json configs[4]) at 32K
+    # Gemma-like d=256 GQA shape (BASELINE.json configs[4]) at 32K and at the top of its 4K-128K sweep
     "gemma-d256-32k": dict(Hq=16, Hkv=8, d=256, N=32768, b=256, g=64, gamma=0.99, eta=16, rho=0.0, paged=0,
                            theta=1e6, seed=505),
+    "gemma-d256-128k": dict(Hq=16, Hkv=8, d=256, N=131072, b=256, g=64, gamma=0.99, eta=16, rho=0.0, paged=0,
+                            theta=1e6, seed=505),
+    "gemma-d256-128k-ratio0.1": dict(Hq=16, Hkv=8, d=256, N=131072, b=256, g=64, gamma=0.99, eta=16, rho=0.0,
+                                     paged=0, theta=1e6, seed=505, keep_ratio=0.1),
+    # the Llama-32K keep-mass threshold sweep of BASELINE.json configs[1] (Tab.mask gamma values) and
+    # the north_star's keep-ratio rule at the same shape
+    "llama8b-32k-gamma0.9": dict(Hq=32, Hkv=8, d=128, N=32768, b=256, g=64, gamma=0.9, eta=16, rho=0.0, paged=0,
+                                 theta=5e5, seed=303),
+    "llama8b-32k-gamma0.95": dict(Hq=32, Hkv=8, d=128, N=32768, b=256, g=64, gamma=0.95, eta=16, rho=0.0, paged=0,
+                                  theta=5e5, seed=303),
+    "llama8b-32k-gamma0.999": dict(Hq=32, Hkv=8, d=128, N=32768, b=256, g=64, gamma=0.999, eta=16, rho=0.0,
+                                   paged=0, theta=5e5, seed=303),
+    "llama8b-32k-ratio0.1": dict(Hq=32, Hkv=8, d=128, N=32768, b=256, g=64, gamma=0.99, eta=16, rho=0.0, paged=0,
+                                 theta=5e5, seed=303, keep_ratio=0.1),
 }
 
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_fullsize(name):
     c = CASES[name]
+    ratio = c.get("keep_ratio", 0.0)
+    sel = dict(select=bf.SELECT_RATIO, keep_ratio=ratio) if ratio else {}
     N, Hq, Hkv, d = c["N"], c["Hq"], c["Hkv"], c["d"]
     prob = workloads.structured(c["seed"], 1, Hq, Hkv, N, N, d, block=c["b"], theta=c["theta"], device="cuda")
     q, k, v = prob.q, prob.k, prob.v
     o = torch.empty_like(q)
     lse = torch.empty(1, Hq, N, dtype=torch.float32, device="cuda")
-    cfg = bf.Config(b=c["b"], g=c["g"], T=64, gamma=c["gamma"], n_local=8, eta=c["eta"], rho=c["rho"])
+    cfg = bf.Config(b=c["b"], g=c["g"], T=64, gamma=c["gamma"], n_local=8, eta=c["eta"], rho=c["rho"], **sel)
     if c["paged"]:
         kc, vc, pt = workloads.paged(k, v, c["paged"], seed=c["seed"])
         P = bf.make_problem(q, kc, vc, o, lse, page_table=pt, n_kv=N)
@@ -55,7 +71,7 @@ def test_fullsize(name):
     st = m.stats_dict()
     qf, kf, vf = (t[0].float().cpu().numpy() for t in (q, k, v))
     ref = oracle.mask_pipeline(qf, kf, b=c["b"], g=c["g"], T=64, gamma=c["gamma"], n_local=8, eta=c["eta"],
-                               rho=c["rho"])
+                               rho=c["rho"], select_mode=cfg.select, keep_ratio=cfg.keep_ratio)
     assert np.array_equal(m.coarse_dense()[0].cpu().numpy(), ref["coarse"]), "coarse mask mismatch"
     labels = m.tile_label[0].cpu().numpy()
     assert np.array_equal(labels, ref["labels"]), "tile mask mismatch"

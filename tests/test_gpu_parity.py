@@ -3,6 +3,7 @@
 Masks (coarse bits, tile labels, lists, counts) must be bit-exact; O within max-abs 2e-2 and
 mean-abs 2e-3 of the fp64 oracle (BASELINE.json).  Sizes span several tiles and ragged tails."""
 import ctypes
+import dataclasses
 
 import numpy as np
 import pytest
@@ -120,10 +121,14 @@ def test_fast_scores_certified_equal_canonical(dist, gamma):
     bound = qn[:, :, None] * np.repeat(kn, 4, axis=0)[:, None, :]
     tri = np.tril(np.ones((Lq, Lkv), bool))
     ratio = (np.abs(S_fast - S_can) / bound)[:, tri].max()
-    n = 64 * 128
-    tau = 2.0 ** -24 * (10 * (128 + 64) ** 0.5 + n / 8)  # api.cu certify_tau (two-level canonical order)
-    print(f"max |S_tc - S_canon| / (|x||y|) = {ratio:.3e}  (tau = {tau:.3e})")
-    assert ratio < tau / 8
+    n, u = 64 * 128, 2.0 ** -24
+    # api.cu certify_tau: worst-case canonical term gamma_{C+g} plus the tensor-core chain (2 n/16 u);
+    # 2 u per split-K partial is not counted here (it only makes tau larger)
+    tau = (128 + 64) * u / (1 - (128 + 64) * u) + u * n / 8
+    print(f"max |S_tc - S_canon| / (|x||y|) = {ratio:.3e}  (tau = {tau:.3e}, ratio {ratio / tau:.3f})")
+    # the bound is a worst case (every rounding of both orders aligned); on these inputs the
+    # observed difference must sit at most a quarter of it, so the certification has >= 4x headroom
+    assert ratio < tau / 4
 
 
 def _ws_norms(ws: torch.Tensor, B, Hq, Hkv, Nq, Nkv, d, b, T=64, paged=False):
@@ -232,16 +237,15 @@ def test_keep_ratio_fast_path(ratio):
 
 @pytest.mark.parametrize("d", [128, 256])
 @pytest.mark.parametrize("ratio", [0.05, 0.3])
-def test_keep_ratio_recompute_band(monkeypatch, ratio, d):
+def test_keep_ratio_recompute_band(ratio, d):
     """Keep-ratio rows that fail certification recompute only the blocks whose fast score lies in the
     band s_cut -/+ 2d around the cut (stage1_select.cu): outside it the rank against the canonical
-    k-th score is already certain.  A widened error bound (BFLA_TAU_SCALE) flags most rows and widens
-    every band, so rows mix fast and canonical scores; the mask must still equal the oracle's bit for
-    bit (d = 128: TMA recompute kernel; d = 256: the global-load one)."""
-    monkeypatch.setenv("BFLA_TAU_SCALE", "3000")
+    k-th score is already certain.  A widened error bound (bfla_config.certify_slack) flags most rows and
+    widens every band, so rows mix fast and canonical scores; the mask must still equal the oracle's bit
+    for bit (d = 128: TMA recompute kernel; d = 256: the chunked TMA one)."""
     prob = workloads.structured(10, B=1, Hq=4, Hkv=2, Nq=3072, Nkv=3072, d=d, block=256)
     kw = dict(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=ratio)
-    fast = run_gpu(prob, bf.Config(**kw, scores=bf.SCORES_AUTO), lse=False)
+    fast = run_gpu(prob, bf.Config(**kw, scores=bf.SCORES_AUTO, certify_slack=3000.0), lse=False)
     assert fast["stats"]["rows_flagged"] >= 8, fast["stats"]
     _check_masks(fast, oracle_masks(prob, bf.Config(**kw)), None)
 
@@ -606,3 +610,37 @@ def test_cuda_graph_capture_of_whole_path():
         assert torch.equal(got[0], o) and torch.equal(got[1], m.tile_count) and torch.equal(got[2], m.coarse_bits)
         outs.append(got[0])
     assert not torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("paged", [0, 16])
+def test_chunked_prefill_tensor_core_stage1(paged):
+    """Aligned chunked prefill (the vLLM case: N_c > 0 with n_q, n_kv multiples of g) takes the
+    tensor-core Stage-1 path (tcgen05 scores + certification + canonical recompute); masks bit-exact
+    against the oracle and equal to the all-canonical path, O on sampled rows within tolerance.
+    n_q = 8192 queries attend to n_kv = 32768 keys (N_c = 24576, Eq. 11-13, R18)."""
+    Hq, Hkv, Nq, Nkv, d = 8, 2, 8192, 32768, 128
+    prob = workloads.structured(18, B=1, Hq=Hq, Hkv=Hkv, Nq=Nq, Nkv=Nkv, d=d, block=256)
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.1, seed=11)
+    n0 = bf.kernel_launches()
+    fast = run_gpu(prob, cfg, paged_page=paged, lse=True)
+    n_fast = bf.kernel_launches() - n0
+    n0 = bf.kernel_launches()
+    canon = run_gpu(prob, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), paged_page=paged, lse=False)
+    n_canon = bf.kernel_launches() - n0
+    # the AUTO call ran the tensor-core chain (norms + tcgen05 scores + select + recompute + re-select),
+    # not the canonical SIMT fallback (scores + select)
+    assert n_fast > n_canon, (n_fast, n_canon)
+    assert np.array_equal(fast["coarse"], canon["coarse"]) and np.array_equal(fast["labels"], canon["labels"])
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(fast, ref, cfg)
+    check_lists(fast, labels, Nq, Nkv, 64)
+    tiles = list(range(0, Nq // 64, 16)) + [Nq // 64 - 1]
+    rows = np.array([[p, i * 64 + r] for p in range(Hq) for i in tiles for r in range(64)], np.int32)
+    (o_ref, lse_ref), = oracle_attention(prob, labels, 64, rows_per_req=[rows])
+    og = fast["o"][0].float().cpu().numpy()[rows[:, 0], rows[:, 1]].astype(np.float64)
+    err = np.abs(og - o_ref)
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+    lg = fast["lse"][0].cpu().numpy()[rows[:, 0], rows[:, 1]]
+    assert np.abs(lg - lse_ref).max() <= 1e-3
+    print(f"chunked TC paged={paged}: kappa={fast['stats']['kept_tiles'] / fast['stats']['causal_tiles']:.3f} "
+          f"flagged={fast['stats']['rows_flagged']} max-abs={err.max():.2e}")

@@ -194,6 +194,41 @@ def test_block_scores_mean_pool_integer(orc):
     assert np.isneginf(S[:, ~tri]).all()
 
 
+def test_block_scores_mean_pool_ragged_blocks(orc):
+    # MEAN (R1, R3) on ragged tails: the mean of a partial block divides by its REAL token count
+    # (5 and 3 here, not b = 16).  Integer tokens are built so every channel sum of a partial block is
+    # a multiple of its count, so the means are exact integers and the scores exact (|S| << 2^24).
+    rng = np.random.default_rng(6)
+
+    def ragged(h, n, b, c):
+        x = rng.integers(-3, 4, size=(h, n, c)).astype(np.float32)
+        n_last = n % b
+        tail = x[:, n - n_last:]
+        target = rng.integers(-2, 3, size=(h, c)).astype(np.float32)
+        tail[:, -1] = n_last * target - tail[:, :-1].sum(1)  # channel sum = n_last * target
+        return x
+
+    for nq, nkv in ((37, 37), (35, 51)):  # square ragged; chunked (N_c = 16) with different tails
+        q = ragged(2, nq, 16, 8)
+        k = ragged(1, nkv, 16, 8)
+        S = orc.block_scores(q, k, 16, 16, orc.POOL_MEAN)
+        Lq, Lkv, nc = -(-nq // 16), -(-nkv // 16), nkv - nq
+        qm = np.stack([q[:, 16 * i:min(nq, 16 * i + 16)].astype(np.float64).mean(1) for i in range(Lq)], 1)
+        km = np.stack([k[0, 16 * j:min(nkv, 16 * j + 16)].astype(np.float64).mean(0) for j in range(Lkv)], 0)
+        # partial-block means are integers by construction; full-block means are dyadic (/16): all exact
+        assert np.array_equal(qm[:, -1], np.round(qm[:, -1])) and np.array_equal(km[-1], np.round(km[-1]))
+        ref = np.einsum("pic,jc->pij", qm, km)
+        for i in range(Lq):
+            e_i = min(nc + 16 * (i + 1) - 1, nkv - 1)  # Eq. 11-13
+            for j in range(Lkv):
+                if 16 * j <= e_i:
+                    assert S[0, i, j] == ref[0, i, j] and S[1, i, j] == ref[1, i, j], (nq, nkv, i, j)
+                else:
+                    assert np.isneginf(S[:, i, j]).all()
+        # the divisor matters: with b = 16 in place of the real count the last blocks would differ
+        assert not np.allclose(k[0, 16 * (Lkv - 1):].sum(0) / 16, km[-1])
+
+
 # ---------------------------------------------------------------- Eq. 15
 def test_exp2_canon_accuracy(orc):
     ts = np.concatenate([np.linspace(-126, 0, 20001), -np.logspace(-8, 0, 500)]).astype(np.float32)

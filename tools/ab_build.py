@@ -1,19 +1,14 @@
-"""Build an A/B variant of libbfla.so: the attention2 unit recompiled with extra -D flags.
+"""Build an A/B variant of the library: every unit recompiled with -DBFLA_EXPERIMENTS (the environment
+switches of common.cuh experiment_knob) plus extra -D flags.
 
   python tools/ab_build.py NAME -DFOO=1 ...   ->  paper_2605_12193_b200/libbfla_NAME.so
-Select it at run time with BFLA_LIB_VARIANT=NAME (experiments only; never used by tests)."""
+Select it in a tool with paper_2605_12193_b200._lib.use_variant(NAME) (experiments only; never used by
+the product path or the tests)."""
 import os
-import subprocess
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_12193_b200 import build as B  # noqa: E402
 
 name, flags = sys.argv[1], sys.argv[2:]
-B.build()
-obj = os.path.join(B.BUILD, f"attention2_{name}.o")
-subprocess.check_call([B.nvcc(), *B.ARCH, *B.COMMON, *flags, "-c", os.path.join(B.CSRC, "attention2.cu"), "-o", obj])
-objs = [os.path.join(B.BUILD, u.replace(".cu", ".o")) for u in B.UNITS if u != "attention2.cu"]
-out = os.path.join(B.HERE, f"libbfla_{name}.so")
-subprocess.check_call([B.nvcc(), *B.ARCH, "-shared", "-o", out, *objs, obj])
-print(out)
+print(B.build(variant=name, extra=flags))

@@ -1,6 +1,6 @@
 """Timeline of the paired-tile attention kernel (k_attn2) from the instrumented build.
 
-Run on a GPU box:  BFLA_TRACE_LIB=1 python tools/attn_trace.py [--dense] [--workload llama8b-32k]
+Run on a GPU box:  python tools/attn_trace.py [--dense] [--workload llama8b-32k]
 (after `python -m paper_2605_12193_b200.build --trace`).  CTAs 0..3 record clock64 stamps per warp
 role; this script prints, per role, the mean spacing between events, i.e. where a step's cycles go:
 
@@ -16,7 +16,6 @@ import sys
 
 import numpy as np
 
-os.environ["BFLA_TRACE_LIB"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
@@ -24,6 +23,8 @@ import torch  # noqa: E402
 import paper_2605_12193_b200 as bf  # noqa: E402
 import workloads  # noqa: E402
 from paper_2605_12193_b200 import _lib  # noqa: E402
+
+_lib.use_variant("trace")
 
 CTAS, ROLES, NEV = 4, 6, 8192
 

@@ -1,5 +1,6 @@
 """Live timing of bfla_block_mask on a BASELINE workload (CUDA events, 20 reps after warm-up), printing
-the flagged-row statistics; run under different BFLA_* experiment env vars to attribute Stage-1 time."""
+the flagged-row statistics; with --variant NAME (an A/B build of tools/ab_build.py) and BFLA_* experiment env vars to attribute
+Stage-1 time."""
 import argparse
 import os
 import sys
@@ -17,7 +18,9 @@ ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--ratio", type=float, default=0.0, help="keep-ratio selection (R9) instead of gamma")
+ap.add_argument("--variant", default="", help="libbfla_<variant>.so (tools/ab_build.py)")
 a = ap.parse_args()
+bf._lib.use_variant(a.variant)
 prob = workloads.structured(303, 1, a.hq, a.hkv, a.n, a.n, a.d, block=256, theta=5e5, device="cuda")
 o = torch.empty_like(prob.q)
 cfg = bf.Config(b=256, g=64, T=64, gamma=0.99, n_local=8, eta=16, rho=0.0)

@@ -6,12 +6,13 @@ Run on a GPU box:  compute-sanitizer --tool memcheck python tools/sanitize_cases
 import os
 import sys
 
-os.environ.setdefault("BFLA_TAU_SCALE", "50")  # force flagged rows so the recompute kernel runs
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2605_12193_b200 as bf  # noqa: E402
 import workloads  # noqa: E402
+
+SLACK = 50.0  # bfla_config.certify_slack: widen tau so rows are flagged and the recompute kernels run
 
 
 def run(prob, cfg, paged=0, slices=0):
@@ -43,8 +44,8 @@ def run(prob, cfg, paged=0, slices=0):
 def main():
     g1 = workloads.gaussian(5, B=1, Hq=8, Hkv=2, Nq=2048, Nkv=2048, d=128, sigma=0.8)
     cases = [
-        ("tc scores + recompute", g1, bf.Config(b=256, g=64, eta=4, rho=0.1), 0),
-        ("keep-ratio", g1, bf.Config(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=0.2), 0),
+        ("tc scores + recompute", g1, bf.Config(b=256, g=64, eta=4, rho=0.1, certify_slack=SLACK), 0),
+        ("keep-ratio", g1, bf.Config(b=256, g=64, select=bf.SELECT_RATIO, keep_ratio=0.2, certify_slack=SLACK), 0),
         ("per-query-head masks", g1, bf.Config(b=256, g=64, mask_groups=bf.MASK_PER_Q_HEAD), 0),
         ("paged", g1, bf.Config(b=256, g=64), 16),
         ("canonical SIMT, ragged chunk", workloads.gaussian(6, B=1, Hq=4, Hkv=1, Nq=1000, Nkv=1500, d=128, sigma=0.8),
