@@ -111,6 +111,88 @@ def make_inputs(w, seed, device):
                                 device=device)
 
 
+def stage1_work(w, Hq=None, Hkv=None):
+    """Algorithmic Stage-1 work of one layer: FLATTEN group scores over the causal block
+    pairs, Eq. 30: 2 * Hq * sum_causal G^2 * g * C flop; bytes = Q and K read once (bf16)."""
+    Hq = w["Hq"] if Hq is None else Hq
+    Hkv = w["Hkv"] if Hkv is None else Hkv
+    N, b, g, d = w["N"], w["b"], w["g"], w["d"]
+    L = -(-N // b)
+    G = b // g
+    flops = 2.0 * Hq * (L * (L + 1) // 2) * G * G * g * d
+    nbytes = 2.0 * (Hq + Hkv) * N * d
+    return flops, nbytes
+
+
+def stage1_roofline(w, s1_ms, peaks, Hq=None, Hkv=None):
+    flops, nbytes = stage1_work(w, Hq, Hkv)
+    gbs = nbytes / (s1_ms * 1e-3) / 1e9
+    tfs = flops / (s1_ms * 1e-3) / 1e12
+    ridge = peaks["bf16"] * 1e12 / (peaks["hbm"] * 1e9)  # FLOP/B where the two roofs meet
+    bound = "hbm" if flops / nbytes < ridge else "tensor"
+    frac = gbs / peaks["hbm"] if bound == "hbm" else tfs / peaks["bf16"]
+    t_bound_ms = max(nbytes / (peaks["hbm"] * 1e9), flops / (peaks["bf16"] * 1e12)) * 1e3
+    return {"bound": bound, "achieved_gbs": gbs, "achieved_tflops": tfs, "peak_gbs": peaks["hbm"],
+            "peak_tflops": peaks["bf16"], "frac": frac, "bound_ms": t_bound_ms, "frac_of_bound_time": t_bound_ms / s1_ms,
+            "algorithmic_bytes": nbytes, "algorithmic_flops": flops, "intensity_flop_per_byte": flops / nbytes,
+            "measured": "CUDA events around bfla_block_mask (whole Stage 1: scores, norms, selection, recompute)"}
+
+
+def layer_timing(name, dev, reps=3, dense_reps=2, tile=64):
+    """One extra workload on this GPU (the default line's 128K point): Stage 1 / Stage 2 / sparse prefill
+    with CUDA events (eager, reps after 2 warm-ups) and the dense comparator; inputs resident in HBM."""
+    import torch
+
+    import paper_2605_12193_b200 as bf
+
+    w = dict(WORKLOADS[name], T=tile)
+    prob = make_inputs(w, 303, dev)
+    q, k, v = prob.q, prob.k, prob.v
+    o = torch.empty_like(q)
+    cfg = bf.Config(b=w["b"], g=w["g"], T=w["T"], gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"])
+    P = bf.make_problem(q, k, v, o)
+    ws = bf.alloc_workspace(P, cfg)
+    m = bf.alloc_mask(P, cfg)
+    st = torch.cuda.current_stream()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps + 2)]
+    for e in evs:
+        e[0].record(st)
+        bf.bfla_block_mask(P, cfg, m, ws)
+        e[1].record(st)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        e[2].record(st)
+        bf.bfla_sparse_prefill(P, cfg, m, ws)
+        e[3].record(st)
+    torch.cuda.synchronize()
+    evs = evs[2:]
+    med = lambda a, b_: statistics.median(e[a].elapsed_time(e[b_]) for e in evs)
+    s1, s2, at, tot = med(0, 1), med(1, 2), med(2, 3), med(0, 3)
+    wsd = bf.alloc_workspace(P, None)
+    bf.bfla_prefill(P, None, None, wsd)
+    de = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    de[0].record(st)
+    for _ in range(dense_reps):
+        bf.bfla_prefill(P, None, None, wsd)
+    de[1].record(st)
+    torch.cuda.synchronize()
+    dense_ms = de[0].elapsed_time(de[1]) / dense_reps
+    stats = m.stats_dict()
+    peaks = load_peaks()
+    kept = stats["kept_tiles"]
+    achieved = 4.0 * w["d"] * (w["Hq"] // w["Hkv"]) * w["T"] * w["T"] * kept / (at * 1e-3) / 1e12
+    N = w["N"]
+    out = {"workload": name, "ms_per_layer": tot, "stages_ms": {"stage1_scores_select": s1,
+           "stage2_expand_rescue": s2, "sparse_prefill": at}, "kappa": kept / max(1, stats["causal_tiles"]),
+           "dense_ms": dense_ms, "speedup_vs_dense": dense_ms / tot,
+           "sparse_roofline_frac": achieved / peaks["bf16"], "sparse_tflops": achieved,
+           "dense_roofline_frac": 4.0 * w["d"] * w["Hq"] * N * (N + 1) / 2 / (dense_ms * 1e-3) / 1e12 / peaks["bf16"],
+           "stage1_roofline": stage1_roofline(w, s1, peaks), "rows_flagged": stats["rows_flagged"],
+           "timing": f"CUDA events, median of {reps} eager layers after 2 warm-ups; dense mean of {dense_reps}"}
+    del prob, q, k, v, o, ws, m, wsd
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, w, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -138,12 +220,14 @@ def run_ours(args, w, rank, world, local_rank):
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
         del full
         Hq, Hkv = q.shape[1], k.shape[1]
-        o_full = torch.empty(1, w["Hq"], N, d, dtype=torch.bfloat16, device=dev)
+        # rank-major full O: this rank's heads are one contiguous chunk the kernel writes in place, and
+        # one in-place all_gather_into_tensor assembles the layer (no staging buffer, cat or copy)
+        hout = parallel.HeadShardedOutput(1, w["Hq"], N, d, world, rank, dev)
     else:
         prob = make_inputs(w, 303 + rank, dev)
         q, k, v = prob.q, prob.k, prob.v
         head_offset = rank * Hkv
-    o = torch.empty_like(q)
+    o = hout.local if heads else torch.empty_like(q)
     cfg = bf.Config(b=w["b"], g=w["g"], T=w["T"], gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"],
                     pool=bf.POOL_MEAN if args.pool == "mean" else bf.POOL_FLATTEN)
     if w["paged"]:
@@ -157,7 +241,6 @@ def run_ours(args, w, rank, world, local_rank):
         layer = parallel.BalancedLayer(q, k, v, o, cfg, rank, world)
         m = layer.ms  # stats of this rank's head group (Stage 1/2 certification)
     st = torch.cuda.current_stream()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
     def step(record=None):
         if bal:  # stages: masks (own heads) | list gather + slice | prefill slice, then O all-reduce
@@ -174,8 +257,10 @@ def run_ours(args, w, rank, world, local_rank):
         bf.bfla_sparse_prefill(P, cfg, m, ws)
         if record is not None:
             record[3].record(st)
-        if heads:  # the only exchange of the path: all-gather O of the head groups (NCCL)
-            o_full.copy_(parallel.gather_heads(o, world))
+        if heads:  # the only exchange of the path: in-place all-gather of O's head groups (NCCL)
+            hout.gather()
+        if record is not None:
+            record[4].record(st)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -204,7 +289,7 @@ def run_ours(args, w, rank, world, local_rank):
         torch.cuda.synchronize()
 
     # ---- timed region: exactly K steps (graph replays, or eager with per-stage events) ----
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -230,14 +315,19 @@ def run_ours(args, w, rank, world, local_rank):
                 evs[s][k_].record(st)
                 sg.replay()
             evs[s][3].record(st)
+            evs[s][4].record(st)
         torch.cuda.synchronize()
     s1 = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
     s2 = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
     at = statistics.median(e[2].elapsed_time(e[3]) for e in evs)
+    gather_ms = statistics.median(e[3].elapsed_time(e[4]) for e in evs) if heads else None
+    rank_ms = [total_ms / args.steps]
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rank_ms = [float(x.item()) / args.steps for x in allt]
+        total_ms = max(float(x.item()) for x in allt)
     ms_per_step = total_ms / args.steps
 
     # ---- dense comparator (same kernel template, all causal tiles; not part of the step) ----
@@ -280,10 +370,14 @@ def run_ours(args, w, rank, world, local_rank):
     qh = q.cpu().pin_memory()
     kh, vh = (kc.cpu().pin_memory(), vc.cpu().pin_memory()) if w["paged"] else (k.cpu().pin_memory(), v.cpu().pin_memory())
     ohs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for _ in range(2)]
-    bufs = []
+    bufs, houts = [], []
     for _ in range(2):
         qd, kd, vd = torch.empty_like(q), torch.empty_like(kh, device=dev), torch.empty_like(vh, device=dev)
-        od = torch.empty_like(o)
+        if heads:
+            houts.append(parallel.HeadShardedOutput(1, w["Hq"], N, d, world, rank, dev))
+            od = houts[-1].local
+        else:
+            od = torch.empty_like(o)
         if w["paged"]:
             Pb = bf.make_problem(qd, kd, vd, od, page_table=pt, n_kv=N, head_offset=rank * Hkv)
         else:
@@ -324,8 +418,8 @@ def run_ours(args, w, rank, world, local_rank):
             bf.bfla_block_mask(Pb, cfg, m, ws)
             bf.bfla_expand_rescue(Pb, cfg, m, ws)
             bf.bfla_sparse_prefill(Pb, cfg, m, ws)
-        if heads:
-            o_full.copy_(parallel.gather_heads(od, world))
+        if heads:  # device-side exchange of the step; each rank then reads back its own heads
+            houts[i % 2].gather()
         ev_done[i].record(st)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_done[i])
@@ -361,7 +455,18 @@ def run_ours(args, w, rank, world, local_rank):
         tr = json.load(open(prof)).get(args.workload, {})
         traffic = tr.get("attention_bytes")
         pipe_pct = tr.get("tensor_pipe_active_pct")
+    s1_roof = stage1_roofline(w, s1, peaks, Hq, Hkv) if not bal else None
+    extra = {}
+    if world == 1 and args.extra_128k and w["N"] < 131072 and not w["paged"]:
+        extra["llama8b_128k"] = layer_timing("llama8b-128k", dev)
+    n1_ms = None
+    if heads:  # the same (unsharded) layer on one GPU, for the driver's strong-scaling efficiency
+        if rank == 0:
+            n1_ms = layer_timing(args.workload, dev, reps=3, dense_reps=1)["ms_per_layer"]
+        dist.barrier()
     res = dict(graph=graph is not None, ms_per_step=ms_per_step, s1=s1, s2=s2, at=at, dense_ms=dense_ms, sdpa_ms=sdpa_ms, kappa=kappa, stats=stats,
+               s1_roof=s1_roof, extra=extra, gather_ms=gather_ms, rank_ms=rank_ms, n1_ms=n1_ms,
+               o_bytes=2.0 * w["Hq"] * w["N"] * w["d"],
                launches=launches, clk=clk.summary(), e2e_ms=e2e_ms, h2d=h2d, d2h=d2h, peaks=peaks,
                achieved_tf=achieved_tf, dense_tf=dense_tf, traffic=traffic, retained_flops=retained_flops,
                pipe_pct=pipe_pct)
@@ -417,22 +522,41 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="llama8b-32k", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="auto", choices=["auto"] + sorted(WORKLOADS),
+                    help="auto: llama8b-32k at 1 GPU (BASELINE configs[1]); llama8b-128k KV-head sharded at N>1 "
+                         "(configs[2])")
     ap.add_argument("--pool", default="flatten", choices=["flatten", "mean"])
     ap.add_argument("--tile", type=int, default=64, choices=[64, 128], help="mask tile T (Eq. 19)")
-    ap.add_argument("--shard", default="layers", choices=["layers", "heads", "balanced"],
+    ap.add_argument("--shard", default="auto", choices=["auto", "layers", "heads", "balanced"],
                     help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O "
                          "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
-                         "slices + O all-reduce (strong, SURVEY §8 f2)")
+                         "slices + O all-reduce (strong, SURVEY §8 f2); auto: heads at N>1 (north_star)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
                     help="1: time CUDA-graph replays of the captured step (layers sharding); 0: eager launches "
                          "(default: at 32K+ the two measure the same within 0.3%%, and eager stage events add up)")
+    ap.add_argument("--extra-128k", type=int, default=1, choices=[0, 1],
+                    help="1 GPU: also time the Llama-128K layer (sparse path + dense) into the line")
     args = ap.parse_args()
-    w = dict(WORKLOADS[args.workload], T=args.tile)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: spawn one rank per GPU on this node (127.0.0.1 rendezvous)
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.workload == "auto":
+        args.workload = "llama8b-128k" if world > 1 else "llama8b-32k"
+    if args.shard == "auto":
+        args.shard = "heads" if world > 1 else "layers"
+    w = dict(WORKLOADS[args.workload], T=args.tile)
     config = {"workload": args.workload, "h_q": w["Hq"], "h_kv": w["Hkv"], "head_dim": w["d"], "n": w["N"],
               "b": w["b"], "g": w["g"], "T": w["T"], "gamma": w["gamma"], "n_local": w["n_local"], "eta": w["eta"],
               "rho": w["rho"], "pool": args.pool, "kv": f"paged{w['paged']}" if w["paged"] else "contiguous",
@@ -509,6 +633,21 @@ def main():
                        else "eager launches"),
             "clocks": r["clk"],
         }
+        if r["s1_roof"] is not None:
+            line["stage1_roofline"] = r["s1_roof"]
+        line.update(r["extra"])
+        if world > 1:
+            mg = {"rank_ms_per_step": r["rank_ms"], "max_over_ranks_ms": max(r["rank_ms"]),
+                  "min_over_ranks_ms": min(r["rank_ms"])}
+            if r["gather_ms"] is not None:
+                recv = r["o_bytes"] * (world - 1) / world
+                mg.update(o_allgather_ms=r["gather_ms"], o_allgather_recv_bytes_per_rank=recv,
+                          o_allgather_gbs=recv / (r["gather_ms"] * 1e-3) / 1e9,
+                          o_allgather="one in-place all_gather_into_tensor into the rank-major full O "
+                                      "(parallel.HeadShardedOutput), exposed after the prefill")
+            if r["n1_ms"] is not None:
+                mg["same_layer_on_1_gpu_ms"] = r["n1_ms"]
+            line["multi_gpu"] = mg
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(line))

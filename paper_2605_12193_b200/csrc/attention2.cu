@@ -485,6 +485,11 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
           for (int e = 0; e < 32; ++e) {
             const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
             float2 pr;
+#ifdef BFLA_WHATIF_NOEXP
+            if (true) {  // timing what-if (A/B builds only): no exponential at all
+              pr = x;
+            } else
+#endif
             if ((POLY >> (e % 8)) & 1) {  // POLY: bit mask over e mod 8 of the pairs on the FMA pipe
               pr = exp2_poly2(x);
             } else {
@@ -522,6 +527,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
           // warpgroups 224 registers); row max first, then the lazy rule, then exponentials.  P of
           // the first tile goes to TMEM while the second tile's exponentials run.
           float v[128];
+#ifdef BFLA_WHATIF_NOLOAD  // timing what-if (A/B builds only): S never read from TMEM
+#pragma unroll
+          for (int c = 0; c < 128; ++c) v[c] = l_run * 1e-30f + (float)(c & 15);
+#else
           tmem_ld32(tS, v);
           tmem_ld32(tS + 32, v + 32);
           if (two) {
@@ -529,6 +538,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
             tmem_ld32(tS + 96, v + 96);
           }
           tmem_wait_ld();
+#endif
           if (lg == 0) TRACE(3 + q, 16);
           if (PP && BFLA_PINGPONG == 2) named_bar_sync(3 + q, 256);  // my turn (max + exponentials)
           if (la < BN - 1) {

@@ -83,6 +83,9 @@ __device__ __forceinline__ Item decode_item(const Geom& g, int idx, int NC) {
 
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+#ifdef BFLA_WHATIF_NOSTORE  // timing what-if (A/B builds only): P never written to TMEM
+  if (r[0] != 0x12345u) return;
+#endif
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),

@@ -49,6 +49,30 @@ def gather_heads(o_shard: torch.Tensor, world: int, group=None) -> torch.Tensor:
     return torch.cat(parts, dim=1)
 
 
+class HeadShardedOutput:
+    """The layer's O in rank-major storage [world][B][Hq/world][N][d].
+
+    Rank r's query heads [r*Hq/world, (r+1)*Hq/world) are ONE contiguous chunk (`local`, [B, Hq/world,
+    N, d]), so the prefill kernel writes its shard straight into the full buffer and a single in-place
+    all_gather_into_tensor assembles the layer: no staging buffer, no torch.cat, no copy.  `full` is
+    the [B, Hq, N, d] view of the same storage (plain for B = 1; for B > 1 heads of different ranks are
+    a further world-stride apart, so `full` is the 5-D [B, world, Hq/world, N, d] view)."""
+
+    def __init__(self, B: int, Hq: int, N: int, d: int, world: int, rank: int, device, dtype=None):
+        if Hq % world:
+            raise ValueError(f"h_q={Hq} is not divisible by world={world}")
+        self.world, self.rank = world, rank
+        self.store = torch.empty(world, B, Hq // world, N, d, dtype=dtype or torch.bfloat16, device=device)
+        self.local = self.store[rank]
+        perm = self.store.permute(1, 0, 2, 3, 4)
+        self.full = perm.reshape(B, Hq, N, d) if B == 1 else perm
+
+    def gather(self, group=None, async_op: bool = False):
+        """In-place all-gather of every rank's chunk (NCCL on GPUs, gloo in the CPU tests)."""
+        return dist.all_gather_into_tensor(self.store.view(-1), self.local.reshape(-1), group=group,
+                                           async_op=async_op)
+
+
 def request_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     """Request (batch) slice for request-level sharding: requests are fully independent."""
     per = -(-batch // world)

@@ -171,3 +171,61 @@ def test_gather_mask_lists_multi_request(tmp_path):
     want_l = (np.arange(B)[:, None, None] * 1000 + np.arange(H)[None, :, None] * 100 + np.arange(C)).reshape(B, -1)
     want_c = np.arange(B)[:, None, None] * 1000 + np.arange(H)[None, :, None] * 100 + np.arange(Tq)
     assert np.array_equal(gl, want_l) and np.array_equal(gc, want_c)
+
+
+def _inplace_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import workloads
+    from paper_2605_12193_b200 import parallel
+
+    prob = workloads.gaussian(6, 1, 8, 4, 384, 384, 128, sigma=0.8)
+    q, k, v, h0 = parallel.shard_views(prob.q, prob.k, prob.v, rank, world)
+    f = lambda t: t[0].float().numpy()
+    res = oracle.mask_pipeline(f(q), f(k), b=128, g=64, T=64, gamma=0.95, eta=4, rho=0.3, seed=9, head_offset=h0)
+    O, _ = oracle.masked_attention(f(q), f(k), f(v), 128 ** -0.5, res["labels"], 64)
+    out = parallel.HeadShardedOutput(1, 8, 384, 128, world, rank, "cpu", dtype=torch.float64)
+    assert out.full.data_ptr() == out.store.data_ptr() and out.full.shape == (1, 8, 384, 128)
+    out.local.copy_(torch.from_numpy(O)[None])  # what the prefill kernel writes in place on a GPU
+    ptr = out.store.data_ptr()
+    out.gather()
+    assert out.store.data_ptr() == ptr  # in place: no new buffer
+    if rank == 0:
+        np.save(os.path.join(out_dir, "o_inplace.npy"), out.full[0].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_head_sharded_output_inplace_gather(tmp_path, orc):
+    """The bench's N>1 exchange (parallel.HeadShardedOutput): each rank's head shard is a contiguous
+    chunk of the full rank-major O, written in place, and ONE in-place all_gather_into_tensor yields the
+    unsharded layer output (world 2, gloo); no staging buffer, no concatenation."""
+    world = 2
+    mp.spawn(_inplace_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    import workloads
+
+    prob = workloads.gaussian(6, 1, 8, 4, 384, 384, 128, sigma=0.8)
+    f = lambda t: t[0].float().numpy()
+    full = orc.mask_pipeline(f(prob.q), f(prob.k), b=128, g=64, T=64, gamma=0.95, eta=4, rho=0.3, seed=9)
+    O, _ = orc.masked_attention(f(prob.q), f(prob.k), f(prob.v), 128 ** -0.5, full["labels"], 64)
+    assert np.array_equal(np.load(tmp_path / "o_inplace.npy"), O)
+
+
+def test_bench_self_launch_command():
+    """bench.py --gpus N without torchrun re-launches itself under torch.distributed.run with one rank
+    per GPU and a 127.0.0.1 rendezvous (checked on the command it builds, with a stub launcher)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, subprocess; sys.argv=['bench.py','--gpus','4','--steps','2'];"
+            "calls=[]; subprocess.call=lambda c: calls.append(c) or 0;"
+            "import runpy\ntry:\n runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit as e:\n"
+            " assert e.code == 0\nc=calls[0]; print(c)\n"
+            "assert c[1:3]==['-m','torch.distributed.run'] and '--nproc-per-node=4' in c and "
+            "'--master-addr=127.0.0.1' in c and c[-4:]==['--gpus','4','--steps','2']")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
