@@ -15,6 +15,19 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
   return d;
 }
 
+// max of 64 row values: four independent 3-input chains (FMNMX3), then their max
+__device__ __forceinline__ float row_max64(const float* v) {
+  float mc[4];
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    float a = max3f(v[16 * k4], v[16 * k4 + 1], v[16 * k4 + 2]);
+#pragma unroll
+    for (int c = 3; c < 15; c += 2) a = max3f(a, v[16 * k4 + c], v[16 * k4 + c + 1]);
+    mc[k4] = fmaxf(a, v[16 * k4 + 15]);
+  }
+  return fmaxf(max3f(mc[0], mc[1], mc[2]), mc[3]);
+}
+
 // 2^x for a pair on the FMA pipe: x = j + f with j = rint(x) (magic-number rounding, f in [-1/2, 1/2]),
 // 2^f by a degree-3 polynomial (relative error 7.7e-5), 2^j folded into the exponent bits.
 // x is clamped at -126 so the exponent field cannot wrap: masked entries (-inf) give a denormal ~2^-126.
@@ -92,6 +105,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+#ifdef BFLA_WHATIF_NOSTORE
+  if (r[0] != 0x12345u) return;
+#endif
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 
 // D[tmem] (+)= A[tmem] * B[smem]  (kind::f16, A from tensor memory: row = lane, 2 bf16 per column),

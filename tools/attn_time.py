@@ -20,6 +20,8 @@ ap.add_argument("--variant", default="")
 ap.add_argument("--workload", default="llama8b-32k")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--dense", type=int, default=1)
+ap.add_argument("--save", default="", help="save a sample of O (every 16th query row) to this .pt file")
+ap.add_argument("--compare", default="", help="compare the O sample with this .pt file (max / mean abs diff)")
 a = ap.parse_args()
 bf._lib.use_variant(a.variant)
 w = WORKLOADS[a.workload]
@@ -55,11 +57,19 @@ def timed(fn, n):
 
 sp = timed(lambda: bf.bfla_sparse_prefill(P, cfg, m, ws), a.reps)
 dig = hashlib.sha1(o.view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16]
+sample = o[0, :, ::16].float().cpu()
+if a.save:
+    torch.save(sample, a.save)
+cmp = None
+if a.compare and os.path.exists(a.compare):
+    ref = torch.load(a.compare)
+    dd = (sample - ref).abs()
+    cmp = dict(max_abs=float(dd.max()), mean_abs=float(dd.mean()))
 st_ = m.stats_dict()
 kept = st_["kept_tiles"]
 fl = 4 * w["d"] * (w["Hq"] // w["Hkv"]) * 64 * 64 * kept
 out = dict(variant=a.variant or "product", workload=a.workload, sparse_ms=sp, sparse_tflops=fl / sp / 1e9,
-           kappa=kept / st_["causal_tiles"], o_digest=dig)
+           kappa=kept / st_["causal_tiles"], o_digest=dig, vs_saved=cmp)
 if a.dense:
     Pd = bf.make_problem(q, k, v, o) if not w["paged"] else P
     wsd = bf.alloc_workspace(Pd, None)
