@@ -432,8 +432,12 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
   static const bool no_dyn = experiment_knob("BFLA_DYN_SCHED", 1) == 0;  // A/B builds: static round-robin
   if (no_dyn) sched = nullptr;
   if (sched) cudaMemsetAsync(sched, 0, sizeof(int32_t), st);
+#ifndef BFLA_ATTN3
+#define BFLA_ATTN3 0
+#endif
   int e = (g.D == 128 && !v1)
-              ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
+              ? (BFLA_ATTN3 ? launch_attention3(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
+                            : launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched))
               : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched);
   if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
   return cuda_check("attention launch");

@@ -59,7 +59,6 @@ constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
 // lazy-rescale headroom (log2 units): p = 2^(x - m_run) <= 2^24; O <= 2^24 * N_kv * |V| << fp32 max
 constexpr float kLazy = 24.0f;
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int NQT, bool PAGED = false, int SPLIT = 1>
 struct Cfg2 {
@@ -255,8 +254,12 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
 #define BFLA_REG_PROD2 56
 #define BFLA_REG_SMX2 112
 #endif
+#ifndef BFLA_SPLIT_SETMAXNREG
+#define BFLA_SPLIT_SETMAXNREG 1
+#endif
     if (NQT == 2 && SMX == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD) : "memory");
-    if (NQT == 2 && SMX == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD2) : "memory");
+    if (NQT == 2 && SMX == 2 && BFLA_SPLIT_SETMAXNREG)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD2) : "memory");
   if (warp == 0) {
     // ================================ TMA producer (K) ================================
     {
@@ -441,7 +444,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
     // other half's S columns too (max only), so both compute the same max, lazy rule and m_run with no
     // exchange; a named barrier per step orders every S read of the tile before any P store over it.
     // Row sums are kept per half and added (half 0 + half 1) in the epilogue through shared memory.
-    if (NQT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BFLA_REG_SMX2) : "memory");
+    if (NQT == 2 && BFLA_SPLIT_SETMAXNREG)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BFLA_REG_SMX2) : "memory");
     const int sw = warp - 4;
     const int q = sw >> 3, hh = (sw >> 2) & 1;
     const int lg = warp & 3;         // TMEM lane group of this warp

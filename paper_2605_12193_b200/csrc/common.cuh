@@ -2,6 +2,7 @@
 // (mbarrier, TMA, tcgen05/TMEM).  Product path only: the CPU oracle shares nothing with this.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>

@@ -59,5 +59,9 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
 int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
                       const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
                       int* sched = nullptr);
+// head_dim 128: one Q tile per item, S double-buffered in TMEM, column-split softmax (attention3.cu)
+int launch_attention3(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
+                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
+                      int* sched = nullptr);
 
 }  // namespace bfla
