@@ -193,6 +193,85 @@ def layer_timing(name, dev, reps=3, dense_reps=2, tile=64):
     return out
 
 
+VARLEN_MIX = [(8192, 32768), (12000, 12000), (5000, 5000), (3000, 20000)]  # (n_q_r, n_kv_r), all ragged / chunked
+
+
+def varlen_timing(dev, reps=3):
+    """§8 f1 performance point: a vLLM-style mixed batch on the Llama-3.1-8B layer shape (32/8 heads,
+    d = 128) — a chunk of a 32K prompt (N_c = 24576), two whole ragged prompts and a short chunk over a
+    20K context — in ONE call per stage (device length table).  Stage 1 runs on the tensor cores
+    (full groups) + the canonical partial-group fixup; the dense comparator is the same varlen batch
+    through bfla_prefill(config = NULL).  Each request's inputs are generated at its own lengths
+    (workloads.structured) and padded into [B, H, max, d] buffers."""
+    import torch
+
+    import paper_2605_12193_b200 as bf
+    import workloads
+
+    w = WORKLOADS["llama8b-32k"]
+    B = len(VARLEN_MIX)
+    nq_max, nkv_max = max(a for a, _ in VARLEN_MIX), max(b_ for _, b_ in VARLEN_MIX)
+    q = torch.zeros(B, w["Hq"], nq_max, w["d"], dtype=torch.bfloat16, device=dev)
+    k = torch.zeros(B, w["Hkv"], nkv_max, w["d"], dtype=torch.bfloat16, device=dev)
+    v = torch.zeros_like(k)
+    for r, (nq, nkv) in enumerate(VARLEN_MIX):
+        pr = workloads.structured(505 + r, 1, w["Hq"], w["Hkv"], nq, nkv, w["d"], block=w["b"], theta=w["theta"],
+                                  device=dev)
+        q[r, :, :nq], k[r, :, :nkv], v[r, :, :nkv] = pr.q[0], pr.k[0], pr.v[0]
+        del pr
+    sl = torch.tensor(VARLEN_MIX, dtype=torch.int32, device=dev)
+    o = torch.zeros_like(q)
+    cfg = bf.Config(b=w["b"], g=w["g"], T=64, gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"])
+    P = bf.make_problem(q, k, v, o, seqlens=sl)
+    ws = bf.alloc_workspace(P, cfg)
+    m = bf.alloc_mask(P, cfg)
+    st = torch.cuda.current_stream()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps + 2)]
+    for e in evs:
+        e[0].record(st)
+        bf.bfla_block_mask(P, cfg, m, ws)
+        e[1].record(st)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        e[2].record(st)
+        bf.bfla_sparse_prefill(P, cfg, m, ws)
+        e[3].record(st)
+    torch.cuda.synchronize()
+    evs = evs[2:]
+    med = lambda a, b_: statistics.median(e[a].elapsed_time(e[b_]) for e in evs)
+    s1, s2, at, tot = med(0, 1), med(1, 2), med(2, 3), med(0, 3)
+    wsd = bf.alloc_workspace(P, None)
+    bf.bfla_prefill(P, None, None, wsd)
+    de = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    de[0].record(st)
+    for _ in range(2):
+        bf.bfla_prefill(P, None, None, wsd)
+    de[1].record(st)
+    torch.cuda.synchronize()
+    dense_ms = de[0].elapsed_time(de[1]) / 2
+    stats = m.stats_dict()
+    peaks = load_peaks()
+    kept = stats["kept_tiles"]
+    achieved = 4.0 * w["d"] * (w["Hq"] // w["Hkv"]) * 64 * 64 * kept / (at * 1e-3) / 1e12
+    # Stage-1 algorithmic work summed over the requests (causal block pairs of each, Eq. 30)
+    G, L = w["b"] // w["g"], lambda n: -(-n // w["b"])
+    fl = nb = 0.0
+    for nq, nkv in VARLEN_MIX:
+        nc = nkv - nq
+        pairs = sum(min(L(nkv), (nc + (i + 1) * w["b"] - 1) // w["b"] + 1) for i in range(L(nq)))
+        fl += 2.0 * w["Hq"] * pairs * G * G * w["g"] * w["d"]
+        nb += 2.0 * (w["Hq"] * nq + w["Hkv"] * nkv) * w["d"]
+    t_bound = max(nb / (peaks["hbm"] * 1e9), fl / (peaks["bf16"] * 1e12)) * 1e3
+    out = {"workload": "llama8b-varlen-mix", "requests": VARLEN_MIX, "ms_per_call": tot,
+           "stages_ms": {"stage1_scores_select": s1, "stage2_expand_rescue": s2, "sparse_prefill": at},
+           "kappa": kept / max(1, stats["causal_tiles"]), "dense_ms": dense_ms, "speedup_vs_dense": dense_ms / tot,
+           "sparse_roofline_frac": achieved / peaks["bf16"], "stage1_frac_of_bound_time": t_bound / s1,
+           "rows_flagged": stats["rows_flagged"],
+           "timing": f"CUDA events, median of {reps} eager calls after 2 warm-ups; dense mean of 2"}
+    del q, k, v, o, ws, m, wsd
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, w, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -459,6 +538,8 @@ def run_ours(args, w, rank, world, local_rank):
     extra = {}
     if world == 1 and args.extra_128k and w["N"] < 131072 and not w["paged"]:
         extra["llama8b_128k"] = layer_timing("llama8b-128k", dev)
+    if world == 1 and args.extra_128k and not w["paged"]:
+        extra["varlen_mix"] = varlen_timing(dev)
     n1_ms = None
     if heads:  # the same (unsharded) layer on one GPU, for the driver's strong-scaling efficiency
         if rank == 0:

@@ -41,7 +41,7 @@ typedef enum {
                                       (Eq. 6), T does not divide b (Eq. 19), gamma not in (0,1] (Eq. 17),
                                       keep_ratio not in (0,1], rho not in [0,1] (Eq. 25), eta < 0, n_local < 0,
                                       n_sink < 0, NULL required pointer                                       */
-    BFLA_ERR_UNSUPPORTED = 2,      /* valid but not built: head_dim not in {128, 256}, T not in {64, 128}, G = b/g > 8,
+    BFLA_ERR_UNSUPPORTED = 2,      /* valid but not built: head_dim not in {128, 256}, T not in {64, 128},
                                       FLATTEN with non-contiguous tokens, page_size not in {16, 32, 64}     */
     BFLA_ERR_MISALIGNED = 3,       /* TMA rules: base address % 16 B, strides % 16 B                         */
     BFLA_ERR_WORKSPACE = 4,        /* ws_bytes < bfla_workspace_size(...) or ws == NULL                       */
@@ -106,7 +106,8 @@ typedef struct {
    b=256, g=64, gamma=0.99, n_local=8, rho=0, eta=16; T=64 and n_sink=1 are our readings (R10, R12). */
 typedef struct {
     int32_t block_b;    /* b: coarse block size (Eq. 4), power of two                                   */
-    int32_t group_g;    /* g: flattening group (Eq. 6), power of two dividing b; G = b/g <= 8 built    */
+    int32_t group_g;    /* g: flattening group (Eq. 6), power of two dividing b; any G = b/g (tensor-core
+                           scores for G <= 16, e.g. b=1024 g=64; canonical SIMT above, e.g. g=1) */
     int32_t tile_t;     /* T: attention tile (Eq. 19), divides b; 64 and 128 built                      */
     int32_t pool;       /* BFLA_POOL_*                                                                  */
     int32_t select;     /* BFLA_SELECT_*                                                                */

@@ -180,8 +180,6 @@ static bfla_status make_geom(const bfla_problem* P, const bfla_config* cfg, Geom
     if (cfg->eta < 0 || cfg->n_local < 0 || cfg->n_sink < 0)
       return fail(BFLA_ERR_INVALID_ARGUMENT, "eta, n_local, n_sink must be >= 0");
     if (T != 64 && T != 128) return fail(BFLA_ERR_UNSUPPORTED, "tile_t %d not built (64, 128)", T);
-    if (cfg->pool == BFLA_POOL_FLATTEN && b / gg > 8)
-      return fail(BFLA_ERR_UNSUPPORTED, "G = b/g = %d > 8 not built for FLATTEN", b / gg);
     if (cfg->mask_groups != BFLA_MASK_PER_KV_HEAD && cfg->mask_groups != BFLA_MASK_PER_Q_HEAD)
       return fail(BFLA_ERR_INVALID_ARGUMENT, "mask_groups");
     if (cfg->certify_slack != 0.f && !(cfg->certify_slack >= 1.f))
@@ -292,8 +290,10 @@ static float certify_tau(const Geom& g, float slack) {
 
 static bool tc_eligible(const Geom& g, const bfla_problem* P, const bfla_config* cfg, const bfla_mask* mask) {
   if (cfg->pool != BFLA_POOL_FLATTEN || cfg->scores_path != BFLA_SCORES_AUTO || mask->kept_mass) return false;
-  if (g.lens) return false;  // varlen: a request's partial group would read padding (canonical path zero-fills)
-  if (g.Nq % g.g || g.Nkv % g.g) return false;       // a TMA group row must not straddle the tail
+  // ragged tails / varlen requests: the tensor maps cover the buffer's full groups and the scores
+  // kernel uses full groups only; k_s1_ragged_fixup rewrites the partial groups' block scores
+  if (g.Nq < g.g || g.Nkv < g.g) return false;  // no full group at all: the canonical path
+  if (g.G > 16) return false;  // the score epilogue max-pools G <= 16 groups per block (g = 1: canonical)
   if (g.qs2 != g.D) return false;                    // group rows = contiguous token runs
   if (!g.paged && g.kvs2 != g.D) return false;
   if ((g.qs1 % 8) || (g.qs0 % 8) || (!g.paged && ((g.kvs1 % 8) || (g.kvs0 % 8)))) return false;
@@ -327,6 +327,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     CUtensorMap tmA, tmB;
     bfla_status s;
     {
+      // floor(N / g) group rows: a partial last group is never read (rows past it are zero-filled)
       const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nq / g.g), (uint64_t)g.Hq, (uint64_t)g.B};
       const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)g.qs1 * 2, (uint64_t)g.qs0 * 2};
       const uint32_t box[4] = {64, 128, 1, 1};
@@ -364,6 +365,11 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     }
     float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
     const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart);
+    const bool ragged = g.lens || (g.Nq % g.g) || (g.Nkv % g.g);
+    if (!tc_err && ragged && launch_ragged_fixup(gk, P->q, kc, S, st)) {
+      if (ss) cudaStreamWaitEvent(st, ss->join, 0);
+      return fail(BFLA_ERR_CUDA, "ragged fixup launch failed");
+    }
     cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);  // joined even on failure: never leave a fork open
     if (tc_err) return fail(BFLA_ERR_CUDA, "tc scores launch failed (%d)", tc_err);

@@ -30,6 +30,8 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
                      cudaStream_t st, float* part = nullptr);
 int tc_splits(const Geom& g);
 size_t tc_part_bytes(const Geom& g);
+// canonical rewrite of the block scores of partial groups (ragged n mod g != 0, varlen requests)
+int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st);
 // with_q = false: key-group norms only (the scores kernel wrote the query norms)
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st,
                         bool with_q = true);

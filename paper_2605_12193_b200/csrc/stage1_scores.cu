@@ -242,6 +242,58 @@ __global__ void __launch_bounds__(256) k_s1_mean_scores(Geom g, const float* __r
   S[idx] = acc;
 }
 
+// Generic canonical FLATTEN scores for any G = b/g (used for G > 8: the paper's b = 1024, g = 64 row
+// of Tab.mask, and g = 1, where Eq. 10 is the exact block max of QK^T).  CTA per (r, p, i, j)
+// (non-causal pairs exit, Eq. 11-13); thread = group pair (u, v), running the canonical order of
+// DESIGN.md §4 item 2 literally: acc = 0; for t: { d = 0; for c: d = fma(q_t[c], k_t[c], d); acc += d }.
+// Padding tokens are skipped (their token dot is an exact +0, and acc + 0 = acc); padding-only groups
+// never take the max (R3).  A CTA max-reduces its pairs (Eq. 10, exact).
+template <int D>
+__global__ void __launch_bounds__(256) k_s1_flatten_scores_any(Geom g, const __nv_bfloat16* __restrict__ q,
+                                                               const __nv_bfloat16* __restrict__ k,
+                                                               const int32_t* __restrict__ pt, float* __restrict__ S) {
+  __shared__ float wmax[8];
+  const int j = blockIdx.x, i = blockIdx.y, rp = blockIdx.z;
+  const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
+  const Req R = req_of(g, r);
+  if (i >= R.Lq || j >= R.Lkv) return;
+  long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+  if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+  if ((long long)j * g.b > e_i) return;
+  const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
+  float best = -INFINITY;
+  for (int uv = threadIdx.x; uv < g.G * g.G; uv += 256) {
+    const int u = uv / g.G, v = uv % g.G;
+    const int tq0 = i * g.b + u * g.g, tk0 = j * g.b + v * g.g;
+    if (tq0 >= R.Nq || tk0 >= R.Nkv) continue;  // padding-only group (R3)
+    float acc = 0.0f;
+    for (int t = 0; t < g.g; ++t) {
+      if (tq0 + t >= R.Nq || tk0 + t >= R.Nkv) break;  // the rest of the group is padding
+      const __nv_bfloat16* x = qb + (long long)(tq0 + t) * g.qs2;
+      const __nv_bfloat16* y = k_token(g, k, pt, r, h, tk0 + t);
+      float d = 0.0f;
+#pragma unroll 4
+      for (int cc = 0; cc < D; cc += 8) {
+        float xf[8], yf[8];
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(x + cc)), xf);
+        bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(y + cc)), yf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d = __fmaf_rn(xf[e], yf[e], d);
+      }
+      acc = __fadd_rn(acc, d);
+    }
+    best = fmaxf(best, acc);
+  }
+  for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = wmax[0];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, wmax[w]);
+    S[(((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j] = m;
+  }
+}
+
 }  // namespace
 
 int launch_flatten_scores(const Geom& g, const void* q, const void* k, const int32_t* pt, float* S,
@@ -259,7 +311,12 @@ int launch_flatten_scores(const Geom& g, const void* q, const void* k, const int
     case 2: go(k_s1_flatten_scores<2>); break;
     case 4: go(k_s1_flatten_scores<4>); break;
     case 8: go(k_s1_flatten_scores<8>); break;
-    default: return -1;
+    default: {  // any other G (> 8): one CTA per block pair
+      if (g.Lq > 65535 || (long long)g.B * g.Hq > 65535) return -1;
+      const dim3 ga(g.Lkv, g.Lq, g.B * g.Hq);
+      if (g.D == 128) k_s1_flatten_scores_any<128><<<ga, 256, 0, st>>>(g, qq, kk, pt, S);
+      else k_s1_flatten_scores_any<256><<<ga, 256, 0, st>>>(g, qq, kk, pt, S);
+    }
   }
   count_launch();
   return 0;

@@ -238,11 +238,16 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 #pragma unroll
       for (int e = 0; e < 32; ++e)
         if (e == lane) sq = v[e];
-      float mx = sqrtf(fmaxf(sq, 0.f));
+      // full groups only: a partial group's row holds padding (zero-filled or another request's
+      // bytes); its scores come from k_s1_ragged_fixup in the canonical order (exact, no bound needed)
+      const bool ufull = (long long)(grow + 1) * g.g <= R.Nq;
+      float mx = ufull ? sqrtf(fmaxf(sq, 0.f)) : 0.f;
       for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
     }
-    const bool uvalid = (long long)grow * g.g < R.Nq;  // padding-only groups never take the max (R3)
+    // padding-only groups never take the max (R3); partial groups (ragged N, varlen) are left to the
+    // canonical fixup, which rewrites every block score they take part in
+    const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;
     long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
         const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
         float mx = -INFINITY;
         for (int vv = 0; vv < g.G; ++vv)
-          if ((long long)(gcol + vv) * g.g < R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);
+          if ((long long)(gcol + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);  // full key groups
         if (!uvalid) mx = -INFINITY;
         for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const int jb = gcol / g.G;
@@ -298,11 +303,11 @@ __global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict_
   if (qn != nullptr && nt == 0 && cg == 0) {
     float sq = 0.f;
     for (int sp = 0; sp < splits; ++sp) sq += qpart[(((long long)rp * n_mt + mt) * splits + sp) * TM + row];
-    float mx = sqrtf(fmaxf(sq, 0.f));
+    float mx = (long long)(grow + 1) * g.g <= R.Nq ? sqrtf(fmaxf(sq, 0.f)) : 0.f;  // full groups only
     for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
   }
-  const bool uvalid = (long long)grow * g.g < R.Nq;
+  const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;  // full groups (partial: k_s1_ragged_fixup)
   long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
   if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
   float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
@@ -310,20 +315,23 @@ __global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict_
   const int c_end = min(nlive, (cg + 1) * kRedCols);
   for (int jb0 = cg * kRedCols; jb0 < c_end; jb0 += g.G) {
     const int gcol = nt * TN + jb0;
-    float a[8];
-#pragma unroll
-    for (int vv = 0; vv < 8; ++vv) a[vv] = vv < g.G ? __ldg(pp + (long long)(jb0 + vv) * TM) : 0.f;
-    for (int sp = 1; sp < splits; ++sp) {
-      float b[8];
-#pragma unroll
-      for (int vv = 0; vv < 8; ++vv) b[vv] = vv < g.G ? __ldg(pp + ((long long)sp * TN + jb0 + vv) * TM) : 0.f;
-#pragma unroll
-      for (int vv = 0; vv < 8; ++vv) a[vv] += b[vv];
-    }
     float mx = -INFINITY;
+    for (int v0 = 0; v0 < g.G; v0 += 8) {  // G <= 16: one or two chunks of 8 key groups
+      float a[8];
 #pragma unroll
-    for (int vv = 0; vv < 8; ++vv)
-      if (vv < g.G && (long long)(gcol + vv) * g.g < R.Nkv) mx = fmaxf(mx, a[vv]);
+      for (int vv = 0; vv < 8; ++vv) a[vv] = v0 + vv < g.G ? __ldg(pp + (long long)(jb0 + v0 + vv) * TM) : 0.f;
+      for (int sp = 1; sp < splits; ++sp) {
+        float b[8];
+#pragma unroll
+        for (int vv = 0; vv < 8; ++vv)
+          b[vv] = v0 + vv < g.G ? __ldg(pp + ((long long)sp * TN + jb0 + v0 + vv) * TM) : 0.f;
+#pragma unroll
+        for (int vv = 0; vv < 8; ++vv) a[vv] += b[vv];
+      }
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv)
+        if (v0 + vv < g.G && (long long)(gcol + v0 + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, a[vv]);
+    }
     if (!uvalid) mx = -INFINITY;
     for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int jb = gcol / g.G;
@@ -351,6 +359,71 @@ __device__ __forceinline__ void bf16x8_f32(const uint4& u, float* f) {
   }
 }
 
+// Canonical S[r, p, i, j] by one CTA (all threads call it): the block pair's G x G group dots as
+// G*G*g token-pair chains (C-long fp32 FMA chains, channel ascending), four per thread side by side
+// straight from global memory (16-byte loads, L1/L2-resident rows); the token dots land in smem and
+// G*G threads add them in ascending token order — the oracle's order exactly; Eq. 10 max over pairs.
+// tokdot: [G*G*g + G*G] floats of shared memory.
+template <int D>
+__device__ void canon_block_score(const Geom& g, const Req& R, const __nv_bfloat16* __restrict__ q,
+                                  const __nv_bfloat16* __restrict__ k, int r, int p, int i, int j,
+                                  float* tokdot, float* __restrict__ S) {
+  const int G = g.G, gg = g.g, nch = G * G * gg;
+  const int h = p / g.m;
+  float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
+  const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
+  const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
+  // chains c = (u, v, t), t fastest: four per thread per pass
+  for (int c0 = threadIdx.x * 4; c0 < nch; c0 += kRecThreads * 4) {
+    const __nv_bfloat16* xs[4];
+    const __nv_bfloat16* ys[4];
+    bool ok[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = c0 + e;
+      const int t = c % gg, uv = c / gg, u = uv / G, v = uv % G;
+      const int tq = i * g.b + u * gg + t, tk = j * g.b + v * gg + t;
+      ok[e] = c < nch && tq < R.Nq && tk < R.Nkv;  // padding tokens are exact zeros: dot 0
+      xs[e] = qb + (long long)(ok[e] ? tq : 0) * g.qs2;
+      ys[e] = kb + (long long)(ok[e] ? tk : 0) * g.kvs2;
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+    for (int cc = 0; cc < D; cc += 8) {
+      float xf[4][8], yf[4][8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(xs[e] + cc)), xf[e]);
+        bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(ys[e] + cc)), yf[e]);
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(xf[e][x], yf[e][x], acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (c0 + e < nch) tokdot[c0 + e] = ok[e] ? acc[e] : 0.0f;
+  }
+  __syncthreads();
+  float* pairtot = tokdot + nch;
+  if (threadIdx.x < G * G) {
+    // thread (u, v): the g token dots added in ascending t (the oracle's order)
+    const int uv = threadIdx.x, u = uv / G, v = uv % G;
+    float a = 0.0f;
+    for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[uv * gg + t]);
+    const bool valid = i * g.b + u * gg < R.Nq && j * g.b + v * gg < R.Nkv;  // padding-only groups (R3)
+    pairtot[uv] = valid ? a : -INFINITY;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = -INFINITY;  // Eq. 10: max over the group pairs (exact, order-free)
+    for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
+    srow[j] = mx;
+  }
+  __syncthreads();  // tokdot is reused by the caller's next unit
+}
+
 template <int D>
 __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const __nv_bfloat16* __restrict__ q,
                                                                    const __nv_bfloat16* __restrict__ k,
@@ -361,7 +434,6 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
                                                                    float* __restrict__ S) {
   extern __shared__ float tokdot[];  // [G*G][g] token dots of the current unit
   (void)n_flagged;
-  const int G = g.G, gg = g.g, nch = G * G * gg;
   const int nunits = *n_units;
   for (int uidx = blockIdx.x; uidx < nunits; uidx += gridDim.x) {
     const int unit = ulist[uidx];  // fidx * Lkv + j (k_s1_select: the row's recompute band)
@@ -369,64 +441,46 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
     const int fidx = unit / g.Lkv;
     const int row = flagged[fidx];  // (r * Hq + p) * Lq + i
     const int i = row % g.Lq, p = (row / g.Lq) % g.Hq, r = row / (g.Lq * g.Hq);
-    const int h = p / g.m;
     const Req R = req_of(g, r);
     long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
     if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
     if ((long long)j * g.b > e_i || j >= R.Lkv) continue;  // non-causal (uniform over the CTA)
-    float* srow = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv;
-    const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
-    const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
-    // chains c = (u, v, t), t fastest: four per thread per pass
-    for (int c0 = threadIdx.x * 4; c0 < nch; c0 += kRecThreads * 4) {
-      const __nv_bfloat16* xs[4];
-      const __nv_bfloat16* ys[4];
-      bool ok[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = c0 + e;
-        const int t = c % gg, uv = c / gg, u = uv / G, v = uv % G;
-        const int tq = i * g.b + u * gg + t, tk = j * g.b + v * gg + t;
-        ok[e] = c < nch && tq < R.Nq && tk < R.Nkv;  // padding tokens are exact zeros: dot 0
-        xs[e] = qb + (long long)(ok[e] ? tq : 0) * g.qs2;
-        ys[e] = kb + (long long)(ok[e] ? tk : 0) * g.kvs2;
-      }
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-      for (int cc = 0; cc < D; cc += 8) {
-        float xf[4][8], yf[4][8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(xs[e] + cc)), xf[e]);
-          bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(ys[e] + cc)), yf[e]);
-        }
-#pragma unroll
-        for (int x = 0; x < 8; ++x)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] = __fmaf_rn(xf[e][x], yf[e][x], acc[e]);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (c0 + e < nch) tokdot[c0 + e] = ok[e] ? acc[e] : 0.0f;
-    }
-    __syncthreads();
-    float* pairtot = tokdot + nch;
-    if (threadIdx.x < G * G) {
-      // thread (u, v): the g token dots added in ascending t (the oracle's order)
-      const int uv = threadIdx.x, u = uv / G, v = uv % G;
-      float a = 0.0f;
-      for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[uv * gg + t]);
-      const bool valid = i * g.b + u * gg < R.Nq && j * g.b + v * gg < R.Nkv;  // padding-only groups (R3)
-      pairtot[uv] = valid ? a : -INFINITY;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float mx = -INFINITY;  // Eq. 10: max over the group pairs (exact, order-free)
-      for (int uv = 0; uv < G * G; ++uv) mx = fmaxf(mx, pairtot[uv]);
-      srow[j] = mx;
-    }
-    __syncthreads();  // tokdot is reused by the next unit
+    canon_block_score<D>(g, R, q, k, r, p, i, j, tokdot, S);
   }
+}
+
+// Ragged tails and varlen requests on the tensor-core path (§8 f1): the scores kernel covers full
+// groups only (a partial group's TMA row would read padding), so every block score a partial group
+// takes part in — row i = L_q,r - 1 when n_q,r mod g != 0, column j = L_kv,r - 1 when n_kv,r mod g != 0 —
+// is rewritten here in the canonical order.  Exact scores need no certification slack: the selector's
+// bound (tau ||x|| ||y||, norms over the full groups) stays conservative for them.  CTA per
+// (r, p, unit): units [0, L_kv) walk the partial row, [L_kv, L_kv + L_q) the partial column.
+template <int D>
+__global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const __nv_bfloat16* __restrict__ q,
+                                                                 const __nv_bfloat16* __restrict__ k,
+                                                                 float* __restrict__ S) {
+  extern __shared__ float tokdot[];
+  const int per = g.Lkv + g.Lq;
+  const int idx = blockIdx.x % per, rp = blockIdx.x / per;
+  const int p = rp % g.Hq, r = rp / g.Hq;
+  const Req R = req_of(g, r);
+  const bool qrag = R.Nq % g.g != 0, krag = R.Nkv % g.g != 0;
+  int i, j;
+  if (idx < g.Lkv) {
+    if (!qrag) return;
+    i = R.Lq - 1;
+    j = idx;
+  } else {
+    if (!krag) return;
+    i = idx - g.Lkv;
+    j = R.Lkv - 1;
+    if (qrag && i == R.Lq - 1) return;  // the row units cover it
+  }
+  if (i >= R.Lq || j >= R.Lkv) return;
+  long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
+  if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+  if ((long long)j * g.b > e_i) return;  // Eq. 11-13: not causal
+  canon_block_score<D>(g, R, q, k, r, p, i, j, tokdot, S);
 }
 
 // Same units and the same arithmetic order, operands staged in shared memory: the unit's K block and
@@ -622,9 +676,9 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
     for (int idx = threadIdx.x; idx < G * gg; idx += kRecThreads) {
       const int t = idx % gg, u = idx / gg;
       const int qtok = u * gg + t;
-      float acc[8];
+      float acc[16];  // G <= 16 chains side by side
 #pragma unroll
-      for (int v = 0; v < 8; ++v) acc[v] = 0.f;
+      for (int v = 0; v < 16; ++v) acc[v] = 0.f;
       const bool qok = i * b + qtok < R.Nq;
       if (qok) {
         for (int cc = 0; cc < NCH; ++cc) {
@@ -633,7 +687,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma(const __grid_c
             float xf[8];
             bf16x8_f32(elem16(qs, qtok, cc, k16), xf);
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
+            for (int v = 0; v < 16; ++v) {
               if (v >= G) break;
               float yf[8];
               bf16x8_f32(elem16(kbuf, v * gg + t, cc, k16), yf);
@@ -730,7 +784,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma_kc(const __gri
   const int idx = threadIdx.x;
   const bool act = idx < G * gg;
   const int t = act ? idx % gg : 0, u = act ? idx / gg : 0;
-  float acc[8];
+  float acc[16];  // G <= 16
   for (long long sg = s0; sg < s1; ++sg) {
     const long long uidx = sg / NCH;
     const int cc = (int)(sg % NCH);
@@ -756,7 +810,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma_kc(const __gri
     const bool qok = act && i * b + qtok < R.Nq;
     if (cc == 0) {
 #pragma unroll
-      for (int v = 0; v < 8; ++v) acc[v] = 0.f;
+      for (int v = 0; v < 16; ++v) acc[v] = 0.f;
     }
     if (qok) {
       const unsigned char* kbuf = kb[buf];
@@ -769,7 +823,7 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_tma_kc(const __gri
                      xf);
         }
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
+        for (int v = 0; v < 16; ++v) {
           if (v >= G) break;
           const int ktok = v * gg + t, rt = ktok >> 6, row = ktok & 63;
           float yf[8];
@@ -880,6 +934,22 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
   return (int)cudaGetLastError();
 }
 
+int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st) {
+  if (g.G * g.G > kRecThreads) return -1;
+  const long long ctas = (long long)g.B * g.Hq * (g.Lkv + g.Lq);
+  const int smem = (g.G * g.G * g.g + g.G * g.G) * 4;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<(int)ctas, kRecThreads, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),
+                                                static_cast<const __nv_bfloat16*>(k), S);
+  };
+  if (g.D == 128) go(k_s1_ragged_fixup<128>);
+  else if (g.D == 256) go(k_s1_ragged_fixup<256>);
+  else return -1;
+  count_launch();
+  return (int)cudaGetLastError();
+}
+
 void launch_block_norms(const Geom& g, const void* q, const void* k, float* qn, float* kn, cudaStream_t st,
                         bool with_q) {
   const long long ctas = (with_q ? (long long)g.B * g.Hq * g.Lq : 0) + (long long)g.B * g.Hkv * g.Lkv;
@@ -900,7 +970,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
   static const int mode = experiment_knob("BFLA_RECOMPUTE", 0);
   {
     const size_t smem_t = (size_t)3 * g.b * g.D * 2 + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4 + 1024;
-    if (mode == 0 && tmQ && tmK && g.D == 128 && g.G <= 8 && g.b % 64 == 0 && smem_t <= 226 * 1024) {
+    if (mode == 0 && tmQ && tmK && g.D == 128 && g.G <= 16 && g.b % 64 == 0 && smem_t <= 226 * 1024) {
       auto kern = k_s1_recompute_tma<128>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
       kern<<<num_sms, kRecThreads, smem_t, st>>>(*tmQ, *tmK, g, flagged, n_flagged, ulist, n_units, S);
@@ -909,7 +979,7 @@ int launch_recompute_rows(const Geom& g, const void* q, const void* k, const int
     }
     const size_t smem_kc = (size_t)g.b * g.D * 2 + (size_t)2 * g.b * 128 + ((size_t)g.G * g.G * g.g + g.G * g.G) * 4 +
                            1024;
-    if (mode == 0 && tmQ && tmK && g.D == 256 && g.G <= 8 && g.b % 64 == 0 && g.G * g.g <= kRecThreads &&
+    if (mode == 0 && tmQ && tmK && g.D == 256 && g.G <= 16 && g.b % 64 == 0 && g.G * g.g <= kRecThreads &&
         smem_kc <= 226 * 1024) {
       auto kern = k_s1_recompute_tma_kc<256>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_kc);

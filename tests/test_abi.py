@@ -111,7 +111,7 @@ def test_problem_validation(L, mut, status):
 @pytest.mark.parametrize("mut,status", [
     (dict(group_g=48), 1), (dict(block_b=128, tile_t=256), 1), (dict(gamma=0.0), 1), (dict(gamma=1.5), 1),
     (dict(rho=-0.1), 1), (dict(eta=-1), 1), (dict(n_local=-1), 1), (dict(select=1, keep_ratio=0.0), 1),
-    (dict(block_b=256, tile_t=256), 2), (dict(block_b=1024, group_g=64), 2),
+    (dict(block_b=256, tile_t=256), 2), (dict(tile_t=32), 2),  # G = 16 (b=1024, g=64) is built now
 ])
 def test_config_validation(L, mut, status):
     so = L.lib()

@@ -77,6 +77,10 @@ def test_shapes(case):
     ref = oracle_masks(prob, cfg)
     labels = _check_masks(gpu, ref, cfg)
     check_lists(gpu, labels, c["Nq"], c["Nkv"], 64)
+    # ragged tails run the tensor-core scores over full groups + the canonical partial-group fixup
+    # (AUTO); the all-canonical SIMT path must give the same bits
+    canon = run_gpu(prob, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), lse=False)
+    assert np.array_equal(canon["coarse"], gpu["coarse"]) and np.array_equal(canon["labels"], gpu["labels"])
     for r, (o_ref, lse_ref) in enumerate(oracle_attention(prob, labels, 64)):
         compare_o(gpu["o"][r], o_ref, str(case))
         assert np.abs(gpu["lse"][r].cpu().numpy() - lse_ref).max() <= 1e-3
@@ -423,6 +427,12 @@ def test_varlen_batch(paged, T):
     bf.bfla_expand_rescue(P, cfg, m, ws)
     bf.bfla_sparse_prefill(P, cfg, m, ws)
     torch.cuda.synchronize()
+    # varlen Stage 1 runs on the tensor cores (full groups) + the canonical partial-group fixup; the
+    # all-canonical path gives the same coarse mask
+    mc = bf.alloc_mask(P, cfg)
+    bf.bfla_block_mask(P, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), mc, bf.alloc_workspace(P, cfg))
+    torch.cuda.synchronize()
+    assert torch.equal(mc.coarse_bits, m.coarse_bits)
     coarse, labels = m.coarse_dense().cpu().numpy(), m.tile_label.cpu().numpy()
     counts, lists = m.tile_count.cpu().numpy(), m.tile_list.cpu().numpy()
     Tq_max, Tkv_max = labels.shape[2], labels.shape[3]
@@ -644,3 +654,92 @@ def test_chunked_prefill_tensor_core_stage1(paged):
     assert np.abs(lg - lse_ref).max() <= 1e-3
     print(f"chunked TC paged={paged}: kappa={fast['stats']['kept_tiles'] / fast['stats']['causal_tiles']:.3f} "
           f"flagged={fast['stats']['rows_flagged']} max-abs={err.max():.2e}")
+
+
+@pytest.mark.parametrize("case", [
+    dict(B=1, Hq=8, Hkv=2, Nq=5000, Nkv=5000, d=128),     # ragged N: 5000 mod 64 = 8, several score tiles
+    dict(B=1, Hq=4, Hkv=2, Nq=3001, Nkv=9001, d=128),     # ragged chunk over a ragged context (N_c = 6000)
+    dict(B=1, Hq=4, Hkv=2, Nq=4100, Nkv=4100, d=256),     # d = 256, partial group of 4 tokens
+])
+def test_ragged_tensor_core_stage1(case):
+    """§8 f1 performance path: ragged N (n mod g != 0) takes the tensor-core Stage 1 (scores over full
+    groups, canonical rewrite of the partial group's row and column), bit-exact against the oracle and
+    against the all-canonical path, with more launches than the canonical chain (proof it ran)."""
+    prob = workloads.structured(23, block=256, **case)
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.1, seed=9)
+    n0 = bf.kernel_launches()
+    fast = run_gpu(prob, cfg, lse=False)
+    n_fast = bf.kernel_launches() - n0
+    n0 = bf.kernel_launches()
+    canon = run_gpu(prob, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), lse=False)
+    n_canon = bf.kernel_launches() - n0
+    assert n_fast > n_canon, (n_fast, n_canon)
+    assert np.array_equal(fast["coarse"], canon["coarse"]) and np.array_equal(fast["labels"], canon["labels"])
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(fast, ref, cfg)
+    check_lists(fast, labels, case["Nq"], case["Nkv"], 64)
+
+
+def test_varlen_tensor_core_stage1_large():
+    """Varlen batch with ragged requests at sizes spanning many score tiles: tensor-core Stage 1 (full
+    groups per request, padding garbage never read into a score) bit-exact against the oracle."""
+    lens = [(4000, 6500), (2048, 2048), (1000, 5000)]
+    prob, sl = _varlen_case(84, lens, Hq=8, Hkv=2)
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.0, seed=2)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o = torch.zeros_like(q)
+    P = bf.make_problem(q, k, v, o, seqlens=sl.cuda())
+    m = bf.alloc_mask(P, cfg, labels=True)
+    n0 = bf.kernel_launches()
+    bf.bfla_block_mask(P, cfg, m, bf.alloc_workspace(P, cfg))
+    n_fast = bf.kernel_launches() - n0
+    bf.bfla_expand_rescue(P, cfg, m, None)
+    mc = bf.alloc_mask(P, cfg)
+    n0 = bf.kernel_launches()
+    bf.bfla_block_mask(P, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), mc, bf.alloc_workspace(P, cfg))
+    n_canon = bf.kernel_launches() - n0
+    torch.cuda.synchronize()
+    assert n_fast > n_canon
+    assert torch.equal(mc.coarse_bits, m.coarse_bits)
+    coarse, labels = m.coarse_dense().cpu().numpy(), m.tile_label.cpu().numpy()
+    for r, (nq, nkv) in enumerate(lens):
+        qf, kf = f32(prob.q[r])[:, :nq], f32(prob.k[r])[:, :nkv]
+        ref = oracle.mask_pipeline(qf, kf, b=256, g=64, T=64, gamma=0.95, eta=16, rho=0.0, seed=2)
+        Lq, Lkv = ref["coarse"].shape[1:]
+        assert np.array_equal(coarse[r, :, :Lq, :Lkv], ref["coarse"]), r
+        Tq, Tkv = ref["labels"].shape[1:]
+        assert np.array_equal(labels[r, :, :Tq, :Tkv], ref["labels"]), r
+
+
+@pytest.mark.parametrize("d", [128, 256])
+def test_group_count_16_tensor_core(d):
+    """§8 f3: G = b/g = 16 — the paper's b = 1024, g = 64 row of Tab.mask — on the tensor-core
+    Stage 1 (the score epilogue max-pools 16 x 16 group pairs), bit-exact against the oracle and the
+    canonical path (which takes the any-G SIMT kernel)."""
+    prob = workloads.structured(31, B=1, Hq=4, Hkv=2, Nq=6144, Nkv=6144, d=d, block=1024)
+    cfg = bf.Config(b=1024, g=64, gamma=0.99, eta=16, rho=0.1, seed=4)
+    fast = run_gpu(prob, cfg, lse=False)
+    canon = run_gpu(prob, dataclasses.replace(cfg, scores=bf.SCORES_CANONICAL), lse=False)
+    assert np.array_equal(fast["coarse"], canon["coarse"]) and np.array_equal(fast["labels"], canon["labels"])
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(fast, ref, cfg)
+    check_lists(fast, labels, 6144, 6144, 64)
+    # G = 16 with g = 16 (b = 256): the recompute kernels' 16 chains per thread, forced through the band
+    cfg2 = bf.Config(b=256, g=16, gamma=0.95, eta=0, certify_slack=3000.0)
+    prob2 = workloads.gaussian(32, B=1, Hq=2, Hkv=1, Nq=2048, Nkv=2048, d=d, sigma=0.7)
+    g2 = run_gpu(prob2, cfg2, lse=False)
+    assert g2["stats"]["rows_flagged"] > 0
+    _check_masks(g2, oracle_masks(prob2, cfg2), cfg2)
+
+
+@pytest.mark.parametrize("b,n", [(64, 1000), (128, 1536)])
+def test_group_size_one_exact_block_max(b, n):
+    """§8 f3: g = 1 — Eq. 10 becomes the exact block max of Q K^T (G = b groups of one token) — on the
+    any-G canonical kernel; bit-exact against the oracle, ragged tail included."""
+    prob = workloads.gaussian(33, B=1, Hq=4, Hkv=2, Nq=n, Nkv=n, d=128, sigma=0.6)
+    cfg = bf.Config(b=b, g=1, gamma=0.95, eta=4, rho=0.0, seed=1)
+    gpu = run_gpu(prob, cfg)
+    ref = oracle_masks(prob, cfg)
+    labels = _check_masks(gpu, ref, cfg)
+    (o_ref, _), = oracle_attention(prob, labels, 64)
+    compare_o(gpu["o"][0], o_ref, f"g=1 b={b}")
