@@ -272,6 +272,32 @@ def varlen_timing(dev, reps=3):
     return out
 
 
+def make_head_output(args, B, Hq, N, d, world, rank, dev):
+    """Full-layer O for KV-head sharding: symmetric memory + the fused epilogue exchange (`--exchange
+    p2p`, default when torch symmetric memory works on this node), else rank-major storage + one in-place
+    NCCL all-gather (`--exchange nccl`, or the fallback)."""
+    from paper_2605_12193_b200 import parallel
+
+    if args.exchange in ("auto", "p2p"):
+        try:
+            out = parallel.PeerHeadOutput(B, Hq, N, d, world, rank, dev)
+            args.exchange_used = "p2p"
+            return out
+        except Exception as e:  # noqa: BLE001 — no NVLink symmetric memory here: NCCL all-gather instead
+            if args.exchange == "p2p":
+                raise
+            args.exchange_fallback = f"{type(e).__name__}: {e}"[:200]
+    args.exchange_used = "nccl"
+    return parallel.HeadShardedOutput(B, Hq, N, d, world, rank, dev)
+
+
+def exchange(hout):
+    if hasattr(hout, "mirrors"):
+        hout.finish()
+    else:
+        hout.gather()
+
+
 def run_ours(args, w, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -301,7 +327,7 @@ def run_ours(args, w, rank, world, local_rank):
         Hq, Hkv = q.shape[1], k.shape[1]
         # rank-major full O: this rank's heads are one contiguous chunk the kernel writes in place, and
         # one in-place all_gather_into_tensor assembles the layer (no staging buffer, cat or copy)
-        hout = parallel.HeadShardedOutput(1, w["Hq"], N, d, world, rank, dev)
+        hout = make_head_output(args, 1, w["Hq"], N, d, world, rank, dev)
     else:
         prob = make_inputs(w, 303 + rank, dev)
         q, k, v = prob.q, prob.k, prob.v
@@ -333,11 +359,14 @@ def run_ours(args, w, rank, world, local_rank):
         bf.bfla_expand_rescue(P, cfg, m, ws)
         if record is not None:
             record[2].record(st)
-        bf.bfla_sparse_prefill(P, cfg, m, ws)
+        if heads and hasattr(hout, "mirrors"):  # fused exchange: the epilogue stores into every peer's O
+            bf.bfla_sparse_prefill_mirrored(P, cfg, m, hout.mirrors, ws=ws)
+        else:
+            bf.bfla_sparse_prefill(P, cfg, m, ws)
         if record is not None:
             record[3].record(st)
-        if heads:  # the only exchange of the path: in-place all-gather of O's head groups (NCCL)
-            hout.gather()
+        if heads:  # the only exchange of the path: peers' stores visible (barrier) or NCCL all-gather of O
+            exchange(hout)
         if record is not None:
             record[4].record(st)
 
@@ -453,7 +482,7 @@ def run_ours(args, w, rank, world, local_rank):
     for _ in range(2):
         qd, kd, vd = torch.empty_like(q), torch.empty_like(kh, device=dev), torch.empty_like(vh, device=dev)
         if heads:
-            houts.append(parallel.HeadShardedOutput(1, w["Hq"], N, d, world, rank, dev))
+            houts.append(make_head_output(args, 1, w["Hq"], N, d, world, rank, dev))
             od = houts[-1].local
         else:
             od = torch.empty_like(o)
@@ -496,9 +525,12 @@ def run_ours(args, w, rank, world, local_rank):
         else:
             bf.bfla_block_mask(Pb, cfg, m, ws)
             bf.bfla_expand_rescue(Pb, cfg, m, ws)
-            bf.bfla_sparse_prefill(Pb, cfg, m, ws)
+            if heads and hasattr(houts[i % 2], "mirrors"):
+                bf.bfla_sparse_prefill_mirrored(Pb, cfg, m, houts[i % 2].mirrors, ws=ws)
+            else:
+                bf.bfla_sparse_prefill(Pb, cfg, m, ws)
         if heads:  # device-side exchange of the step; each rank then reads back its own heads
-            houts[i % 2].gather()
+            exchange(houts[i % 2])
         ev_done[i].record(st)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_done[i])
@@ -612,6 +644,10 @@ def main():
                     help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O "
                          "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
                          "slices + O all-reduce (strong, SURVEY §8 f2); auto: heads at N>1 (north_star)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="heads sharding: p2p = the prefill epilogue stores O into every peer's symmetric-memory "
+                         "buffer (fused exchange, §8 f2); nccl = in-place all-gather after the kernel; auto = p2p "
+                         "when symmetric memory is available")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
                     help="1: time CUDA-graph replays of the captured step (layers sharding); 0: eager launches "
@@ -643,7 +679,7 @@ def main():
               "rho": w["rho"], "pool": args.pool, "kv": f"paged{w['paged']}" if w["paged"] else "contiguous",
               "inputs": "structured synthetic (sinks+local+scattered heavy blocks), seed 303+rank",
               "l2": "no flush: per-layer inputs Q+K+V+O exceed the 126 MB L2" if w["N"] >= 16384 else "small",
-              "parallelism": (f"KV-head groups x{world} + NCCL all-gather of O" if args.shard == "heads" and world > 1
+              "parallelism": (f"KV-head groups x{world} + O exchange" if args.shard == "heads" and world > 1
                               else f"masks by KV-head group, prefill by cost-balanced row slices x{world} + NCCL "
                                    f"list all-gather and O all-reduce" if args.shard == "balanced" and world > 1
                               else f"independent layer per rank x{world}")}
@@ -717,15 +753,27 @@ def main():
         if r["s1_roof"] is not None:
             line["stage1_roofline"] = r["s1_roof"]
         line.update(r["extra"])
+        if args.shard == "heads" and world > 1:
+            line["config"]["exchange"] = ("fused: prefill epilogue stores O tiles into every peer's symmetric-memory "
+                                          "buffer + device barrier" if getattr(args, "exchange_used", "") == "p2p"
+                                          else "NCCL in-place all-gather after the prefill")
+            if getattr(args, "exchange_fallback", None):
+                line["config"]["exchange_fallback"] = args.exchange_fallback
         if world > 1:
             mg = {"rank_ms_per_step": r["rank_ms"], "max_over_ranks_ms": max(r["rank_ms"]),
                   "min_over_ranks_ms": min(r["rank_ms"])}
             if r["gather_ms"] is not None:
                 recv = r["o_bytes"] * (world - 1) / world
-                mg.update(o_allgather_ms=r["gather_ms"], o_allgather_recv_bytes_per_rank=recv,
-                          o_allgather_gbs=recv / (r["gather_ms"] * 1e-3) / 1e9,
-                          o_allgather="one in-place all_gather_into_tensor into the rank-major full O "
-                                      "(parallel.HeadShardedOutput), exposed after the prefill")
+                if getattr(args, "exchange_used", "") == "p2p":
+                    mg.update(o_exchange_exposed_ms=r["gather_ms"], o_exchange_recv_bytes_per_rank=recv,
+                              o_exchange="fused into the prefill epilogue (bfla_sparse_prefill_mirrored: every O "
+                                         "tile also TMA-stored into each peer's symmetric-memory buffer); the "
+                                         "exposed part is the device barrier after the kernel")
+                else:
+                    mg.update(o_allgather_ms=r["gather_ms"], o_allgather_recv_bytes_per_rank=recv,
+                              o_allgather_gbs=recv / (r["gather_ms"] * 1e-3) / 1e9,
+                              o_allgather="one in-place all_gather_into_tensor into the rank-major full O "
+                                          "(parallel.HeadShardedOutput), exposed after the prefill")
             if r["n1_ms"] is not None:
                 mg["same_layer_on_1_gpu_ms"] = r["n1_ms"]
             line["multi_gpu"] = mg

@@ -202,6 +202,27 @@ bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* 
 bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                      int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes, void* stream);
 
+/* Fused output exchange: the prefill epilogue stores every O row (+ LSE row) it
+   produces into up to BFLA_MAX_MIRRORS further buffers as well as problem->o / problem->lse — e.g. the
+   same head chunk of every peer GPU's full-layer O, mapped into this device's address space (NVLink
+   P2P / symmetric memory).  The exchange then overlaps the computation tile by tile instead of
+   following it as a separate all-gather; the caller orders the peers' reads after the kernel (a
+   device-side barrier across the ranks).  mirrors->o[k] uses problem->o's element offsets and strides
+   (same shape), mirrors->lse[k] problem->lse's (NULL: LSE not mirrored; ignored if problem->lse is
+   NULL).  Pointers: device-accessible, 16-byte aligned (else BFLA_ERR_MISALIGNED); never dereferenced
+   on the host.  row_begin = row_end = 0 means every row, otherwise the slice semantics of
+   bfla_sparse_prefill_rows.  n = 0 is exactly bfla_sparse_prefill(_rows).  Errors as those calls, plus
+   BFLA_ERR_INVALID_ARGUMENT for n outside [0, BFLA_MAX_MIRRORS] or a NULL o[k]. */
+#define BFLA_MAX_MIRRORS 7
+typedef struct {
+    int32_t n;
+    void* o[BFLA_MAX_MIRRORS];
+    float* lse[BFLA_MAX_MIRRORS];
+} bfla_mirrors;
+bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla_config* config,
+                                         const bfla_mask* mask, int64_t row_begin, int64_t row_end,
+                                         const bfla_mirrors* mirrors, void* ws, size_t ws_bytes, void* stream);
+
 /* Host-only (no GPU, no CUDA call): cost-balanced contiguous partition of the LPT row order into
    `parts` slices for bfla_sparse_prefill_rows (§8 f2: per-head kappa differs, so equal head counts per
    GPU are not equal work; P:443 runs 8 GPUs without naming a scheme).  tile_count is a HOST copy of

@@ -19,7 +19,7 @@ from ._lib import (KV_CONTIGUOUS, KV_PAGED, MASK_PER_KV_HEAD, MASK_PER_Q_HEAD, P
                    SCORES_CANONICAL, SELECT_MASS, SELECT_RATIO, bfla_config,
                    bfla_mask, bfla_problem, bfla_stats, check, lib)
 
-__all__ = ["Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
+__all__ = ["bfla_sparse_prefill_mirrored", "Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
            "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill",
            "bfla_sparse_prefill_rows", "bfla_balance_rows", "bfla_prefill", "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
            "SCORES_CANONICAL", "MASK_PER_KV_HEAD", "MASK_PER_Q_HEAD"]
@@ -218,6 +218,38 @@ def bfla_sparse_prefill_rows(problem: Problem, cfg: Config, mask: Mask, row_begi
     check(lib().bfla_sparse_prefill_rows(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
                                          int(row_begin), int(row_end), _ptr(ws), 0 if ws is None else ws.numel(),
                                          _stream(stream)), "bfla_sparse_prefill_rows")
+
+
+def bfla_sparse_prefill_mirrored(problem: Problem, cfg: Config, mask: Mask, mirrors, lse_mirrors=None,
+                                 rows: tuple[int, int] = (0, 0), ws: Optional[torch.Tensor] = None,
+                                 stream=None) -> None:
+    """Sparse prefill whose epilogue also stores every O (+ LSE) row into each of `mirrors` (§8 f2 fused
+    exchange, include/bfla.h).  mirrors: device tensors shaped like O, or raw device addresses (ints,
+    e.g. peer-mapped symmetric-memory pointers) with O's layout; lse_mirrors likewise (or None).
+    rows = (0, 0): every row, else an LPT row slice as in bfla_sparse_prefill_rows."""
+    mirrors = list(mirrors)
+    if len(mirrors) > _lib.MAX_MIRRORS:
+        raise ValueError(f"at most {_lib.MAX_MIRRORS} mirrors")
+    mc = _lib.bfla_mirrors()
+    mc.n = len(mirrors)
+    keep = []
+    for k, t in enumerate(mirrors):
+        if isinstance(t, torch.Tensor):
+            o = problem.tensors[3]
+            if t.shape != o.shape or t.stride() != o.stride() or t.dtype != o.dtype or t.device != o.device:
+                raise ValueError("an O mirror must have O's shape, strides and dtype")
+            keep.append(t)
+            mc.o[k] = t.data_ptr()
+        else:
+            mc.o[k] = int(t)
+        if lse_mirrors is not None and lse_mirrors[k] is not None:
+            lt = lse_mirrors[k]
+            mc.lse[k] = lt.data_ptr() if isinstance(lt, torch.Tensor) else int(lt)
+    m = mask.c()
+    check(lib().bfla_sparse_prefill_mirrored(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
+                                             int(rows[0]), int(rows[1]), ctypes.byref(mc), _ptr(ws),
+                                             0 if ws is None else ws.numel(), _stream(stream)),
+          "bfla_sparse_prefill_mirrored")
 
 
 def bfla_balance_rows(tile_count, parts: int, row_overhead: int = 3) -> list[int]:

@@ -62,10 +62,18 @@ class bfla_mask(ctypes.Structure):
                 ("tile_count", vp), ("tile_label", vp), ("kept_mass", vp), ("stats", vp)]
 
 
+MAX_MIRRORS = 7
+
+
+class bfla_mirrors(ctypes.Structure):
+    _fields_ = [("n", i32), ("o", vp * MAX_MIRRORS), ("lse", vp * MAX_MIRRORS)]
+
+
 _lib = None
 
 ENTRY_POINTS = ["bfla_workspace_size", "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue",
-                "bfla_sparse_prefill", "bfla_sparse_prefill_rows", "bfla_balance_rows", "bfla_prefill",
+                "bfla_sparse_prefill", "bfla_sparse_prefill_rows", "bfla_sparse_prefill_mirrored",
+                "bfla_balance_rows", "bfla_prefill",
                 "bfla_status_string", "bfla_last_error",
                 "bfla_kernel_launches"]
 
@@ -90,6 +98,9 @@ def lib():
         L.bfla_sparse_prefill_rows.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64, vp,
                                                ctypes.c_size_t, vp]
         L.bfla_sparse_prefill_rows.restype = ctypes.c_int
+        L.bfla_sparse_prefill_mirrored.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64,
+                                                   P(bfla_mirrors), vp, ctypes.c_size_t, vp]
+        L.bfla_sparse_prefill_mirrored.restype = ctypes.c_int
         L.bfla_balance_rows.argtypes = [P(i32), i32, i32, i32, i32, i32, P(i64)]
         L.bfla_balance_rows.restype = ctypes.c_int
         L.bfla_status_string.argtypes = [ctypes.c_int]

@@ -27,7 +27,6 @@ UNITS = {
     "stage2.cu": [],
     "attention.cu": [],
     "attention2.cu": [],
-    "attention3.cu": [],
 }
 
 

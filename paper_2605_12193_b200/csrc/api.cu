@@ -417,6 +417,10 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
     static const bool no_otma = experiment_knob("BFLA_OTMA", 1) == 0;  // A/B builds only
     maps.o_ok = 0;
     if (oal && !g.lens && !no_otma && encode_4d_quiet(&maps.o, P->o, dims, ostr, box)) maps.o_ok = 1;
+    // mirrors (fused exchange): TMA store maps with O's layout; if any cannot be encoded, every row
+    // (local and mirrored) goes through per-thread stores
+    for (int k = 0; k < g.n_mirror && maps.o_ok; ++k)
+      if (((uintptr_t)g.mo[k] % 16) || !encode_4d_quiet(&maps.mo.m[k], g.mo[k], dims, ostr, box)) maps.o_ok = 0;
   }
   if (!g.paged) {
     const uint64_t dims[4] = {(uint64_t)g.D, (uint64_t)g.Nkv, (uint64_t)g.Hkv_real, (uint64_t)g.B};
@@ -438,12 +442,8 @@ static bfla_status run_attention(const Geom& g, const bfla_problem* P, const int
   static const bool no_dyn = experiment_knob("BFLA_DYN_SCHED", 1) == 0;  // A/B builds: static round-robin
   if (no_dyn) sched = nullptr;
   if (sched) cudaMemsetAsync(sched, 0, sizeof(int32_t), st);
-#ifndef BFLA_ATTN3
-#define BFLA_ATTN3 0
-#endif
   int e = (g.D == 128 && !v1)
-              ? (BFLA_ATTN3 ? launch_attention3(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
-                            : launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched))
+              ? launch_attention2(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched)
               : launch_attention(g, maps, list, count, pt, dense, P->o, P->lse, num_sms_current(), st, sched);
   if (e) return fail(BFLA_ERR_CUDA, "attention launch: %s", cudaGetErrorString((cudaError_t)e));
   return cuda_check("attention launch");
@@ -532,6 +532,43 @@ bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_con
   if (row_end == row_begin) return BFLA_OK;  // an empty slice enqueues nothing
   g.row0 = (int)row_begin;
   g.nrows = (int)(row_end - row_begin);
+  const WsLayout L = ws_layout(g);
+  int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
+                                                : nullptr;
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
+}
+
+bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                         int64_t row_begin, int64_t row_end, const bfla_mirrors* mirrors, void* ws,
+                                         size_t ws_bytes, void* stream) {
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if (!mask || !mask->tile_list || !mask->tile_count) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask lists are NULL");
+  if (mirrors) {
+    if (mirrors->n < 0 || mirrors->n > BFLA_MAX_MIRRORS)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "mirrors->n = %d outside [0, %d]", mirrors->n, BFLA_MAX_MIRRORS);
+    for (int k = 0; k < mirrors->n; ++k) {
+      if (!mirrors->o[k]) return fail(BFLA_ERR_INVALID_ARGUMENT, "mirrors->o[%d] is NULL", k);
+      if (((uintptr_t)mirrors->o[k] % 16) || (mirrors->lse[k] && ((uintptr_t)mirrors->lse[k] % 4)))
+        return fail(BFLA_ERR_MISALIGNED, "mirror %d misaligned", k);
+      g.mo[k] = mirrors->o[k];
+      g.ml[k] = problem->lse ? mirrors->lse[k] : nullptr;
+    }
+    g.n_mirror = mirrors->n;
+  }
+  const int64_t rows = (int64_t)g.B * g.Hkv * g.Tq;
+  if (!(row_begin == 0 && row_end == 0)) {
+    if (row_begin < 0 || row_end < row_begin || row_end > rows)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                  (long long)row_end, (long long)rows);
+    if (row_end == row_begin) return BFLA_OK;
+    if (row_begin != 0 || row_end != rows) {
+      g.row0 = (int)row_begin;
+      g.nrows = (int)(row_end - row_begin);
+    }
+  }
   const WsLayout L = ws_layout(g);
   int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
                                                 : nullptr;

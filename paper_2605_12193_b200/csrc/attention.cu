@@ -371,6 +371,10 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         if (valid) {
           for (int c = 0; c < DH; ++c) orow[c] = __float2bfloat16(0.0f);
           if (lse && half == 0) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          for (int mi = 0; mi < g.n_mirror; ++mi) {
+            for (int c = 0; c < DH; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
+            if (lse && half == 0 && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          }
         }
         continue;
       }
@@ -493,11 +497,20 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
           uint4* dst = reinterpret_cast<uint4*>(orow + cc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          for (int mi = 0; mi < g.n_mirror; ++mi) {  // fused exchange (bfla_sparse_prefill_mirrored)
+            uint4* md = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O) + cc);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) md[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
         }
       }
-      if (valid && lse && half == 0)
-        lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
-            l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+      if (valid && lse && half == 0) {
+        const long long li = ((long long)it.r * g.Hq + p) * g.Nq + t;
+        const float lv = l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+        lse[li] = lv;
+        for (int mi = 0; mi < g.n_mirror; ++mi)
+          if (g.ml[mi]) g.ml[mi][li] = lv;
+      }
       tc_fence_before();
       mbar_arrive(o_free + q);
       pair_sync();  // partner has read lslot before the slot is reused by the next item's tile tc

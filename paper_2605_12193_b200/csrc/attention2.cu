@@ -78,7 +78,7 @@ struct Cfg2 {
   static constexpr int OFF_K = OFF_Q + QS * QBYTES;
   static constexpr int OFF_V = OFF_K + KS * SLOT;
   static constexpr int OFF_BAR = OFF_V + VS * SLOT;
-  static constexpr int NBAR = 2 * QS + 2 * KS + 2 * VS + 4 * NQT + 2 * 4;  // + item ring full/empty
+  static constexpr int NBAR = 2 * QS + 2 * KS + 2 * VS + 5 * NQT + 2 * 4;  // + item ring full/empty, p_half
   static constexpr int OFF_RING = OFF_BAR + NBAR * 8 + 16;  // int2 (item index, kept-tile count) x 4
   static constexpr int OFF_LX = OFF_RING + 4 * 8;  // SPLIT: row sums of the two column halves [NQT][2][128]
   static constexpr int SMEM_TOTAL = OFF_LX + (SPLIT == 2 ? NQT * 2 * 128 * 4 : 0);
@@ -91,14 +91,25 @@ struct Cfg2 {
 // SMX: softmax variant — 0 fused single pass with exact redo, 1 max-first whole row per thread
 // (MAXFIRST, default).  (Splitting a Q tile's 128 columns over two warpgroups with a row-max
 // exchange was measured 10% slower: the exponential phases of all softmax warps then coincide.)
+// A/B switches (default off): BFLA_SPLIT_P — PV of a two-tile step issued in halves (p_half after tile
+// a's P); BFLA_SUM_AFTER — the row sum of P taken from the stored bf16 P after the P arrive, off the
+// softmax -> MMA critical path
+#ifndef BFLA_SPLIT_P
+#define BFLA_SPLIT_P 0
+#endif
+#ifndef BFLA_SUM_AFTER
+#define BFLA_SUM_AFTER 0
+#endif
 template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY, bool SLICE = false>
 __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, int otma, Geom g, const int32_t* __restrict__ list,
+            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+            const __grid_constant__ MirrorMaps tmM, int otma, Geom g, const int32_t* __restrict__ list,
             const int32_t* __restrict__ count, const int32_t* __restrict__ page_table,
             __nv_bfloat16* __restrict__ O, float* __restrict__ lse, int n_items, int hpq, int NC, int opts,
             int* __restrict__ sched) {
   constexpr bool MAXFIRST = SMX >= 1;
+  constexpr bool SPLITP = BFLA_SPLIT_P && SMX == 1;  // split PV issue (the SMX = 1 softmax arrives p_half)
   constexpr int SPL = SMX == 2 ? 2 : 1;  // softmax warps per (TMEM lane group, Q tile)
   using C = Cfg2<NQT, PAGED, SPL>;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -116,7 +127,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
   uint64_t* o_free = o_full + NQT;     // [NQT]: epilogue has read O (128 arrivals)
   uint64_t* it_full = o_free + NQT;    // [4]: item ring entry published (K producer)
   uint64_t* it_empty = it_full + 4;    // [4]: entry read by every other role (11 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::QS + 2 * C::KS + 2 * C::VS + 4 * NQT + 8);
+  uint64_t* p_half = it_empty + 4;     // [NQT]: P_q of the step's first kept tile in TMEM (BFLA_SPLIT_P)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::QS + 2 * C::KS + 2 * C::VS + 5 * NQT + 8);
   volatile int* ring = reinterpret_cast<volatile int*>(smem + C::OFF_RING);  // [4][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -138,6 +150,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
       mbar_init(p_full + q, 128 * SPL);
       mbar_init(o_full + q, 1);
       mbar_init(o_free + q, 128 * SPL);
+      mbar_init(p_half + q, 128 * SPL);
     }
     for (int e = 0; e < 4; ++e) {
       mbar_init(it_full + e, 1);
@@ -357,14 +370,27 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
     const uint64_t dK = sdesc_sw128(smem_u32(smem + C::OFF_K), 16, 1024);
     const uint64_t dV = sdesc_sw128(smem_u32(smem + C::OFF_V), C::CHUNK, 1024);
     uint32_t ks0 = 0, nit = 0, st0 = 0;
-    auto issue_PV = [&](int q, uint32_t vslot, int ntile, bool acc_first) {
+    auto issue_PV = [&](int q, uint32_t vslot, int ntile, bool acc_first, int kk0 = 0) {
       const uint32_t idO = idesc_bf16(BM, D, 0, 1);
       const uint64_t b0 = dV + (uint64_t)((vslot * C::SLOT) >> 4);
       const uint32_t aP = tmem + C::COL_S + q * 128;
 #pragma unroll 8
-      for (int kk = 0; kk < ntile * 4; ++kk)  // split softmax: P of key tile b at column 64 (not 32)
+      for (int kk = kk0; kk < ntile * 4; ++kk)  // split softmax: P of key tile b at column 64 (not 32)
         umma_f16_ts_warp(tmem + C::COL_O + q * D, aP + kk * 8 + (SPL == 2 && kk >= 4 ? 32 : 0),
                          b0 + (uint64_t)((kk * 2048) >> 4), idO, (acc_first || kk > 0) ? 1u : 0u);
+    };
+    // BFLA_SPLIT_P: PV of a two-tile step in two halves — tile a's 4 MMAs as soon as its P is in TMEM
+    // (p_half), tile b's after p_full — so PV_a overlaps the softmax of tile b
+    uint32_t hph = 0;  // two-tile steps whose p_half has been consumed (same count for every q)
+    auto issue_PV_split = [&](int q, uint32_t vslot, uint32_t pfull_par, bool acc_first, bool first_of_item,
+                              uint32_t my_it) {
+      mbar_wait(p_half + q, hph & 1);
+      if (first_of_item) mbar_wait(o_free + q, (my_it & 1) ^ 1);
+      tc_fence_after();
+      issue_PV(q, vslot, 1, acc_first);
+      mbar_wait(p_full + q, pfull_par);
+      tc_fence_after();
+      issue_PV(q, vslot, 2, true, 4);
     };
     auto issue_S = [&](int q, int qsl, uint32_t kslot, int ntile) {
       const uint32_t idS = ntile == 2 ? idesc_bf16(BM, 2 * BN, 0, 0) : idesc_bf16(BM, BN, 0, 0);
@@ -399,11 +425,16 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
 #pragma unroll
         for (int q = 0; q < NQT; ++q) {
           if (s > 0) {  // O_q += P_q(s-1) [V]
+            if constexpr (SPLITP) {
+              issue_PV_split(q, vst, (st0 + s - 1) & 1, s > 1, s == 1, my_it);
+              if (q == NQT - 1) ++hph;
+            } else {
             mbar_wait(p_full + q, (st0 + s - 1) & 1);
             TRACE(0, 3 + 16 * q);
             if (s == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
             tc_fence_after();
             issue_PV(q, vst, 2, s > 1);  // every step but the last holds two tiles
+            }
           }
           const int qsl = qslot(my_it, q);
           if (s == 0) {
@@ -425,11 +456,16 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
       const int ntl = cnt - 2 * (ns - 1);
 #pragma unroll
       for (int q = 0; q < NQT; ++q) {
+        if (SPLITP && ntl == 2) {
+          issue_PV_split(q, vst, (st0 + ns - 1) & 1, ns > 1, ns == 1, my_it);
+          if (q == NQT - 1) ++hph;
+        } else {
         mbar_wait(p_full + q, (st0 + ns - 1) & 1);
         TRACE(0, 5 + 16 * q);
         if (ns == 1) mbar_wait(o_free + q, (my_it & 1) ^ 1);
         tc_fence_after();
         issue_PV(q, vst, ntl, ns > 1);
+        }
         umma_commit_warp(o_full + q);
       }
       umma_commit_warp(v_empty + vst);
@@ -470,6 +506,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         if (valid && hh == 0) {
           for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
           if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          for (int mi = 0; mi < g.n_mirror; ++mi) {
+            for (int c = 0; c < D; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
+            if (lse && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          }
         }
         continue;
       }
@@ -611,11 +651,20 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
           uint4* dst = reinterpret_cast<uint4*>(orow + hh * 64 + cc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          for (int mi = 0; mi < g.n_mirror; ++mi) {
+            uint4* md = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O) + hh * 64 + cc);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) md[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
         }
       }
-      if (valid && lse && hh == 0)
-        lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
-            l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+      if (valid && lse && hh == 0) {
+        const long long li = ((long long)it.r * g.Hq + p) * g.Nq + t;
+        const float lv = l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
+        lse[li] = lv;
+        for (int mi = 0; mi < g.n_mirror; ++mi)
+          if (g.ml[mi]) g.ml[mi][li] = lv;
+      }
       if (tr) TRACE(3 + q, 25);
       if (otma) {
         fence_proxy_async_smem();
@@ -624,9 +673,13 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
           for (int s = 0; s < hpq; ++s) {
             const int pls = it.c * heads_in_chunk + q * hpq + s;
             if (pls >= g.m) continue;
-            for (int dc = 0; dc < D / 64; ++dc)
+            for (int dc = 0; dc < D / 64; ++dc) {
               tma_store_4d(&tmO, qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T, it.h * g.m + pls,
                            it.r);
+              for (int mi = 0; mi < g.n_mirror; ++mi)  // fused exchange: the same tile into every mirror
+                tma_store_4d(&tmM.m[mi], qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T,
+                             it.h * g.m + pls, it.r);
+            }
           }
           bulk_commit();
           bulk_wait_read0();  // the smem has been read: Q of the next item may land there
@@ -661,6 +714,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         if (valid) {
           for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
           if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          for (int mi = 0; mi < g.n_mirror; ++mi) {
+            for (int c = 0; c < D; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
+            if (lse && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
+          }
         }
         continue;
       }
@@ -697,7 +754,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
               pr.x = ex2_approx(x.x);
               pr.y = ex2_approx(x.y);
             }
-            ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
+            if (!BFLA_SUM_AFTER || !MAXFIRST) ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
             pk[hf * 32 + e] = pack_bf16x2(pr.x, pr.y);
           }
         };
@@ -754,17 +811,35 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
           }
           const float msub = m_run == -INFINITY ? 0.0f : m_run;
           ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
+          if (SPLITP && s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+            // PV of tile a may start before this step's P is complete: rescale O first (O is
+            // complete through PV(s-1): the s_full commit covers every earlier MMA)
+#pragma unroll 1
+            for (int cc = 0; cc < D; cc += 32) {
+              float ov[32];
+              tmem_ld32(tO + cc, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+              tmem_st32(tO + cc, ov);
+            }
+          }
           exps64(v, 0, msub);
           tmem_st16(tS, pk);
           tmem_st16(tS + 16, pk + 16);
           if (lg == 0) TRACE(3 + q, 17);
           if (two) {
+            if (SPLITP) {  // tile a's P (and any O rescale) visible to the MMA warp
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(p_half + q);
+            }
             exps64(v + BN, 1, msub);
             tmem_st16(tS + 32, pk + 32);
             tmem_st16(tS + 48, pk + 48);
           }
           if (lg == 0) TRACE(3 + q, 9);
-          if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+          if (!SPLITP && s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
             // O is complete through PV(s-1): the s_full commit covers every earlier MMA
 #pragma unroll 1
             for (int cc = 0; cc < D; cc += 32) {
@@ -776,7 +851,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
               tmem_st32(tO + cc, ov);
             }
           }
-          l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+          if (!BFLA_SUM_AFTER)
+            l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
         } else {
           // fast path (running max known): one TMEM pass against m_run, checking the max on the way;
           // valid unless some row's max grew by more than 8 (then the lazy rule moves m_run)
@@ -862,6 +938,15 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         tc_fence_before();
         mbar_arrive(p_full + q);
         if (lg == 0) TRACE(3 + q, 10);
+        if (BFLA_SUM_AFTER && MAXFIRST) {  // row sum of the stored (bf16) P, off the critical path
+          float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            if (e >= 32 && !two) break;
+            a2[e & 3] = __fadd2_rn(a2[e & 3], make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
+          }
+          l_run += ((a2[0].x + a2[0].y) + (a2[1].x + a2[1].y)) + ((a2[2].x + a2[2].y) + (a2[3].x + a2[3].y));
+        }
       }
       // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2.  With otma, O is
       // staged (SW128) in this tile's Q smem — free once the last PV is done — and written by TMA
@@ -897,11 +982,20 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
           uint4* dst = reinterpret_cast<uint4*>(orow + cc);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          for (int mi = 0; mi < g.n_mirror; ++mi) {
+            uint4* md = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O) + cc);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) md[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
         }
       }
-      if (valid && lse)
-        lse[((long long)it.r * g.Hq + p) * g.Nq + t] =
-            l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+      if (valid && lse) {
+        const long long li = ((long long)it.r * g.Hq + p) * g.Nq + t;
+        const float lv = l_run > 0.0f ? (m_run + log2f(l_run)) * 0.6931471805599453f : -INFINITY;
+        lse[li] = lv;
+        for (int mi = 0; mi < g.n_mirror; ++mi)
+          if (g.ml[mi]) g.ml[mi][li] = lv;
+      }
       if (lg == 0) TRACE(3 + q, 25);
       if (otma) {
         fence_proxy_async_smem();
@@ -911,9 +1005,13 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
           for (int s = 0; s < hpq; ++s) {
             const int pls = it.c * heads_in_chunk + q * hpq + s;
             if (pls >= g.m) continue;
-            for (int dc = 0; dc < D / 64; ++dc)
+            for (int dc = 0; dc < D / 64; ++dc) {
               tma_store_4d(&tmO, qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T, it.h * g.m + pls,
                            it.r);
+              for (int mi = 0; mi < g.n_mirror; ++mi)  // fused exchange: the same tile into every mirror
+                tma_store_4d(&tmM.m[mi], qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T,
+                             it.h * g.m + pls, it.r);
+            }
           }
           bulk_commit();
           bulk_wait_read0();     // the smem has been read: Q of the next item may land there
@@ -943,7 +1041,7 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
   auto go = [&](auto kern, int smem, int threads) -> int {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
-    kern<<<grid, threads, smem, st>>>(maps.q, maps.k, maps.v, maps.o, maps.o_ok, g, list, count, pt,
+    kern<<<grid, threads, smem, st>>>(maps.q, maps.k, maps.v, maps.o, maps.mo, maps.o_ok, g, list, count, pt,
                                       static_cast<__nv_bfloat16*>(o), lse, n_items, hpq, NC, opts, sched);
     count_launch();
     return (int)cudaGetLastError();

@@ -48,6 +48,11 @@ struct Geom {
   // prefill work slice (bfla_sparse_prefill_rows, §8 f2): rows [row0, row0 + nrows) of the LPT row
   // order rho = (r * Hkv + h) * Tq + (Tq - 1 - i); nrows = 0 means every row
   int row0, nrows;
+  // fused output exchange (bfla_sparse_prefill_mirrored, §8 f2): every O / LSE row is also stored at the
+  // same element offset from mo[k] / ml[k] (ml[k] may be NULL), k < n_mirror
+  int n_mirror;
+  void* mo[7];
+  float* ml[7];
 };
 
 // Logical dimensions of request r (Eq. 4, 11, 19 with that request's N_q, N_kv).

@@ -47,10 +47,14 @@ void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int
                           unsigned long long* stats, cudaStream_t st);
 
 // Sparse / dense prefill (Eq. 27 / Eq. 1) — tcgen05 + TMEM + TMA.
+struct MirrorMaps {
+  CUtensorMap m[7];  // O mirrors as TMA store targets (attention2 epilogue, Geom::n_mirror of them)
+};
 struct AttnMaps {
   CUtensorMap q, k, v;
-  CUtensorMap o;  // O as a TMA store target (attention2 epilogue), valid when o_ok
+  CUtensorMap o;  // O as a TMA store target (attention2 epilogue), valid when o_ok (and every mirror map)
   int o_ok = 0;
+  MirrorMaps mo;
 };
 size_t attn_smem_bytes(int D, int nqt);
 int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
@@ -61,9 +65,4 @@ int launch_attention(const Geom& g, const AttnMaps& maps, const int32_t* list, c
 int launch_attention2(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
                       const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
                       int* sched = nullptr);
-// head_dim 128: one Q tile per item, S double-buffered in TMEM, column-split softmax (attention3.cu)
-int launch_attention3(const Geom& g, const AttnMaps& maps, const int32_t* list, const int32_t* count,
-                      const int32_t* page_table, int dense, void* o, float* lse, int num_sms, cudaStream_t st,
-                      int* sched = nullptr);
-
 }  // namespace bfla

@@ -449,20 +449,22 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
   }
 }
 
-// Ragged tails and varlen requests on the tensor-core path (§8 f1): the scores kernel covers full
-// groups only (a partial group's TMA row would read padding), so every block score a partial group
+// Ragged tails and varlen requests on the tensor-core path (§8 f1): the scores kernel max-pools full
+// groups only (a partial group's TMA row would read padding), so every block pair a partial group
 // takes part in — row i = L_q,r - 1 when n_q,r mod g != 0, column j = L_kv,r - 1 when n_kv,r mod g != 0 —
-// is rewritten here in the canonical order.  Exact scores need no certification slack: the selector's
-// bound (tau ||x|| ||y||, norms over the full groups) stays conservative for them.  CTA per
+// is finished here: the group pairs that involve a partial group, (u_p, v) and (u, v_p), are computed
+// in the canonical order (token chains of C fp32 FMAs, token dots added in ascending t) and max-ed into
+// the tensor-core score of the full pairs.  Those pairs are exact, so |S_f - S_c| <= tau ||x|| ||y|| (norms
+// over the full groups) still bounds the block score: the certification stays a proof.  CTA per
 // (r, p, unit): units [0, L_kv) walk the partial row, [L_kv, L_kv + L_q) the partial column.
 template <int D>
 __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const __nv_bfloat16* __restrict__ q,
                                                                  const __nv_bfloat16* __restrict__ k,
                                                                  float* __restrict__ S) {
-  extern __shared__ float tokdot[];
+  extern __shared__ float tokdot[];  // [2G - 1][g] token dots, then [2G - 1] pair totals
   const int per = g.Lkv + g.Lq;
   const int idx = blockIdx.x % per, rp = blockIdx.x / per;
-  const int p = rp % g.Hq, r = rp / g.Hq;
+  const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
   const Req R = req_of(g, r);
   const bool qrag = R.Nq % g.g != 0, krag = R.Nkv % g.g != 0;
   int i, j;
@@ -480,7 +482,61 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
   long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
   if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
   if ((long long)j * g.b > e_i) return;  // Eq. 11-13: not causal
-  canon_block_score<D>(g, R, q, k, r, p, i, j, tokdot, S);
+  const int G = g.G, gg = g.g;
+  // partial groups of this unit: u_p = full groups before the tail of the last query block (-1: none)
+  const int up = (qrag && i == R.Lq - 1) ? (R.Nq - i * g.b) / gg : -1;
+  const int vp = (krag && j == R.Lkv - 1) ? (R.Nkv - j * g.b) / gg : -1;
+  const int nrow = up >= 0 ? G : 0;                 // pairs (u_p, v), v = 0..G-1
+  const int npair = nrow + (vp >= 0 ? (up >= 0 ? G - 1 : G) : 0);  // + pairs (u, v_p), u != u_p
+  auto pair_uv = [&](int pi, int& u, int& v) {
+    if (pi < nrow) {
+      u = up;
+      v = pi;
+    } else {
+      const int kx = pi - nrow;
+      u = (up >= 0 && kx >= up) ? kx + 1 : kx;
+      v = vp;
+    }
+  };
+  const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
+  const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
+  for (int c = threadIdx.x; c < npair * gg; c += kRecThreads) {  // chain (pair, t), t fastest
+    int u, v;
+    pair_uv(c / gg, u, v);
+    const int t = c % gg;
+    const int tq = i * g.b + u * gg + t, tk = j * g.b + v * gg + t;
+    float acc = 0.f;
+    if (tq < R.Nq && tk < R.Nkv) {  // padding tokens are exact zeros: dot 0
+      const __nv_bfloat16* x = qb + (long long)tq * g.qs2;
+      const __nv_bfloat16* y = kb + (long long)tk * g.kvs2;
+#pragma unroll 4
+      for (int cc = 0; cc < D; cc += 8) {
+        float xf[8], yf[8];
+        bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(x + cc)), xf);
+        bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(y + cc)), yf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xf[e], yf[e], acc);
+      }
+    }
+    tokdot[c] = acc;
+  }
+  __syncthreads();
+  float* pairtot = tokdot + npair * gg;
+  for (int pi = threadIdx.x; pi < npair; pi += kRecThreads) {
+    int u, v;
+    pair_uv(pi, u, v);
+    float a = 0.0f;
+    for (int t = 0; t < gg; ++t) a = __fadd_rn(a, tokdot[pi * gg + t]);  // ascending t (§4 item 2)
+    const bool valid = i * g.b + u * gg < R.Nq && j * g.b + v * gg < R.Nkv;  // padding-only groups (R3)
+    pairtot[pi] = valid ? a : -INFINITY;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float* s = S + (((long long)r * g.Hq + p) * g.Lq + i) * g.Lkv + j;
+    float mx = *s;  // the tensor-core max over the full pairs (-inf if there are none)
+    for (int pi = 0; pi < npair; ++pi) mx = fmaxf(mx, pairtot[pi]);  // Eq. 10
+    *s = mx;
+  }
 }
 
 // Same units and the same arithmetic order, operands staged in shared memory: the unit's K block and
@@ -935,9 +991,8 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
 }
 
 int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st) {
-  if (g.G * g.G > kRecThreads) return -1;
   const long long ctas = (long long)g.B * g.Hq * (g.Lkv + g.Lq);
-  const int smem = (g.G * g.G * g.g + g.G * g.G) * 4;
+  const int smem = ((2 * g.G - 1) * g.g + 2 * g.G) * 4;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<(int)ctas, kRecThreads, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),

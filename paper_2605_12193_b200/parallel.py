@@ -73,6 +73,48 @@ class HeadShardedOutput:
                                            async_op=async_op)
 
 
+def mirror_addresses(buffer_ptrs, rank: int, chunk_offset_bytes: int) -> list[int]:
+    """Addresses of this rank's head chunk inside every PEER's full-layer buffer (rank order, self
+    excluded): buffer_ptrs[p] is peer p's symmetric buffer as mapped into this device's address space;
+    the chunk sits at the same byte offset in every rank's buffer (rank-major storage)."""
+    return [int(b) + int(chunk_offset_bytes) for p, b in enumerate(buffer_ptrs) if p != rank]
+
+
+class PeerHeadOutput:
+    """Fused O exchange for KV-head sharding (§8 f2 / §8(e)): the rank-major full-layer O of
+    HeadShardedOutput, allocated in symmetric memory (torch.distributed._symmetric_memory maps every
+    rank's buffer into every peer's address space over NVLink).  The prefill writes its head chunk into
+    its own buffer and, through bfla_sparse_prefill_mirrored, into the same chunk of every peer's
+    buffer from the attention epilogue — the exchange rides along tile by tile instead of running as an
+    all-gather after the kernel.  finish() is the device-side cross-rank barrier (signal pads) after
+    which every rank's buffer holds the whole layer.  Raises if symmetric memory is unavailable (the
+    caller then falls back to HeadShardedOutput + NCCL)."""
+
+    def __init__(self, B: int, Hq: int, N: int, d: int, world: int, rank: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+
+        if Hq % world:
+            raise ValueError(f"h_q={Hq} is not divisible by world={world}")
+        if world - 1 > 7:
+            raise ValueError("at most 7 peers (BFLA_MAX_MIRRORS)")
+        self.world, self.rank = world, rank
+        self.store = symm.empty((world, B, Hq // world, N, d), dtype=torch.bfloat16, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        self.hdl = symm.rendezvous(self.store, grp.group_name)
+        self.local = self.store[rank]
+        base = int(self.hdl.buffer_ptrs[rank])
+        off = self.local.data_ptr() - base  # this rank's chunk inside any rank's buffer
+        if off < 0:
+            raise RuntimeError("symmetric buffer does not start at the tensor")
+        self.mirrors = mirror_addresses(self.hdl.buffer_ptrs, rank, off)
+        perm = self.store.permute(1, 0, 2, 3, 4)
+        self.full = perm.reshape(B, Hq, N, d) if B == 1 else perm
+
+    def finish(self):
+        """Every rank's mirrored stores are visible in every buffer once all ranks pass this barrier."""
+        self.hdl.barrier(channel=0)
+
+
 def request_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     """Request (batch) slice for request-level sharding: requests are fully independent."""
     per = -(-batch // world)

@@ -43,6 +43,7 @@ def test_struct_layout_matches_header(L, tmp_path):
         "bfla_config": [f[0] for f in L.bfla_config._fields_],
         "bfla_mask": [f[0] for f in L.bfla_mask._fields_],
         "bfla_stats": [f[0] for f in L.bfla_stats._fields_],
+        "bfla_mirrors": [f[0] for f in L.bfla_mirrors._fields_],
     }
     lines = ['#include "bfla.h"', "#include <stdio.h>", "#include <stddef.h>", "int main(void){"]
     for s, fs in fields.items():
@@ -133,3 +134,21 @@ def test_misaligned_and_workspace(L):
     m.tile_list_capacity = 5
     assert so.bfla_expand_rescue(ctypes.byref(p), ctypes.byref(_cfg(L)), ctypes.byref(m), None, 0, None) == 5
     assert so.bfla_status_string(5) == b"BFLA_ERR_CAPACITY"
+
+
+def test_mirrored_prefill_validation(L):
+    """bfla_sparse_prefill_mirrored validates its mirror set on the host before any launch."""
+    so = L.lib()
+    m = L.bfla_mask()
+    m.tile_list = m.tile_count = 1 << 20
+    mir = L.bfla_mirrors()
+    mir.n = L.MAX_MIRRORS + 1
+    P = ctypes.byref
+    r = so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 0, 0, P(mir), None, 0, None)
+    assert r == 1 and b"mirrors" in so.bfla_last_error()
+    mir.n = 1  # o[0] is NULL
+    assert so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 0, 0, P(mir), None, 0, None) == 1
+    mir.o[0] = (1 << 20) + 8  # not 16-byte aligned
+    assert so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 0, 0, P(mir), None, 0, None) == 3
+    mir.o[0] = 1 << 20
+    assert so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 5, 3, P(mir), None, 0, None) == 1

@@ -743,3 +743,98 @@ def test_group_size_one_exact_block_max(b, n):
     labels = _check_masks(gpu, ref, cfg)
     (o_ref, _), = oracle_attention(prob, labels, 64)
     compare_o(gpu["o"][0], o_ref, f"g=1 b={b}")
+
+
+@pytest.mark.parametrize("case", ["d128", "d256", "varlen", "rows", "paged"])
+def test_mirrored_prefill_fused_exchange(case):
+    """§8 f2 fused exchange: bfla_sparse_prefill_mirrored stores every O / LSE row into each mirror as
+    well (on a multi-GPU box the mirrors are peers' symmetric-memory buffers; here, two local buffers).
+    Mirrors and the local O must equal the plain sparse prefill bit for bit — TMA-store epilogue
+    (d128, rows, paged), per-thread stores (d256, varlen) — and a row slice writes only its rows."""
+    d = 256 if case == "d256" else 128
+    if case == "varlen":
+        prob, sl = _varlen_case(91, [(1500, 3000), (700, 700)], Hq=8, Hkv=2)
+    else:
+        prob, sl = workloads.structured(41, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=d, block=256), None
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.1, seed=3)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    B, Hq, Nq, _ = q.shape
+    o_ref = torch.zeros_like(q)
+    l_ref = torch.zeros(B, Hq, Nq, dtype=torch.float32, device="cuda")
+    if case == "paged":
+        kc, vc, pt = workloads.paged(k, v, 16, seed=9, extra_pages=2)
+        mk = lambda o, l: bf.make_problem(q, kc, vc, o, l, page_table=pt, n_kv=k.shape[2])
+    else:
+        mk = lambda o, l: bf.make_problem(q, k, v, o, l, seqlens=None if sl is None else sl.cuda())
+    P = mk(o_ref, l_ref)
+    ws, m = bf.alloc_workspace(P, cfg), bf.alloc_mask(P, cfg)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    o = torch.zeros_like(q)
+    l = torch.zeros_like(l_ref)
+    mo = [torch.zeros_like(q) for _ in range(2)]
+    ml = [torch.zeros_like(l_ref) for _ in range(2)]
+    P2 = mk(o, l)
+    rows = (0, 0)
+    if case == "rows":
+        Tq = -(-Nq // 64)
+        rows = (Tq // 3, 2 * Tq)  # part of head group 0 and all of head group 1 (LPT order)
+    n0 = bf.kernel_launches()
+    bf.bfla_sparse_prefill_mirrored(P2, cfg, m, mo, ml, rows=rows, ws=ws)
+    torch.cuda.synchronize()
+    assert bf.kernel_launches() - n0 == 1  # one kernel: the exchange is fused into its epilogue
+    if case != "rows":
+        for t, ref in [(o, o_ref)] + [(x, o_ref) for x in mo]:
+            assert torch.equal(t, ref)
+        for t in [l] + ml:
+            assert torch.equal(t, l_ref)
+        return
+    # the slice's rows: (h, i) for LPT rho in [r0, r1) -> query heads h*m .. h*m+m-1, tokens i*64 ..
+    Tq, m_ = -(-Nq // 64), Hq // 2
+    want = torch.zeros(B, Hq, Nq, dtype=torch.bool, device="cuda")
+    for rho in range(*rows):
+        h, i = rho // Tq, Tq - 1 - rho % Tq
+        want[:, h * m_:(h + 1) * m_, i * 64:(i + 1) * 64] = True
+    for t in [o] + mo:
+        assert torch.equal(t[want], o_ref[want]) and not t[~want].any()
+    for t in [l] + ml:
+        assert torch.equal(t[want], l_ref[want]) and not t[~want].any()
+
+
+def test_peer_head_output_symmetric_memory_single_rank():
+    """The fused-exchange plumbing on one rank: parallel.PeerHeadOutput allocates the rank-major O in
+    torch symmetric memory and rendezvouses (no peers, so no mirrors); the mirrored prefill into its
+    local chunk plus the device barrier equals the plain prefill.  On a one-GPU box without symmetric
+    memory support the test is skipped (bench falls back to the NCCL all-gather, reported in its line)."""
+    import socket
+
+    import torch.distributed as dist
+    from paper_2605_12193_b200 import parallel
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        prob = workloads.structured(16, B=1, Hq=8, Hkv=2, Nq=3072, Nkv=3072, d=128, block=256)
+        q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+        cfg = bf.Config(b=256, g=64, eta=8, rho=0.1, seed=4)
+        o_ref, _ = bf.prefill(q, k, v, cfg)
+        try:
+            hout = parallel.PeerHeadOutput(1, 8, 3072, 128, 1, 0, q.device)
+        except Exception as e:  # noqa: BLE001
+            pytest.skip(f"torch symmetric memory unavailable: {e}")
+        assert hout.mirrors == []
+        P = bf.make_problem(q, k, v, hout.local)
+        ws, m = bf.alloc_workspace(P, cfg), bf.alloc_mask(P, cfg)
+        bf.bfla_block_mask(P, cfg, m, ws)
+        bf.bfla_expand_rescue(P, cfg, m, ws)
+        bf.bfla_sparse_prefill_mirrored(P, cfg, m, hout.mirrors, ws=ws)
+        hout.finish()
+        torch.cuda.synchronize()
+        assert torch.equal(hout.full, o_ref)
+    finally:
+        dist.destroy_process_group()

@@ -229,3 +229,17 @@ def test_bench_self_launch_command():
     env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_mirror_addresses_peer_chunks():
+    """Fused exchange (parallel.PeerHeadOutput): rank r's head chunk sits at the same byte offset in every
+    rank's symmetric buffer; the mirrors are the peers' buffers (self excluded) at that offset, in rank
+    order — checked against an explicit rank-major layout."""
+    from paper_2605_12193_b200 import parallel
+
+    world, chunk = 4, 3 * 1024
+    bases = [0x7f0000000000 + p * (1 << 30) for p in range(world)]  # peer buffers as mapped locally
+    for rank in range(world):
+        got = parallel.mirror_addresses(bases, rank, rank * chunk)
+        assert got == [bases[p] + rank * chunk for p in range(world) if p != rank]
+        assert len(got) == world - 1
