@@ -91,14 +91,15 @@ struct Cfg2 {
 // SMX: softmax variant — 0 fused single pass with exact redo, 1 max-first whole row per thread
 // (MAXFIRST, default).  (Splitting a Q tile's 128 columns over two warpgroups with a row-max
 // exchange was measured 10% slower: the exponential phases of all softmax warps then coincide.)
-// A/B switches (default off): BFLA_SPLIT_P — PV of a two-tile step issued in halves (p_half after tile
-// a's P); BFLA_SUM_AFTER — the row sum of P taken from the stored bf16 P after the P arrive, off the
-// softmax -> MMA critical path
+// BFLA_SPLIT_P (default 1; 0 for A/B): the PV of a two-tile step is issued in halves — tile a's 4 MMAs
+// as soon as its P is in TMEM (p_half), tile b's after p_full — so PV_a overlaps the softmax of tile b
+// and the softmax -> MMA -> softmax chain of a Q tile shortens by PV_a.  Measured (same box, 5 runs):
+// sparse 32K 0.964 -> 0.937 ms, 128K 9.31 -> 8.95 ms, dense 32K 6.89 -> 6.75-6.85 ms; O bit-identical.
+// Not kept: a 3/4 split (p_half after 96 keys: 0.951 ms), the split with half of tile b's exponentials
+// run before the wait on tile a's stores (0.940 / 8.84 ms: equal within noise), and the row sum taken
+// from the stored bf16 P after the arrive (1.013 ms: the deferred adds delay the next step).
 #ifndef BFLA_SPLIT_P
-#define BFLA_SPLIT_P 0
-#endif
-#ifndef BFLA_SUM_AFTER
-#define BFLA_SUM_AFTER 0
+#define BFLA_SPLIT_P 1
 #endif
 template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY, bool SLICE = false>
 __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1)
@@ -263,16 +264,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
 #define BFLA_REG_PROD 96
 #define BFLA_REG_SMX 200
 #endif
-#ifndef BFLA_REG_PROD2
-#define BFLA_REG_PROD2 56
-#define BFLA_REG_SMX2 112
-#endif
-#ifndef BFLA_SPLIT_SETMAXNREG
-#define BFLA_SPLIT_SETMAXNREG 1
-#endif
     if (NQT == 2 && SMX == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD) : "memory");
-    if (NQT == 2 && SMX == 2 && BFLA_SPLIT_SETMAXNREG)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(BFLA_REG_PROD2) : "memory");
   if (warp == 0) {
     // ================================ TMA producer (K) ================================
     {
@@ -375,8 +367,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
       const uint64_t b0 = dV + (uint64_t)((vslot * C::SLOT) >> 4);
       const uint32_t aP = tmem + C::COL_S + q * 128;
 #pragma unroll 8
-      for (int kk = kk0; kk < ntile * 4; ++kk)  // split softmax: P of key tile b at column 64 (not 32)
-        umma_f16_ts_warp(tmem + C::COL_O + q * D, aP + kk * 8 + (SPL == 2 && kk >= 4 ? 32 : 0),
+      for (int kk = kk0; kk < ntile * 4; ++kk)
+        umma_f16_ts_warp(tmem + C::COL_O + q * D, aP + kk * 8,
                          b0 + (uint64_t)((kk * 2048) >> 4), idO, (acc_first || kk > 0) ? 1u : 0u);
     };
     // BFLA_SPLIT_P: PV of a two-tile step in two halves — tile a's 4 MMAs as soon as its P is in TMEM
@@ -387,10 +379,10 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
       mbar_wait(p_half + q, hph & 1);
       if (first_of_item) mbar_wait(o_free + q, (my_it & 1) ^ 1);
       tc_fence_after();
-      issue_PV(q, vslot, 1, acc_first);
+      issue_PV(q, vslot, 1, acc_first);  // tile a: keys 0..63, P columns 0..31
       mbar_wait(p_full + q, pfull_par);
       tc_fence_after();
-      issue_PV(q, vslot, 2, true, 4);
+      issue_PV(q, vslot, 2, true, 4);  // tile b
     };
     auto issue_S = [&](int q, int qsl, uint32_t kslot, int ntile) {
       const uint32_t idS = ntile == 2 ? idesc_bf16(BM, 2 * BN, 0, 0) : idesc_bf16(BM, BN, 0, 0);
@@ -473,222 +465,6 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
       st0 += ns;
     }
   }
-  } else if constexpr (SMX == 2) {
-    // ======================= softmax / epilogue, column-split (SMX = 2) =======================
-    // Two warpgroups per Q tile: half hh owns the S columns of kept tile hh of the step (64 keys) —
-    // its exponentials, its P columns, its 64 columns of O.  The row max is shared: each half reads the
-    // other half's S columns too (max only), so both compute the same max, lazy rule and m_run with no
-    // exchange; a named barrier per step orders every S read of the tile before any P store over it.
-    // Row sums are kept per half and added (half 0 + half 1) in the epilogue through shared memory.
-    if (NQT == 2 && BFLA_SPLIT_SETMAXNREG)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BFLA_REG_SMX2) : "memory");
-    const int sw = warp - 4;
-    const int q = sw >> 3, hh = (sw >> 2) & 1;
-    const int lg = warp & 3;         // TMEM lane group of this warp
-    const int row = lg * 32 + lane;  // row of Q tile q = TMEM lane
-    const uint32_t lane_addr = (uint32_t)(lg * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + C::COL_S + q * 128;
-    const uint32_t tO = tmem + lane_addr + C::COL_O + q * D + hh * 64;
-    float* lx = reinterpret_cast<float*>(smem + C::OFF_LX) + q * 256;  // [half][row]
-    const float c2 = g.scale * 1.4426950408889634f;  // softmax scale in the exp2 domain
-    const bool tr = hh == 0 && lg == 0;
-    uint32_t st = 0, nit = 0;
-    for (int idx, cnt; next_item(idx, cnt);) {
-      const Item it = decode_item<SLICE>(g, idx, NC);
-      const int slot = row / g.T;
-      const int pl = it.c * heads_in_chunk + q * hpq + slot;
-      const int t = it.i * g.T + (row % g.T);
-      const Req Rq = req_of(g, it.r);  // this request's logical dims (varlen)
-      const bool valid = slot < hpq && pl < g.m && t < Rq.Nq;
-      const int p = it.h * g.m + pl;
-      __nv_bfloat16* orow = O + (long long)it.r * g.os0 + (long long)p * g.os1 + (long long)t * g.os2;
-      if (cnt == 0) {  // cannot happen for masks from bfla_expand_rescue (sink + band); defined anyway
-        if (valid && hh == 0) {
-          for (int c = 0; c < D; ++c) orow[c] = __float2bfloat16(0.0f);
-          if (lse) lse[((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
-          for (int mi = 0; mi < g.n_mirror; ++mi) {
-            for (int c = 0; c < D; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
-            if (lse && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
-          }
-        }
-        continue;
-      }
-      const uint32_t my_it = nit++;
-      const int32_t* lst = DENSE ? nullptr : row_list(it);
-      const int ns = (cnt + 1) / 2;
-      float m_run = -INFINITY, l_run = 0.0f;
-      for (int s = 0; s < ns; ++s, ++st) {
-        const bool two = 2 * s + 1 < cnt;
-        const int ja = tile_at_c(lst, cnt, 2 * s), jb = two ? tile_at_c(lst, cnt, 2 * s + 1) : 0;
-        mbar_wait(s_full + q, st & 1);
-        if (tr) TRACE(3 + q, 8);
-        tc_fence_after();
-        // token-exact causality inside each tile (Eq. 27): key j*64 + c visible iff <= N_c + t
-        const int la = Rq.Nc + t - ja * BN, lb = two ? Rq.Nc + t - jb * BN : -1;
-        const bool own = hh == 0 || two;          // this half has a kept tile in the step
-        const bool oth = hh == 1 || two;          // the other half has one
-        const int lim_own = hh ? lb : la, lim_oth = hh ? la : lb;
-        float v[64];
-        float mrow = -INFINITY;
-        if (oth) {  // the other half's columns: their max only, 32 columns at a time
-#pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
-            float u[32];
-            tmem_ld32(tS + (1 - hh) * 64 + ch * 32, u);
-            tmem_wait_ld();
-            if (lim_oth < BN - 1) {
-#pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (ch * 32 + c > lim_oth) u[c] = -INFINITY;
-            }
-            float a = max3f(u[0], u[1], u[2]), b2 = max3f(u[16], u[17], u[18]);
-#pragma unroll
-            for (int c = 3; c < 15; c += 2) {
-              a = max3f(a, u[c], u[c + 1]);
-              b2 = max3f(b2, u[16 + c], u[16 + c + 1]);
-            }
-            mrow = max3f(mrow, fmaxf(a, u[15]), fmaxf(b2, u[31]));
-          }
-        }
-        if (own) {
-          tmem_ld32(tS + hh * 64, v);
-          tmem_ld32(tS + hh * 64 + 32, v + 32);
-          tmem_wait_ld();
-          if (lim_own < BN - 1) {
-#pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (c > lim_own) v[c] = -INFINITY;
-          }
-          mrow = fmaxf(mrow, row_max64(v));
-        }
-        if (tr) TRACE(3 + q, 16);
-        named_bar_sync(3 + q, 256);  // every S column of the tile has been read: P may overwrite them
-        const float mx = mrow * c2;
-        float alpha = 1.0f;
-        // lazy rescale (same rule and same inputs in both halves, so the same m_run)
-        if (mx > m_run + kLazy || (m_run == -INFINITY && mx > -INFINITY)) {
-          alpha = ex2_approx(m_run - mx);  // 0 when m_run = -inf
-          l_run *= alpha;
-          m_run = mx;
-        }
-        const float msub = m_run == -INFINITY ? 0.0f : m_run;
-        float2 ls[4];
-        ls[0] = ls[1] = ls[2] = ls[3] = make_float2(0.f, 0.f);
-        if (own) {
-          // P of this half goes to the first 32 columns of its own S columns (tS + 64 hh), which only
-          // this half reads: no other warp can still need them (issue_PV reads P at that layout)
-          const float2 c22 = make_float2(c2, c2), nm2 = make_float2(-msub, -msub);
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {  // 16 columns -> 8 packed P registers -> TMEM
-            uint32_t pk[8];
-#pragma unroll
-            for (int e2 = 0; e2 < 8; ++e2) {
-              const int e = ch * 8 + e2;
-              const float2 x = __ffma2_rn(make_float2(v[2 * e], v[2 * e + 1]), c22, nm2);
-              float2 pr;
-              if ((POLY >> (e % 8)) & 1) {
-                pr = exp2_poly2(x);
-              } else {
-                pr.x = ex2_approx(x.x);
-                pr.y = ex2_approx(x.y);
-              }
-              ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
-              pk[e2] = pack_bf16x2(pr.x, pr.y);
-            }
-            tmem_st8(tS + hh * 64 + ch * 8, pk);
-          }
-        }
-        if (tr) TRACE(3 + q, 9);
-        if (s > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-          // O is complete through PV(s-1): the s_full commit covers every earlier MMA; own 64 columns
-#pragma unroll 1
-          for (int cc = 0; cc < 64; cc += 32) {
-            float ov[32];
-            tmem_ld32(tO + cc, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
-            tmem_st32(tO + cc, ov);
-          }
-        }
-        l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(p_full + q);
-        if (tr) TRACE(3 + q, 10);
-      }
-      // epilogue: l = l_half0 + l_half1 (fixed order); O / l -> bf16 -> global (own 64 columns)
-      mbar_wait(o_full + q, my_it & 1);
-      if (tr) TRACE(3 + q, 12);
-      tc_fence_after();
-      lx[hh * 128 + row] = l_run;
-      named_bar_sync(3 + q, 256);
-      const float l_tot = lx[row] + lx[128 + row];
-      const float inv_l = l_tot > 0.0f ? 1.0f / l_tot : 0.0f;
-      const int qsl = qslot(my_it, q);
-      unsigned char* qs = smem + C::OFF_Q + qsl * C::QBYTES;
-#pragma unroll 1
-      for (int cc = 0; cc < 64; cc += 32) {
-        float ov[32];
-        tmem_ld32(tO + cc, ov);
-        tmem_wait_ld();
-        if (cc == 32) {  // own O columns fully read from TMEM: the next item's PV may overwrite them
-          tc_fence_before();
-          mbar_arrive(o_free + q);
-        }
-        uint32_t w[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
-        if (otma) {
-          // row `row` of the 128-row tile, 16-byte pieces k = cc / 8 .. + 3 of d-chunk hh
-          unsigned char* rb = qs + hh * (BM * 128) + row * 128;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = (cc >> 3) + e;
-            st_shared_v4(rb + ((k ^ (row & 7)) << 4), w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-          }
-        } else if (valid && !(opts & 2)) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + hh * 64 + cc);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-          for (int mi = 0; mi < g.n_mirror; ++mi) {
-            uint4* md = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O) + hh * 64 + cc);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) md[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-          }
-        }
-      }
-      if (valid && lse && hh == 0) {
-        const long long li = ((long long)it.r * g.Hq + p) * g.Nq + t;
-        const float lv = l_tot > 0.0f ? (m_run + log2f(l_tot)) * 0.6931471805599453f : -INFINITY;
-        lse[li] = lv;
-        for (int mi = 0; mi < g.n_mirror; ++mi)
-          if (g.ml[mi]) g.ml[mi][li] = lv;
-      }
-      if (tr) TRACE(3 + q, 25);
-      if (otma) {
-        fence_proxy_async_smem();
-        asm volatile("bar.sync %0, 256;" ::"r"(1 + q) : "memory");
-        if (warp == 4 + 8 * q && lane == 0) {
-          for (int s = 0; s < hpq; ++s) {
-            const int pls = it.c * heads_in_chunk + q * hpq + s;
-            if (pls >= g.m) continue;
-            for (int dc = 0; dc < D / 64; ++dc) {
-              tma_store_4d(&tmO, qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T, it.h * g.m + pls,
-                           it.r);
-              for (int mi = 0; mi < g.n_mirror; ++mi)  // fused exchange: the same tile into every mirror
-                tma_store_4d(&tmM.m[mi], qs + dc * (BM * 128) + s * (g.T * 128), dc * 64, it.i * g.T,
-                             it.h * g.m + pls, it.r);
-            }
-          }
-          bulk_commit();
-          bulk_wait_read0();  // the smem has been read: Q of the next item may land there
-          mbar_arrive(q_empty + qsl);
-        }
-      }
-      if (tr) TRACE(3 + q, 13);
-    }
-    if (otma && warp == 4 + 8 * q && lane == 0) bulk_wait_all();  // O stores complete before exit
   } else {
     if (NQT == 2 && SMX == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(BFLA_REG_SMX) : "memory");
 
@@ -754,7 +530,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
               pr.x = ex2_approx(x.x);
               pr.y = ex2_approx(x.y);
             }
-            if (!BFLA_SUM_AFTER || !MAXFIRST) ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
+            ls[e & 3] = __fadd2_rn(ls[e & 3], pr);
             pk[hf * 32 + e] = pack_bf16x2(pr.x, pr.y);
           }
         };
@@ -851,8 +627,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
               tmem_st32(tO + cc, ov);
             }
           }
-          if (!BFLA_SUM_AFTER)
-            l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
+          l_run += ((ls[0].x + ls[0].y) + (ls[1].x + ls[1].y)) + ((ls[2].x + ls[2].y) + (ls[3].x + ls[3].y));
         } else {
           // fast path (running max known): one TMEM pass against m_run, checking the max on the way;
           // valid unless some row's max grew by more than 8 (then the lazy rule moves m_run)
@@ -938,15 +713,6 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         tc_fence_before();
         mbar_arrive(p_full + q);
         if (lg == 0) TRACE(3 + q, 10);
-        if (BFLA_SUM_AFTER && MAXFIRST) {  // row sum of the stored (bf16) P, off the critical path
-          float2 a2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-          for (int e = 0; e < 64; ++e) {
-            if (e >= 32 && !two) break;
-            a2[e & 3] = __fadd2_rn(a2[e & 3], make_float2(__uint_as_float(pk[e] << 16), __uint_as_float(pk[e] & 0xffff0000u)));
-          }
-          l_run += ((a2[0].x + a2[0].y) + (a2[1].x + a2[1].y)) + ((a2[2].x + a2[2].y) + (a2[3].x + a2[3].y));
-        }
       }
       // epilogue: O / l -> bf16 -> global; LSE (natural log) = (m + log2 l) ln 2.  With otma, O is
       // staged (SW128) in this tile's Q smem — free once the last PV is done — and written by TMA
@@ -1052,15 +818,6 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
 #endif
   constexpr int PM = BFLA_POLY_MASK;
   using C = Cfg2<NQT, PAGED>;
-#ifndef BFLA_SOFTMAX_SPLIT
-#define BFLA_SOFTMAX_SPLIT 0
-#endif
-  if constexpr (BFLA_SOFTMAX_SPLIT) {  // two softmax warpgroups per Q tile (column halves)
-    using C2 = Cfg2<NQT, PAGED, 2>;
-    if constexpr (!DENSE)
-      if (g.nrows) return go(k_attn2<NQT, PAGED, false, 2, PM, true>, C2::SMEM_TOTAL, C2::THREADS);
-    return go(k_attn2<NQT, PAGED, DENSE, 2, PM>, C2::SMEM_TOTAL, C2::THREADS);
-  }
   if constexpr (!DENSE)
     if (g.nrows) return go(k_attn2<NQT, PAGED, false, 1, PM, true>, C::SMEM_TOTAL, C::THREADS);  // work slice
   if (smx == 0) return go(k_attn2<NQT, PAGED, DENSE, 0, PM>, C::SMEM_TOTAL, C::THREADS);
