@@ -456,15 +456,16 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
 // in the canonical order (token chains of C fp32 FMAs, token dots added in ascending t) and max-ed into
 // the tensor-core score of the full pairs.  Those pairs are exact, so |S_f - S_c| <= tau ||x|| ||y|| (norms
 // over the full groups) still bounds the block score: the certification stays a proof.  CTA per
-// (r, p, unit): units [0, L_kv) walk the partial row, [L_kv, L_kv + L_q) the partial column.
+// (r, h, unit) over the m query heads of mask group h (so a KV block is read from L2 once and re-read
+// from L1 by the other heads): units [0, L_kv) walk the partial row, [L_kv, L_kv + L_q) the partial column.
 template <int D>
 __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const __nv_bfloat16* __restrict__ q,
                                                                  const __nv_bfloat16* __restrict__ k,
                                                                  float* __restrict__ S) {
   extern __shared__ float tokdot[];  // [2G - 1][g] token dots, then [2G - 1] pair totals
   const int per = g.Lkv + g.Lq;
-  const int idx = blockIdx.x % per, rp = blockIdx.x / per;
-  const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
+  const int idx = blockIdx.x % per, rh = blockIdx.x / per;
+  const int h = rh % g.Hkv, r = rh / g.Hkv;
   const Req R = req_of(g, r);
   const bool qrag = R.Nq % g.g != 0, krag = R.Nkv % g.g != 0;
   int i, j;
@@ -498,8 +499,9 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
       v = vp;
     }
   };
-  const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
   const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
+  for (int p = h * g.m; p < (h + 1) * g.m; ++p) {
+  const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
   for (int c = threadIdx.x; c < npair * gg; c += kRecThreads) {  // chain (pair, t), t fastest
     int u, v;
     pair_uv(c / gg, u, v);
@@ -536,6 +538,8 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
     float mx = *s;  // the tensor-core max over the full pairs (-inf if there are none)
     for (int pi = 0; pi < npair; ++pi) mx = fmaxf(mx, pairtot[pi]);  // Eq. 10
     *s = mx;
+  }
+  __syncthreads();  // tokdot / pairtot reused by the next query head
   }
 }
 
@@ -991,7 +995,7 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
 }
 
 int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st) {
-  const long long ctas = (long long)g.B * g.Hq * (g.Lkv + g.Lq);
+  const long long ctas = (long long)g.B * g.Hkv * (g.Lkv + g.Lq);
   const int smem = ((2 * g.G - 1) * g.g + 2 * g.G) * 4;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
