@@ -278,6 +278,15 @@ def make_head_output(args, B, Hq, N, d, world, rank, dev):
     NCCL all-gather (`--exchange nccl`, or the fallback)."""
     from paper_2605_12193_b200 import parallel
 
+    if args.exchange in ("auto", "nvls"):
+        try:
+            out = parallel.PeerHeadOutput(B, Hq, N, d, world, rank, dev, multicast=True)
+            args.exchange_used = "nvls"
+            return out
+        except Exception as e:  # noqa: BLE001 — no multicast here: P2P stores, else NCCL
+            if args.exchange == "nvls":
+                raise
+            args.exchange_fallback = f"nvls: {type(e).__name__}: {e}"[:200]
     if args.exchange in ("auto", "p2p"):
         try:
             out = parallel.PeerHeadOutput(B, Hq, N, d, world, rank, dev)
@@ -286,7 +295,7 @@ def make_head_output(args, B, Hq, N, d, world, rank, dev):
         except Exception as e:  # noqa: BLE001 — no NVLink symmetric memory here: NCCL all-gather instead
             if args.exchange == "p2p":
                 raise
-            args.exchange_fallback = f"{type(e).__name__}: {e}"[:200]
+            args.exchange_fallback = (getattr(args, "exchange_fallback", "") + f"; p2p: {type(e).__name__}: {e}")[:300]
     args.exchange_used = "nccl"
     return parallel.HeadShardedOutput(B, Hq, N, d, world, rank, dev)
 
@@ -360,7 +369,7 @@ def run_ours(args, w, rank, world, local_rank):
         if record is not None:
             record[2].record(st)
         if heads and hasattr(hout, "mirrors"):  # fused exchange: the epilogue stores into every peer's O
-            bf.bfla_sparse_prefill_mirrored(P, cfg, m, hout.mirrors, ws=ws)
+            bf.bfla_sparse_prefill_mirrored(P, cfg, m, hout.mirrors, ws=ws, multicast_o=hout.multicast_o)
         else:
             bf.bfla_sparse_prefill(P, cfg, m, ws)
         if record is not None:
@@ -526,7 +535,8 @@ def run_ours(args, w, rank, world, local_rank):
             bf.bfla_block_mask(Pb, cfg, m, ws)
             bf.bfla_expand_rescue(Pb, cfg, m, ws)
             if heads and hasattr(houts[i % 2], "mirrors"):
-                bf.bfla_sparse_prefill_mirrored(Pb, cfg, m, houts[i % 2].mirrors, ws=ws)
+                bf.bfla_sparse_prefill_mirrored(Pb, cfg, m, houts[i % 2].mirrors, ws=ws,
+                                                multicast_o=houts[i % 2].multicast_o)
             else:
                 bf.bfla_sparse_prefill(Pb, cfg, m, ws)
         if heads:  # device-side exchange of the step; each rank then reads back its own heads
@@ -644,10 +654,10 @@ def main():
                     help="layers: one independent layer per rank (weak); heads: KV-head groups of one layer + O "
                          "all-gather (strong); balanced: masks by KV-head group, prefill by cost-balanced row "
                          "slices + O all-reduce (strong, SURVEY §8 f2); auto: heads at N>1 (north_star)")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
-                    help="heads sharding: p2p = the prefill epilogue stores O into every peer's symmetric-memory "
-                         "buffer (fused exchange, §8 f2); nccl = in-place all-gather after the kernel; auto = p2p "
-                         "when symmetric memory is available")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nvls", "p2p", "nccl"],
+                    help="heads sharding: nvls = the prefill epilogue stores O through the symmetric buffer's NVLS "
+                         "multicast address (multimem.st, fused exchange, §8 f2); p2p = one TMA store per peer "
+                         "buffer; nccl = in-place all-gather after the kernel; auto = the first that works")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", type=int, default=0, choices=[0, 1],
                     help="1: time CUDA-graph replays of the captured step (layers sharding); 0: eager launches "
@@ -754,9 +764,10 @@ def main():
             line["stage1_roofline"] = r["s1_roof"]
         line.update(r["extra"])
         if args.shard == "heads" and world > 1:
-            line["config"]["exchange"] = ("fused: prefill epilogue stores O tiles into every peer's symmetric-memory "
-                                          "buffer + device barrier" if getattr(args, "exchange_used", "") == "p2p"
-                                          else "NCCL in-place all-gather after the prefill")
+            line["config"]["exchange"] = {
+                "nvls": "fused: prefill epilogue multimem.st of O rows through the NVLS multicast address + device barrier",
+                "p2p": "fused: prefill epilogue TMA-stores O tiles into every peer's symmetric-memory buffer + device barrier",
+            }.get(getattr(args, "exchange_used", ""), "NCCL in-place all-gather after the prefill")
             if getattr(args, "exchange_fallback", None):
                 line["config"]["exchange_fallback"] = args.exchange_fallback
         if world > 1:
@@ -764,11 +775,12 @@ def main():
                   "min_over_ranks_ms": min(r["rank_ms"])}
             if r["gather_ms"] is not None:
                 recv = r["o_bytes"] * (world - 1) / world
-                if getattr(args, "exchange_used", "") == "p2p":
+                if getattr(args, "exchange_used", "") in ("p2p", "nvls"):
                     mg.update(o_exchange_exposed_ms=r["gather_ms"], o_exchange_recv_bytes_per_rank=recv,
                               o_exchange="fused into the prefill epilogue (bfla_sparse_prefill_mirrored: every O "
-                                         "tile also TMA-stored into each peer's symmetric-memory buffer); the "
-                                         "exposed part is the device barrier after the kernel")
+                                         "row also stored into each peer's symmetric-memory buffer, by NVLS "
+                                         "multimem.st or per-peer TMA stores, see config.exchange); the exposed "
+                                         "part is the device barrier after the kernel")
                 else:
                     mg.update(o_allgather_ms=r["gather_ms"], o_allgather_recv_bytes_per_rank=recv,
                               o_allgather_gbs=recv / (r["gather_ms"] * 1e-3) / 1e9,

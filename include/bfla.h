@@ -212,12 +212,18 @@ bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_con
    NULL).  Pointers: device-accessible, 16-byte aligned (else BFLA_ERR_MISALIGNED); never dereferenced
    on the host.  row_begin = row_end = 0 means every row, otherwise the slice semantics of
    bfla_sparse_prefill_rows.  n = 0 is exactly bfla_sparse_prefill(_rows).  Errors as those calls, plus
-   BFLA_ERR_INVALID_ARGUMENT for n outside [0, BFLA_MAX_MIRRORS] or a NULL o[k]. */
+   BFLA_ERR_INVALID_ARGUMENT for n outside [0, BFLA_MAX_MIRRORS] or a NULL o[k].
+   multicast_o / multicast_lse (optional, NULL = unused): NVLS multicast addresses (e.g. the
+   multicast_ptr of a torch symmetric-memory buffer) with problem->o's / problem->lse's layout; every
+   O / LSE row is also written through `multimem.st` to them, so the NVSwitch replicates it into every
+   member GPU's buffer (one store per row instead of one per peer).  16-byte aligned. */
 #define BFLA_MAX_MIRRORS 7
 typedef struct {
     int32_t n;
     void* o[BFLA_MAX_MIRRORS];
     float* lse[BFLA_MAX_MIRRORS];
+    void* multicast_o;
+    float* multicast_lse;
 } bfla_mirrors;
 bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla_config* config,
                                          const bfla_mask* mask, int64_t row_begin, int64_t row_end,

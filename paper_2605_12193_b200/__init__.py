@@ -222,10 +222,11 @@ def bfla_sparse_prefill_rows(problem: Problem, cfg: Config, mask: Mask, row_begi
 
 def bfla_sparse_prefill_mirrored(problem: Problem, cfg: Config, mask: Mask, mirrors, lse_mirrors=None,
                                  rows: tuple[int, int] = (0, 0), ws: Optional[torch.Tensor] = None,
-                                 stream=None) -> None:
+                                 stream=None, multicast_o: int = 0, multicast_lse: int = 0) -> None:
     """Sparse prefill whose epilogue also stores every O (+ LSE) row into each of `mirrors` (§8 f2 fused
     exchange, include/bfla.h).  mirrors: device tensors shaped like O, or raw device addresses (ints,
     e.g. peer-mapped symmetric-memory pointers) with O's layout; lse_mirrors likewise (or None).
+    multicast_o / multicast_lse: NVLS multicast addresses (ints) written through multimem.st.
     rows = (0, 0): every row, else an LPT row slice as in bfla_sparse_prefill_rows."""
     mirrors = list(mirrors)
     if len(mirrors) > _lib.MAX_MIRRORS:
@@ -245,6 +246,8 @@ def bfla_sparse_prefill_mirrored(problem: Problem, cfg: Config, mask: Mask, mirr
         if lse_mirrors is not None and lse_mirrors[k] is not None:
             lt = lse_mirrors[k]
             mc.lse[k] = lt.data_ptr() if isinstance(lt, torch.Tensor) else int(lt)
+    mc.multicast_o = int(multicast_o) or None
+    mc.multicast_lse = int(multicast_lse) or None
     m = mask.c()
     check(lib().bfla_sparse_prefill_mirrored(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
                                              int(rows[0]), int(rows[1]), ctypes.byref(mc), _ptr(ws),

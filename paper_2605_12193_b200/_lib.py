@@ -66,7 +66,8 @@ MAX_MIRRORS = 7
 
 
 class bfla_mirrors(ctypes.Structure):
-    _fields_ = [("n", i32), ("o", vp * MAX_MIRRORS), ("lse", vp * MAX_MIRRORS)]
+    _fields_ = [("n", i32), ("o", vp * MAX_MIRRORS), ("lse", vp * MAX_MIRRORS), ("multicast_o", vp),
+                ("multicast_lse", vp)]
 
 
 _lib = None

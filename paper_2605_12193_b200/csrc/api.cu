@@ -557,6 +557,12 @@ bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla
       g.ml[k] = problem->lse ? mirrors->lse[k] : nullptr;
     }
     g.n_mirror = mirrors->n;
+    if (mirrors->multicast_o) {
+      if (((uintptr_t)mirrors->multicast_o % 16) || (mirrors->multicast_lse && ((uintptr_t)mirrors->multicast_lse % 4)))
+        return fail(BFLA_ERR_MISALIGNED, "multicast address misaligned");
+      g.mco = mirrors->multicast_o;
+      g.mcl = problem->lse ? mirrors->multicast_lse : nullptr;
+    }
   }
   const int64_t rows = (int64_t)g.B * g.Hkv * g.Tq;
   if (!(row_begin == 0 && row_end == 0)) {

@@ -375,6 +375,9 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
             for (int c = 0; c < DH; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
             if (lse && half == 0 && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
           }
+          if (g.mco)
+            for (int c = 0; c < DH; c += 8) multimem_st16(static_cast<__nv_bfloat16*>(g.mco) + (orow - O) + c, 0u, 0u, 0u, 0u);
+          if (lse && half == 0 && g.mcl) multimem_st_f32(g.mcl + ((long long)it.r * g.Hq + p) * g.Nq + t, -INFINITY);
         }
         continue;
       }
@@ -502,6 +505,11 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) md[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
           }
+          if (g.mco) {  // NVLS multicast: one store per 16 bytes reaches every member GPU
+            __nv_bfloat16* mc = static_cast<__nv_bfloat16*>(g.mco) + (orow - O) + cc;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) multimem_st16(mc + 8 * e, w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          }
         }
       }
       if (valid && lse && half == 0) {
@@ -510,6 +518,7 @@ __global__ void __launch_bounds__(Cfg<D, NQT, SPL>::THREADS, 1)
         lse[li] = lv;
         for (int mi = 0; mi < g.n_mirror; ++mi)
           if (g.ml[mi]) g.ml[mi][li] = lv;
+        if (g.mcl) multimem_st_f32(g.mcl + li, lv);
       }
       tc_fence_before();
       mbar_arrive(o_free + q);

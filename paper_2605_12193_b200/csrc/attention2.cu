@@ -96,13 +96,16 @@ struct Cfg2 {
 // and the softmax -> MMA -> softmax chain of a Q tile shortens by PV_a.  Measured (same box, 5 runs):
 // sparse 32K 0.964 -> 0.937 ms, 128K 9.31 -> 8.95 ms, dense 32K 6.89 -> 6.75-6.85 ms; O bit-identical.
 // Not kept: a 3/4 split (p_half after 96 keys: 0.951 ms), the split with half of tile b's exponentials
-// run before the wait on tile a's stores (0.940 / 8.84 ms: equal within noise), and the row sum taken
-// from the stored bf16 P after the arrive (1.013 ms: the deferred adds delay the next step).
+// run before the wait on tile a's stores (0.940 / 8.84 ms: equal within noise), the row sum taken
+// from the stored bf16 P after the arrive (1.013 ms: the deferred adds delay the next step), and both
+// softmax warpgroups sharing each Q tile by column halves with a smem row-max exchange (correct on the
+// parity suite, but 1.046 vs 0.935 ms / 10.38 vs 9.25 ms at 128K: the TMEM load, exchange and P-store
+// latencies are then paid twice per step per warpgroup).
 #ifndef BFLA_SPLIT_P
 #define BFLA_SPLIT_P 1
 #endif
 template <int NQT, bool PAGED, bool DENSE, int SMX, int POLY, bool SLICE = false>
-__global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     k_attn2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
             const __grid_constant__ MirrorMaps tmM, int otma, Geom g, const int32_t* __restrict__ list,
@@ -111,8 +114,8 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
             int* __restrict__ sched) {
   constexpr bool MAXFIRST = SMX >= 1;
   constexpr bool SPLITP = BFLA_SPLIT_P && SMX == 1;  // split PV issue (the SMX = 1 softmax arrives p_half)
-  constexpr int SPL = SMX == 2 ? 2 : 1;  // softmax warps per (TMEM lane group, Q tile)
-  using C = Cfg2<NQT, PAGED, SPL>;
+  constexpr int SPL = 1;
+  using C = Cfg2<NQT, PAGED>;
   extern __shared__ __align__(1024) unsigned char smem[];
   if (smem_u32(smem) & 1023) __trap();  // SW128 operands need 1024-byte alignment (no static smem here)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -375,14 +378,14 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
     // (p_half), tile b's after p_full — so PV_a overlaps the softmax of tile b
     uint32_t hph = 0;  // two-tile steps whose p_half has been consumed (same count for every q)
     auto issue_PV_split = [&](int q, uint32_t vslot, uint32_t pfull_par, bool acc_first, bool first_of_item,
-                              uint32_t my_it) {
+                              uint32_t my_it, int ntile = 2) {
       mbar_wait(p_half + q, hph & 1);
       if (first_of_item) mbar_wait(o_free + q, (my_it & 1) ^ 1);
       tc_fence_after();
       issue_PV(q, vslot, 1, acc_first);  // tile a: keys 0..63, P columns 0..31
       mbar_wait(p_full + q, pfull_par);
       tc_fence_after();
-      issue_PV(q, vslot, 2, true, 4);  // tile b
+      if (ntile == 2) issue_PV(q, vslot, 2, true, 4);  // tile b
     };
     auto issue_S = [&](int q, int qsl, uint32_t kslot, int ntile) {
       const uint32_t idS = ntile == 2 ? idesc_bf16(BM, 2 * BN, 0, 0) : idesc_bf16(BM, BN, 0, 0);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
 #pragma unroll
       for (int q = 0; q < NQT; ++q) {
         if (SPLITP && ntl == 2) {
-          issue_PV_split(q, vst, (st0 + ns - 1) & 1, ns > 1, ns == 1, my_it);
+          issue_PV_split(q, vst, (st0 + ns - 1) & 1, ns > 1, ns == 1, my_it, ntl);
           if (q == NQT - 1) ++hph;
         } else {
         mbar_wait(p_full + q, (st0 + ns - 1) & 1);
@@ -494,6 +497,9 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
             for (int c = 0; c < D; ++c) (static_cast<__nv_bfloat16*>(g.mo[mi]) + (orow - O))[c] = __float2bfloat16(0.0f);
             if (lse && g.ml[mi]) g.ml[mi][((long long)it.r * g.Hq + p) * g.Nq + t] = -INFINITY;
           }
+          if (g.mco)
+            for (int c = 0; c < D; c += 8) multimem_st16(static_cast<__nv_bfloat16*>(g.mco) + (orow - O) + c, 0u, 0u, 0u, 0u);
+          if (lse && g.mcl) multimem_st_f32(g.mcl + ((long long)it.r * g.Hq + p) * g.Nq + t, -INFINITY);
         }
         continue;
       }
@@ -736,6 +742,11 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) w[e] = pack_bf16x2(ov[2 * e] * inv_l, ov[2 * e + 1] * inv_l);
+        if (g.mco && valid) {  // NVLS: the switch replicates the row into every member GPU's O
+          __nv_bfloat16* mc = static_cast<__nv_bfloat16*>(g.mco) + (orow - O) + cc;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) multimem_st16(mc + 8 * e, w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+        }
         if (otma) {
           // row `row` of the 128-row tile, 16-byte pieces k = (cc % 64) / 8 .. + 3 of d-chunk cc / 64
           unsigned char* rb = qs + (cc / 64) * (BM * 128) + row * 128;
@@ -761,6 +772,7 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED, SMX == 2 ? 2 : 1>::THREADS, 1
         lse[li] = lv;
         for (int mi = 0; mi < g.n_mirror; ++mi)
           if (g.ml[mi]) g.ml[mi][li] = lv;
+        if (g.mcl) multimem_st_f32(g.mcl + li, lv);
       }
       if (lg == 0) TRACE(3 + q, 25);
       if (otma) {

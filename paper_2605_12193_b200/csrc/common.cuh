@@ -53,7 +53,20 @@ struct Geom {
   int n_mirror;
   void* mo[7];
   float* ml[7];
+  // NVLS multicast addresses of O / LSE (multimem.st reaches every member GPU's buffer); NULL = unused
+  void* mco;
+  float* mcl;
 };
+
+// multimem stores (NVLS): 16 bytes / one fp32 through a multicast address
+__device__ __forceinline__ void multimem_st16(void* mc, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(__uint_as_float(a)),
+               "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d))
+               : "memory");
+}
+__device__ __forceinline__ void multimem_st_f32(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
 
 // Logical dimensions of request r (Eq. 4, 11, 19 with that request's N_q, N_kv).
 struct Req {

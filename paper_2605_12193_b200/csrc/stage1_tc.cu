@@ -458,11 +458,14 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_recompute_rows(Geom g, const
 // over the full groups) still bounds the block score: the certification stays a proof.  CTA per
 // (r, h, unit) over the m query heads of mask group h (so a KV block is read from L2 once and re-read
 // from L1 by the other heads): units [0, L_kv) walk the partial row, [L_kv, L_kv + L_q) the partial column.
-template <int D>
+template <int D, bool STAGE>
 __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const __nv_bfloat16* __restrict__ q,
                                                                  const __nv_bfloat16* __restrict__ k,
                                                                  float* __restrict__ S) {
-  extern __shared__ float tokdot[];  // [2G - 1][g] token dots, then [2G - 1] pair totals
+  constexpr int PITCH = D * 2 + 16;  // staged key row (bytes), padded: lanes (consecutive tokens) hit distinct banks
+  extern __shared__ __align__(16) unsigned char fx[];  // [b][PITCH] key block, then token dots + pair totals
+  // (STAGE = false, blocks too large for smem: keys are read from global memory / L1 instead)
+  float* tokdot = reinterpret_cast<float*>(fx + (STAGE ? (size_t)g.b * PITCH : 0));  // [2G - 1][g], then [2G - 1]
   const int per = g.Lkv + g.Lq;
   const int idx = blockIdx.x % per, rh = blockIdx.x / per;
   const int h = rh % g.Hkv, r = rh / g.Hkv;
@@ -500,6 +503,14 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
     }
   };
   const __nv_bfloat16* kb = k + (long long)r * g.kvs0 + (long long)(h / g.kvdiv) * g.kvs1;
+  // the unit's key block, staged once with coalesced 16-byte copies (shared by every chain and head)
+  const int kt0 = j * g.b, nkt = min(g.b, R.Nkv - kt0);
+  for (int x = threadIdx.x; STAGE && x < nkt * (D / 8); x += kRecThreads) {
+    const int tr = x / (D / 8), c8 = x % (D / 8);
+    *reinterpret_cast<uint4*>(fx + (size_t)tr * PITCH + c8 * 16) =
+        __ldg(reinterpret_cast<const uint4*>(kb + (long long)(kt0 + tr) * g.kvs2) + c8);
+  }
+  __syncthreads();
   for (int p = h * g.m; p < (h + 1) * g.m; ++p) {
   const __nv_bfloat16* qb = q + (long long)r * g.qs0 + (long long)p * g.qs1;
   for (int c = threadIdx.x; c < npair * gg; c += kRecThreads) {  // chain (pair, t), t fastest
@@ -510,12 +521,13 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
     float acc = 0.f;
     if (tq < R.Nq && tk < R.Nkv) {  // padding tokens are exact zeros: dot 0
       const __nv_bfloat16* x = qb + (long long)tq * g.qs2;
-      const __nv_bfloat16* y = kb + (long long)tk * g.kvs2;
+      const unsigned char* y = fx + (size_t)(tk - kt0) * PITCH;
+      const __nv_bfloat16* yg = kb + (long long)tk * g.kvs2;
 #pragma unroll 4
       for (int cc = 0; cc < D; cc += 8) {
         float xf[8], yf[8];
         bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(x + cc)), xf);
-        bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(y + cc)), yf);
+        bf16x8_f32(STAGE ? *reinterpret_cast<const uint4*>(y + cc * 2) : __ldg(reinterpret_cast<const uint4*>(yg + cc)), yf);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc = __fmaf_rn(xf[e], yf[e], acc);
       }
@@ -996,14 +1008,17 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
 
 int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st) {
   const long long ctas = (long long)g.B * g.Hkv * (g.Lkv + g.Lq);
-  const int smem = ((2 * g.G - 1) * g.g + 2 * g.G) * 4;
+  const int dots = ((2 * g.G - 1) * g.g + 2 * g.G) * 4;
+  const int staged = g.b * (g.D * 2 + 16) + dots;
+  const bool stage = staged <= 200 * 1024;  // else keys from global memory (b = 1024, or d = 256 at b = 512)
+  const int smem = stage ? staged : dots;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kern<<<(int)ctas, kRecThreads, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),
                                                 static_cast<const __nv_bfloat16*>(k), S);
   };
-  if (g.D == 128) go(k_s1_ragged_fixup<128>);
-  else if (g.D == 256) go(k_s1_ragged_fixup<256>);
+  if (g.D == 128) stage ? go(k_s1_ragged_fixup<128, true>) : go(k_s1_ragged_fixup<128, false>);
+  else if (g.D == 256) stage ? go(k_s1_ragged_fixup<256, true>) : go(k_s1_ragged_fixup<256, false>);
   else return -1;
   count_launch();
   return (int)cudaGetLastError();

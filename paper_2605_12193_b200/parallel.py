@@ -90,7 +90,8 @@ class PeerHeadOutput:
     which every rank's buffer holds the whole layer.  Raises if symmetric memory is unavailable (the
     caller then falls back to HeadShardedOutput + NCCL)."""
 
-    def __init__(self, B: int, Hq: int, N: int, d: int, world: int, rank: int, device, group=None):
+    def __init__(self, B: int, Hq: int, N: int, d: int, world: int, rank: int, device, group=None,
+                 multicast: bool = False):
         import torch.distributed._symmetric_memory as symm
 
         if Hq % world:
@@ -107,6 +108,15 @@ class PeerHeadOutput:
         if off < 0:
             raise RuntimeError("symmetric buffer does not start at the tensor")
         self.mirrors = mirror_addresses(self.hdl.buffer_ptrs, rank, off)
+        # NVLS (multicast=True): one multimem.st per 16 bytes through the buffer's multicast address
+        # reaches every rank's buffer (the switch replicates it) instead of one P2P store per peer
+        self.multicast_o = 0
+        if multicast:
+            mc = int(getattr(self.hdl, "multicast_ptr", 0) or 0)
+            if not mc:
+                raise RuntimeError("no NVLS multicast address for this symmetric buffer")
+            self.multicast_o = mc + off
+            self.mirrors = []
         perm = self.store.permute(1, 0, 2, 3, 4)
         self.full = perm.reshape(B, Hq, N, d) if B == 1 else perm
 

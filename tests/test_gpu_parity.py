@@ -661,12 +661,12 @@ def test_chunked_prefill_tensor_core_stage1(paged):
     dict(B=1, Hq=4, Hkv=2, Nq=3001, Nkv=9001, d=128),     # ragged chunk over a ragged context (N_c = 6000)
     dict(B=1, Hq=4, Hkv=2, Nq=4100, Nkv=4100, d=256),     # d = 256, partial group of 4 tokens
 ])
-def test_ragged_tensor_core_stage1(case):
+def test_ragged_tensor_core_stage1(case, b=256):
     """§8 f1 performance path: ragged N (n mod g != 0) takes the tensor-core Stage 1 (scores over full
     groups, canonical rewrite of the partial group's row and column), bit-exact against the oracle and
     against the all-canonical path, with more launches than the canonical chain (proof it ran)."""
-    prob = workloads.structured(23, block=256, **case)
-    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.1, seed=9)
+    prob = workloads.structured(23, block=b, **case)
+    cfg = bf.Config(b=b, g=64, gamma=0.95, eta=16, rho=0.1, seed=9)
     n0 = bf.kernel_launches()
     fast = run_gpu(prob, cfg, lse=False)
     n_fast = bf.kernel_launches() - n0
@@ -836,5 +836,25 @@ def test_peer_head_output_symmetric_memory_single_rank():
         hout.finish()
         torch.cuda.synchronize()
         assert torch.equal(hout.full, o_ref)
+        # NVLS: the same through the buffer's multicast address (multimem.st), when the node has one
+        try:
+            hmc = parallel.PeerHeadOutput(1, 8, 3072, 128, 1, 0, q.device, multicast=True)
+        except Exception as e:  # noqa: BLE001
+            print(f"NVLS multicast unavailable on this node: {e}")
+            return
+        hmc.local.zero_()
+        scratch = torch.zeros_like(q)  # local O of the call; the multicast stores fill hmc's buffer
+        Pm = bf.make_problem(q, k, v, scratch)
+        bf.bfla_sparse_prefill_mirrored(Pm, cfg, m, [], ws=ws, multicast_o=hmc.multicast_o)
+        hmc.finish()
+        torch.cuda.synchronize()
+        assert torch.equal(scratch, o_ref) and torch.equal(hmc.full, o_ref)
     finally:
         dist.destroy_process_group()
+
+
+def test_ragged_tensor_core_stage1_large_blocks():
+    """Ragged N at b = 1024 (G = 16: the partial-group fixup reads keys from global memory, the block does
+    not fit the staged layout) and d = 256 at b = 512 (same), bit-exact as above."""
+    test_ragged_tensor_core_stage1(dict(B=1, Hq=4, Hkv=2, Nq=5000, Nkv=5000, d=128), b=1024)
+    test_ragged_tensor_core_stage1(dict(B=1, Hq=4, Hkv=2, Nq=3100, Nkv=3100, d=256), b=512)
