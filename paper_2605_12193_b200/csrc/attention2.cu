@@ -58,7 +58,6 @@ constexpr int BN = 64;    // mask tile T
 constexpr int RS = 128;   // K/V rows per ring slot (two tiles)
 // lazy-rescale headroom (log2 units): p = 2^(x - m_run) <= 2^24; O <= 2^24 * N_kv * |V| << fp32 max
 constexpr float kLazy = 24.0f;
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int NQT, bool PAGED = false, int SPLIT = 1>
 struct Cfg2 {

@@ -11,6 +11,7 @@
 // rows it cannot certify are recomputed here in the canonical order (k_s1_recompute_rows).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -467,25 +468,29 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
   // (STAGE = false, blocks too large for smem: keys are read from global memory / L1 instead)
   float* tokdot = reinterpret_cast<float*>(fx + (STAGE ? (size_t)g.b * PITCH : 0));  // [2G - 1][g], then [2G - 1]
   const int per = g.Lkv + g.Lq;
-  const int idx = blockIdx.x % per, rh = blockIdx.x / per;
+  // grid-stride over every (r, h, unit): most units of a varlen batch are dead (no partial group, not
+  // causal) and skipping them in a loop costs far less than launching a CTA for each
+  const long long total = (long long)g.B * g.Hkv * per;
+  for (long long unit = blockIdx.x; unit < total; unit += gridDim.x) {
+  const int idx = (int)(unit % per), rh = (int)(unit / per);
   const int h = rh % g.Hkv, r = rh / g.Hkv;
   const Req R = req_of(g, r);
   const bool qrag = R.Nq % g.g != 0, krag = R.Nkv % g.g != 0;
   int i, j;
   if (idx < g.Lkv) {
-    if (!qrag) return;
+    if (!qrag) continue;
     i = R.Lq - 1;
     j = idx;
   } else {
-    if (!krag) return;
+    if (!krag) continue;
     i = idx - g.Lkv;
     j = R.Lkv - 1;
-    if (qrag && i == R.Lq - 1) return;  // the row units cover it
+    if (qrag && i == R.Lq - 1) continue;  // the row units cover it
   }
-  if (i >= R.Lq || j >= R.Lkv) return;
+  if (i >= R.Lq || j >= R.Lkv) continue;
   long long e_i = (long long)R.Nc + (long long)(i + 1) * g.b - 1;
   if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
-  if ((long long)j * g.b > e_i) return;  // Eq. 11-13: not causal
+  if ((long long)j * g.b > e_i) continue;  // Eq. 11-13: not causal
   const int G = g.G, gg = g.g;
   // partial groups of this unit: u_p = full groups before the tail of the last query block (-1: none)
   const int up = (qrag && i == R.Lq - 1) ? (R.Nq - i * g.b) / gg : -1;
@@ -551,7 +556,8 @@ __global__ void __launch_bounds__(kRecThreads) k_s1_ragged_fixup(Geom g, const _
     for (int pi = 0; pi < npair; ++pi) mx = fmaxf(mx, pairtot[pi]);  // Eq. 10
     *s = mx;
   }
-  __syncthreads();  // tokdot / pairtot reused by the next query head
+  __syncthreads();  // tokdot / pairtot reused by the next query head (and the key block by the next unit)
+  }
   }
 }
 
@@ -1007,15 +1013,18 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
 }
 
 int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st) {
-  const long long ctas = (long long)g.B * g.Hkv * (g.Lkv + g.Lq);
+  const long long units = (long long)g.B * g.Hkv * (g.Lkv + g.Lq);
   const int dots = ((2 * g.G - 1) * g.g + 2 * g.G) * 4;
   const int staged = g.b * (g.D * 2 + 16) + dots;
   const bool stage = staged <= 200 * 1024;  // else keys from global memory (b = 1024, or d = 256 at b = 512)
   const int smem = stage ? staged : dots;
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<(int)ctas, kRecThreads, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),
-                                                static_cast<const __nv_bfloat16*>(k), S);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRecThreads, smem);
+    const long long grid = std::min<long long>(units, (long long)148 * (per_sm > 0 ? per_sm : 1));
+    kern<<<(int)grid, kRecThreads, smem, st>>>(g, static_cast<const __nv_bfloat16*>(q),
+                                               static_cast<const __nv_bfloat16*>(k), S);
   };
   if (g.D == 128) stage ? go(k_s1_ragged_fixup<128, true>) : go(k_s1_ragged_fixup<128, false>);
   else if (g.D == 256) stage ? go(k_s1_ragged_fixup<256, true>) : go(k_s1_ragged_fixup<256, false>);

@@ -42,5 +42,5 @@ for _ in range(a.reps):
     ts.append(e0.elapsed_time(e1))
 ts.sort()
 st = m.stats_dict()
-print(f"env={ {k: v for k, v in os.environ.items() if k.startswith('BFLA_')} } n={a.n} ratio={a.ratio} block_mask ms: median "
+print(f"variant={a.variant or 'product'} env={ {k: v for k, v in os.environ.items() if k.startswith('BFLA_')} } n={a.n} ratio={a.ratio} block_mask ms: median "
       f"{ts[len(ts) // 2]:.4f} min {ts[0]:.4f}  flagged {st['rows_flagged']} recomputed {st['rows_recomputed']}")
