@@ -145,12 +145,19 @@ def layer_timing(name, dev, reps=3, dense_reps=2, tile=64):
 
     import paper_2605_12193_b200 as bf
 
+    import workloads
+
     w = dict(WORKLOADS[name], T=tile)
     prob = make_inputs(w, 303, dev)
     q, k, v = prob.q, prob.k, prob.v
     o = torch.empty_like(q)
     cfg = bf.Config(b=w["b"], g=w["g"], T=w["T"], gamma=w["gamma"], n_local=w["n_local"], eta=w["eta"], rho=w["rho"])
-    P = bf.make_problem(q, k, v, o)
+    if w["paged"]:  # vLLM layout [pages, page_size, h_kv, d] + a seeded page table (Qwen config)
+        kc, vc, pt = workloads.paged(k, v, w["paged"], seed=404)
+        del k, v
+        P = bf.make_problem(q, kc, vc, o, page_table=pt, n_kv=w["N"])
+    else:
+        P = bf.make_problem(q, k, v, o)
     ws = bf.alloc_workspace(P, cfg)
     m = bf.alloc_mask(P, cfg)
     st = torch.cuda.current_stream()
@@ -188,7 +195,7 @@ def layer_timing(name, dev, reps=3, dense_reps=2, tile=64):
            "dense_roofline_frac": 4.0 * w["d"] * w["Hq"] * N * (N + 1) / 2 / (dense_ms * 1e-3) / 1e12 / peaks["bf16"],
            "stage1_roofline": stage1_roofline(w, s1, peaks), "rows_flagged": stats["rows_flagged"],
            "timing": f"CUDA events, median of {reps} eager layers after 2 warm-ups; dense mean of {dense_reps}"}
-    del prob, q, k, v, o, ws, m, wsd
+    del prob, q, o, ws, m, wsd, P
     torch.cuda.empty_cache()
     return out
 
@@ -582,6 +589,9 @@ def run_ours(args, w, rank, world, local_rank):
         extra["llama8b_128k"] = layer_timing("llama8b-128k", dev)
     if world == 1 and args.extra_128k and not w["paged"]:
         extra["varlen_mix"] = varlen_timing(dev)
+        # the other BASELINE.json configs, so every round's driver run sees them (not only builder runs)
+        extra["qwen32b_64k_paged"] = layer_timing("qwen32b-64k-paged", dev, reps=3, dense_reps=1)
+        extra["gemma_d256_32k"] = layer_timing("gemma-d256-32k", dev, reps=3, dense_reps=1)
     n1_ms = None
     if heads:  # the same (unsharded) layer on one GPU, for the driver's strong-scaling efficiency
         if rank == 0:

@@ -530,6 +530,21 @@ def test_row_slices_compose_to_full_prefill(case):
         bf.bfla_sparse_prefill_rows(Ps, cfg, m, a, b_, ws)
     torch.cuda.synchronize()
     assert torch.equal(o_s, o_full) and torch.equal(l_s, l_full)
+    # the composed slices against the CPU oracle itself (masks from the oracle, fp64 Eq. 27): every
+    # slice boundary row plus a sample of the rest, all heads
+    ref = oracle_masks(prob, cfg)
+    labels = np.stack([x["labels"] for x in ref])
+    assert np.array_equal(m.tile_dense().cpu().numpy(), (labels > 0).astype(np.uint8))
+    rows_t = sorted({min(N - 1, i * 64 + off) for i in range(0, -(-N // 64), 5) for off in (0, 63)}
+                    | {min(N - 1, (Tq - 1 - (bb % Tq)) * 64) for bb in bounds[1:-1]})
+    for r in range(B):
+        rows = np.array([[p_, t] for p_ in range(Hq) for t in rows_t], np.int32)
+        (o_ref, lse_ref), = oracle_attention(workloads.Problem(prob.q[r:r + 1], prob.k[r:r + 1], prob.v[r:r + 1]),
+                                             labels[r:r + 1], 64, rows_per_req=[rows])
+        og = o_s[r].float().cpu().numpy()[rows[:, 0], rows[:, 1]].astype(np.float64)
+        err = np.abs(og - o_ref)
+        assert err.max() <= 2e-2 and err.mean() <= 2e-3, (err.max(), err.mean())
+        assert np.abs(l_s[r].cpu().numpy()[rows[:, 0], rows[:, 1]] - lse_ref).max() <= 1e-3
 
     # one slice alone: exactly its rows
     a, b_ = bounds[1], bounds[2]

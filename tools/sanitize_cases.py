@@ -15,15 +15,15 @@ import workloads  # noqa: E402
 SLACK = 50.0  # bfla_config.certify_slack: widen tau so rows are flagged and the recompute kernels run
 
 
-def run(prob, cfg, paged=0, slices=0):
+def run(prob, cfg, paged=0, slices=0, mirrors=0, seqlens=None):
     q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
-    o = torch.empty_like(q)
-    lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    o = torch.zeros_like(q)
+    lse = torch.zeros(q.shape[:3], dtype=torch.float32, device="cuda")
     if paged:
         kc, vc, pt = workloads.paged(k, v, paged, seed=3, extra_pages=3)
         P = bf.make_problem(q, kc, vc, o, lse, page_table=pt, n_kv=k.shape[2])
     else:
-        P = bf.make_problem(q, k, v, o, lse)
+        P = bf.make_problem(q, k, v, o, lse, seqlens=seqlens)
     if cfg is None:
         bf.bfla_prefill(P, None, None, None)
     else:
@@ -35,6 +35,12 @@ def run(prob, cfg, paged=0, slices=0):
             bounds = bf.bfla_balance_rows(m.tile_count.cpu(), slices)
             for a, b in zip(bounds[:-1], bounds[1:]):
                 bf.bfla_sparse_prefill_rows(P, cfg, m, a, b, ws)
+        elif mirrors:  # fused exchange: every O / LSE row also stored into `mirrors` buffers
+            mo = [torch.zeros_like(q) for _ in range(mirrors)]
+            ml = [torch.zeros_like(lse) for _ in range(mirrors)]
+            bf.bfla_sparse_prefill_mirrored(P, cfg, m, mo, ml, ws=ws)
+            torch.cuda.synchronize()
+            assert all(torch.equal(x, o) for x in mo) and all(torch.equal(x, lse) for x in ml)
         else:
             bf.bfla_sparse_prefill(P, cfg, m, ws)
     torch.cuda.synchronize()
@@ -59,8 +65,28 @@ def main():
         ("row slices (5-way balanced), d=256",
          workloads.gaussian(8, B=2, Hq=4, Hkv=2, Nq=1000, Nkv=1000, d=256, sigma=0.8), bf.Config(b=256, g=64), 0, 5),
     ]
+    # round 2: tensor-core Stage 1 on ragged N / varlen (+ partial-group fixup), G = 16, g = 1 (any-G
+    # canonical kernel), and the mirrored (fused-exchange) epilogues of both attention kernels
+    vq = workloads.gaussian(9, B=3, Hq=4, Hkv=2, Nq=1500, Nkv=2600, d=128, sigma=0.8)
+    vl = torch.tensor([[1500, 2600], [700, 700], [1100, 1900]], dtype=torch.int32, device="cuda")
+    cases += [
+        ("ragged tc + fixup", workloads.gaussian(10, B=1, Hq=8, Hkv=2, Nq=2100, Nkv=2100, d=128, sigma=0.8),
+         bf.Config(b=256, g=64, eta=4, certify_slack=SLACK), 0, 0),
+        ("G=16 (b=1024)", workloads.gaussian(11, B=1, Hq=4, Hkv=2, Nq=3000, Nkv=3000, d=128, sigma=0.8),
+         bf.Config(b=1024, g=64), 0, 0),
+        ("g=1 any-G canonical", workloads.gaussian(12, B=1, Hq=2, Hkv=1, Nq=600, Nkv=600, d=128, sigma=0.6),
+         bf.Config(b=64, g=1), 0, 0),
+    ]
     for name, prob, cfg, paged, slices in cases:
         o = run(prob, cfg, paged, slices)
+        print(f"{name}: ok, |O| max {o.float().abs().max().item():.3f}", flush=True)
+    for name, prob, cfg, kw in [
+        ("varlen tc + fixup", vq, bf.Config(b=256, g=64, certify_slack=SLACK), dict(seqlens=vl)),
+        ("mirrored d=128 (TMA epilogue)", g1, bf.Config(b=256, g=64), dict(mirrors=2)),
+        ("mirrored d=256 (thread stores)", workloads.gaussian(13, B=1, Hq=4, Hkv=2, Nq=1024, Nkv=1024, d=256,
+                                                              sigma=0.8), bf.Config(b=256, g=64), dict(mirrors=2)),
+    ]:
+        o = run(prob, cfg, **kw)
         print(f"{name}: ok, |O| max {o.float().abs().max().item():.3f}", flush=True)
 
 
