@@ -9,11 +9,19 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: named ranges for nsys / ncu --nvtx, no link dependency
+
 #include "../../include/bfla.h"
 #include "common.cuh"
 #include "kernels.h"
 
 namespace bfla {
+
+// One NVTX range per entry point (host-side enqueue span; the kernels it launches nest under it in nsys)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -483,6 +491,7 @@ int64_t bfla_tile_list_capacity(const bfla_problem* problem, const bfla_config* 
 
 bfla_status bfla_block_mask(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
                             size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_block_mask");
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
@@ -494,6 +503,7 @@ bfla_status bfla_block_mask(const bfla_problem* problem, const bfla_config* conf
 
 bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
                                size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_expand_rescue");
   (void)ws;
   (void)ws_bytes;
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
@@ -506,6 +516,7 @@ bfla_status bfla_expand_rescue(const bfla_problem* problem, const bfla_config* c
 
 bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                 void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_sparse_prefill");
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
@@ -520,6 +531,7 @@ bfla_status bfla_sparse_prefill(const bfla_problem* problem, const bfla_config* 
 
 bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                      int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_sparse_prefill_rows");
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
@@ -541,6 +553,7 @@ bfla_status bfla_sparse_prefill_rows(const bfla_problem* problem, const bfla_con
 bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
                                          int64_t row_begin, int64_t row_end, const bfla_mirrors* mirrors, void* ws,
                                          size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_sparse_prefill_mirrored");
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
@@ -638,6 +651,7 @@ bfla_status bfla_balance_rows(const int32_t* tile_count, int32_t batch, int32_t 
 
 bfla_status bfla_prefill(const bfla_problem* problem, const bfla_config* config, bfla_mask* mask, void* ws,
                          size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("bfla_prefill");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Geom g;
   bfla_status s = make_geom(problem, config, &g);
