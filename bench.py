@@ -285,6 +285,9 @@ def make_head_output(args, B, Hq, N, d, world, rank, dev):
     NCCL all-gather (`--exchange nccl`, or the fallback)."""
     from paper_2605_12193_b200 import parallel
 
+    if getattr(args, "force_nccl", False):  # the fused exchange failed its self-check on this node
+        args.exchange_used = "nccl"
+        return parallel.HeadShardedOutput(B, Hq, N, d, world, rank, dev)
     if args.exchange in ("auto", "nvls"):
         try:
             out = parallel.PeerHeadOutput(B, Hq, N, d, world, rank, dev, multicast=True)
@@ -389,6 +392,25 @@ def run_ours(args, w, rank, world, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if heads and hasattr(hout, "mirrors"):
+        # self-check of the fused exchange on this node: the layer every rank assembled through the
+        # epilogue stores must equal the NCCL all-gather of the ranks' own chunks; otherwise fall back to
+        # the all-gather for the timed run (and say so in the line)
+        ref = parallel.HeadShardedOutput(1, w["Hq"], N, d, world, rank, dev)
+        ref.local.copy_(hout.local)
+        ref.gather()
+        ok = torch.tensor([1 if torch.equal(ref.full, hout.full) else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        args.exchange_verified = bool(ok.item())
+        if not args.exchange_verified:
+            args.exchange_fallback = f"{args.exchange_used}: assembled O differs from the NCCL all-gather"
+            args.exchange_used = "nccl"
+            args.force_nccl = True
+            hout = ref
+            P = bf.make_problem(q, k, v, hout.local, head_offset=head_offset)
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
     stats = m.stats_dict()
     kappa = stats["kept_tiles"] / max(1, stats["causal_tiles"])
 
@@ -724,7 +746,8 @@ def main():
                           "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
                           "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic", "config": config,
                           "impl": "reference", "cpu_baseline": cb,
-                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
         return
 
     import torch
@@ -780,6 +803,8 @@ def main():
             }.get(getattr(args, "exchange_used", ""), "NCCL in-place all-gather after the prefill")
             if getattr(args, "exchange_fallback", None):
                 line["config"]["exchange_fallback"] = args.exchange_fallback
+            if hasattr(args, "exchange_verified"):
+                line["config"]["exchange_verified_vs_nccl"] = args.exchange_verified
         if world > 1:
             mg = {"rank_ms_per_step": r["rank_ms"], "max_over_ranks_ms": max(r["rank_ms"]),
                   "min_over_ranks_ms": min(r["rank_ms"])}
@@ -801,7 +826,7 @@ def main():
             line["multi_gpu"] = mg
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(w)
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
 
