@@ -229,6 +229,29 @@ bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla
                                          const bfla_mask* mask, int64_t row_begin, int64_t row_end,
                                          const bfla_mirrors* mirrors, void* ws, size_t ws_bytes, void* stream);
 
+/* Split-KV (a row too long for one GPU or one SM): the sparse prefill restricted to the kept
+   tiles j (mask tile index, T units) in [kv_tile_begin, kv_tile_end) of every row — Eq. 27 over that
+   subset of the row's kept tiles; a row with none writes O = 0 and LSE = -inf.  problem->lse is required
+   (the merge needs it).  Errors as bfla_sparse_prefill, plus BFLA_ERR_INVALID_ARGUMENT unless
+   0 <= kv_tile_begin <= kv_tile_end, or if problem->lse is NULL. */
+bfla_status bfla_sparse_prefill_kvrange(const bfla_problem* problem, const bfla_config* config,
+                                        const bfla_mask* mask, int64_t kv_tile_begin, int64_t kv_tile_end,
+                                        void* ws, size_t ws_bytes, void* stream);
+/* Merge of KV-range partials: for every row, with M = max_k LSE_k and w_k = exp(LSE_k - M),
+   O = sum_k w_k O_k / sum_k w_k and LSE = M + log(sum_k w_k) — the online softmax of Eq. 27 over the
+   union of the ranges (exact up to the bf16 rounding of each O_k).  parts->o[k] / parts->lse[k]: device
+   buffers with problem->o / problem->lse's layout (ranges that do not overlap, e.g. from
+   bfla_sparse_prefill_kvrange).  Writes problem->o and, if not NULL, problem->lse; q/k/v are not read
+   (but must be valid pointers).  Errors: BFLA_ERR_INVALID_ARGUMENT for n outside [1, BFLA_MAX_PARTS]
+   or a NULL part; BFLA_ERR_MISALIGNED for parts not 16-byte aligned. */
+#define BFLA_MAX_PARTS 8
+typedef struct {
+    int32_t n;
+    const void* o[BFLA_MAX_PARTS];
+    const float* lse[BFLA_MAX_PARTS];
+} bfla_partials;
+bfla_status bfla_merge_partials(const bfla_problem* problem, const bfla_partials* parts, void* stream);
+
 /* Host-only (no GPU, no CUDA call): cost-balanced contiguous partition of the LPT row order into
    `parts` slices for bfla_sparse_prefill_rows (§8 f2: per-head kappa differs, so equal head counts per
    GPU are not equal work; P:443 runs 8 GPUs without naming a scheme).  tile_count is a HOST copy of

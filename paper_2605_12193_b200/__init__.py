@@ -19,7 +19,7 @@ from ._lib import (KV_CONTIGUOUS, KV_PAGED, MASK_PER_KV_HEAD, MASK_PER_Q_HEAD, P
                    SCORES_CANONICAL, SELECT_MASS, SELECT_RATIO, bfla_config,
                    bfla_mask, bfla_problem, bfla_stats, check, lib)
 
-__all__ = ["bfla_sparse_prefill_mirrored", "Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
+__all__ = ["bfla_sparse_prefill_mirrored", "bfla_sparse_prefill_kvrange", "bfla_merge_partials", "Config", "Problem", "Mask", "make_problem", "alloc_mask", "alloc_workspace", "bfla_workspace_size",
            "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue", "bfla_sparse_prefill",
            "bfla_sparse_prefill_rows", "bfla_balance_rows", "bfla_prefill", "prefill", "kernel_launches", "POOL_FLATTEN", "POOL_MEAN", "SELECT_MASS", "SELECT_RATIO", "SCORES_AUTO",
            "SCORES_CANONICAL", "MASK_PER_KV_HEAD", "MASK_PER_Q_HEAD"]
@@ -253,6 +253,28 @@ def bfla_sparse_prefill_mirrored(problem: Problem, cfg: Config, mask: Mask, mirr
                                              int(rows[0]), int(rows[1]), ctypes.byref(mc), _ptr(ws),
                                              0 if ws is None else ws.numel(), _stream(stream)),
           "bfla_sparse_prefill_mirrored")
+
+
+def bfla_sparse_prefill_kvrange(problem: Problem, cfg: Config, mask: Mask, kv_begin: int, kv_end: int,
+                                ws: Optional[torch.Tensor] = None, stream=None) -> None:
+    """Split-KV partial: the sparse prefill over the kept tiles j in [kv_begin, kv_end) (mask tiles) only;
+    writes the range's normalised O and its LSE (problem must carry an LSE buffer)."""
+    m = mask.c()
+    check(lib().bfla_sparse_prefill_kvrange(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
+                                            int(kv_begin), int(kv_end), _ptr(ws), 0 if ws is None else ws.numel(),
+                                            _stream(stream)), "bfla_sparse_prefill_kvrange")
+
+
+def bfla_merge_partials(problem: Problem, o_parts, lse_parts, stream=None) -> None:
+    """O / LSE of problem from KV-range partials (tensors with O's / LSE's layout)."""
+    if len(o_parts) != len(lse_parts) or not 1 <= len(o_parts) <= _lib.MAX_PARTS:
+        raise ValueError(f"1..{_lib.MAX_PARTS} (O, LSE) partial pairs")
+    pc = _lib.bfla_partials()
+    pc.n = len(o_parts)
+    for k, (o, l) in enumerate(zip(o_parts, lse_parts)):
+        pc.o[k], pc.lse[k] = o.data_ptr(), l.data_ptr()
+    check(lib().bfla_merge_partials(ctypes.byref(problem.c), ctypes.byref(pc), _stream(stream)),
+          "bfla_merge_partials")
 
 
 def bfla_balance_rows(tile_count, parts: int, row_overhead: int = 3) -> list[int]:

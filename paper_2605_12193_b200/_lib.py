@@ -70,10 +70,18 @@ class bfla_mirrors(ctypes.Structure):
                 ("multicast_lse", vp)]
 
 
+MAX_PARTS = 8
+
+
+class bfla_partials(ctypes.Structure):
+    _fields_ = [("n", i32), ("o", vp * MAX_PARTS), ("lse", vp * MAX_PARTS)]
+
+
 _lib = None
 
 ENTRY_POINTS = ["bfla_workspace_size", "bfla_tile_list_capacity", "bfla_block_mask", "bfla_expand_rescue",
                 "bfla_sparse_prefill", "bfla_sparse_prefill_rows", "bfla_sparse_prefill_mirrored",
+                "bfla_sparse_prefill_kvrange", "bfla_merge_partials",
                 "bfla_balance_rows", "bfla_prefill",
                 "bfla_status_string", "bfla_last_error",
                 "bfla_kernel_launches"]
@@ -102,6 +110,11 @@ def lib():
         L.bfla_sparse_prefill_mirrored.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64,
                                                    P(bfla_mirrors), vp, ctypes.c_size_t, vp]
         L.bfla_sparse_prefill_mirrored.restype = ctypes.c_int
+        L.bfla_sparse_prefill_kvrange.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64, vp,
+                                                  ctypes.c_size_t, vp]
+        L.bfla_sparse_prefill_kvrange.restype = ctypes.c_int
+        L.bfla_merge_partials.argtypes = [P(bfla_problem), P(bfla_partials), vp]
+        L.bfla_merge_partials.restype = ctypes.c_int
         L.bfla_balance_rows.argtypes = [P(i32), i32, i32, i32, i32, i32, P(i64)]
         L.bfla_balance_rows.restype = ctypes.c_int
         L.bfla_status_string.argtypes = [ctypes.c_int]

@@ -27,6 +27,7 @@ UNITS = {
     "stage2.cu": [],
     "attention.cu": [],
     "attention2.cu": [],
+    "merge.cu": [],
 }
 
 

@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/bfla.h: validation, geometry, workspace carving, TMA descriptor
 // encoding and kernel launches.  No allocation, no device synchronisation, no global mutable
 // state beyond the thread-local error detail and a launch counter.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -592,6 +593,48 @@ bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla
   int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
                                                 : nullptr;
   return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
+}
+
+bfla_status bfla_sparse_prefill_kvrange(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
+                                        int64_t kv_tile_begin, int64_t kv_tile_end, void* ws, size_t ws_bytes,
+                                        void* stream) {
+  NvtxRange nvtx_("bfla_sparse_prefill_kvrange");
+  if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
+  Geom g;
+  bfla_status s = make_geom(problem, config, &g);
+  if (s != BFLA_OK) return s;
+  if (!mask || !mask->tile_list || !mask->tile_count) return fail(BFLA_ERR_INVALID_ARGUMENT, "mask lists are NULL");
+  if (!problem->lse) return fail(BFLA_ERR_INVALID_ARGUMENT, "split-KV partials need problem->lse");
+  if (kv_tile_begin < 0 || kv_tile_end < kv_tile_begin)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "kv tile range [%lld, %lld)", (long long)kv_tile_begin,
+                (long long)kv_tile_end);
+  g.kv_range = 1;
+  g.kv_lo = (int)std::min<int64_t>(kv_tile_begin, (int64_t)g.Tkv);
+  g.kv_hi = (int)std::min<int64_t>(kv_tile_end, (int64_t)g.Tkv);
+  const WsLayout L = ws_layout(g);
+  int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
+                                                : nullptr;
+  return run_attention(g, problem, mask->tile_list, mask->tile_count, 0, static_cast<cudaStream_t>(stream), sched);
+}
+
+bfla_status bfla_merge_partials(const bfla_problem* problem, const bfla_partials* parts, void* stream) {
+  NvtxRange nvtx_("bfla_merge_partials");
+  Geom g;
+  bfla_status s = make_geom(problem, nullptr, &g);
+  if (s != BFLA_OK) return s;
+  if (!parts || parts->n < 1 || parts->n > BFLA_MAX_PARTS)
+    return fail(BFLA_ERR_INVALID_ARGUMENT, "parts->n outside [1, %d]", BFLA_MAX_PARTS);
+  MergeParts mp;
+  mp.n = parts->n;
+  for (int k = 0; k < parts->n; ++k) {
+    if (!parts->o[k] || !parts->lse[k]) return fail(BFLA_ERR_INVALID_ARGUMENT, "part %d is NULL", k);
+    if ((uintptr_t)parts->o[k] % 16) return fail(BFLA_ERR_MISALIGNED, "part %d O not 16-byte aligned", k);
+    mp.o[k] = parts->o[k];
+    mp.lse[k] = parts->lse[k];
+  }
+  if (launch_merge_partials(g, mp, problem->o, problem->lse, static_cast<cudaStream_t>(stream)))
+    return cuda_check("bfla_merge_partials launch");
+  return cuda_check("bfla_merge_partials launch");
 }
 
 bfla_status bfla_balance_rows(const int32_t* tile_count, int32_t batch, int32_t h_kv, int32_t tq, int32_t row_overhead,

@@ -189,10 +189,17 @@ __global__ void __launch_bounds__(Cfg2<NQT, PAGED>::THREADS, 1)
     const Req R = req_of(g, it.r);
     if (it.i >= R.Tq) return 0;  // padding query tile of a shorter request (varlen): no work
     if (DENSE) return (int)req_row_count(R, g.T, it.i) * TR;
-    return count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i] * TR;
+    const int n = count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i];
+    if (!g.kv_range) return n * TR;
+    // split-KV: only the row's kept tiles inside [kv_lo, kv_hi) (the list is ascending in j)
+    const int32_t* l = list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(R, g.T, it.i);
+    return (list_lower_bound(l, n, g.kv_hi) - list_lower_bound(l, n, g.kv_lo)) * TR;
   };
   auto row_list = [&](const Item& it) -> const int32_t* {
-    return list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
+    const int32_t* l =
+        list + ((long long)it.r * g.Hkv + it.h) * g.causal_per_head + req_row_offset(req_of(g, it.r), g.T, it.i);
+    if (!g.kv_range) return l;
+    return l + list_lower_bound(l, count[((long long)it.r * g.Hkv + it.h) * g.Tq + it.i], g.kv_lo);
   };
   // tiles are visited in DESCENDING j (diagonal / local band first): the largest scores usually sit
   // near the diagonal, so the running max settles on the first step and the lazy-max fast path holds

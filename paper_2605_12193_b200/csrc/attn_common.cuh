@@ -9,6 +9,17 @@ struct Item {
   int r, h, c, i;
 };
 
+// split-KV: first index of an ascending kept-tile list (n entries) whose tile is >= x
+__device__ __forceinline__ int list_lower_bound(const int32_t* l, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(l + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ float max3f(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

@@ -56,6 +56,8 @@ struct Geom {
   // NVLS multicast addresses of O / LSE (multimem.st reaches every member GPU's buffer); NULL = unused
   void* mco;
   float* mcl;
+  // split-KV (bfla_sparse_prefill_kvrange): only kept tiles j (mask tile units) in [kv_lo, kv_hi)
+  int kv_range, kv_lo, kv_hi;
 };
 
 // multimem stores (NVLS): 16 bytes / one fp32 through a multicast address

@@ -46,6 +46,14 @@ void launch_expand_rescue(const Geom& g, const uint32_t* coarse, int n_sink, int
                           uint64_t seed, uint32_t* tile_bits, int32_t* list, int32_t* count, uint8_t* label,
                           unsigned long long* stats, cudaStream_t st);
 
+// split-KV merge (merge.cu): O / LSE of up to 8 KV-range partials, each with the problem's O layout
+struct MergeParts {
+  int n;
+  const void* o[8];
+  const float* lse[8];
+};
+int launch_merge_partials(const Geom& g, const MergeParts& mp, void* o, float* lse, cudaStream_t st);
+
 // Sparse / dense prefill (Eq. 27 / Eq. 1) — tcgen05 + TMEM + TMA.
 struct MirrorMaps {
   CUtensorMap m[7];  // O mirrors as TMA store targets (attention2 epilogue, Geom::n_mirror of them)

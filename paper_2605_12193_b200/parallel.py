@@ -125,6 +125,15 @@ class PeerHeadOutput:
         self.hdl.barrier(channel=0)
 
 
+def split_kv_ranges(tkv: int, parts: int) -> list[tuple[int, int]]:
+    """Split-KV (§8 f2): `parts` contiguous, equal-width KV-tile ranges [a, b) covering [0, tkv) for
+    bfla_sparse_prefill_kvrange; the partials are combined by bfla_merge_partials (LSE merge).  Used
+    when one row is too long for one rank (a diffuse head at 32K): its ranges go to different
+    GPUs or SMs and only (O_k, LSE_k) travel."""
+    edges = [round(k * tkv / parts) for k in range(parts + 1)]
+    return [(edges[k], edges[k + 1]) for k in range(parts)]
+
+
 def request_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     """Request (batch) slice for request-level sharding: requests are fully independent."""
     per = -(-batch // world)

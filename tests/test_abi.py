@@ -44,6 +44,7 @@ def test_struct_layout_matches_header(L, tmp_path):
         "bfla_mask": [f[0] for f in L.bfla_mask._fields_],
         "bfla_stats": [f[0] for f in L.bfla_stats._fields_],
         "bfla_mirrors": [f[0] for f in L.bfla_mirrors._fields_],
+        "bfla_partials": [f[0] for f in L.bfla_partials._fields_],
     }
     lines = ['#include "bfla.h"', "#include <stdio.h>", "#include <stddef.h>", "int main(void){"]
     for s, fs in fields.items():
@@ -152,3 +153,23 @@ def test_mirrored_prefill_validation(L):
     assert so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 0, 0, P(mir), None, 0, None) == 3
     mir.o[0] = 1 << 20
     assert so.bfla_sparse_prefill_mirrored(P(_problem(L)), P(_cfg(L)), P(m), 5, 3, P(mir), None, 0, None) == 1
+
+
+def test_split_kv_validation(L):
+    """Split-KV calls validate on the host: the partial prefill needs an LSE buffer and a sane range, the
+    merge 1..BFLA_MAX_PARTS non-NULL aligned parts."""
+    so = L.lib()
+    P = ctypes.byref
+    m = L.bfla_mask()
+    m.tile_list = m.tile_count = 1 << 20
+    p = _problem(L)
+    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 0, 4, None, 0, None) == 1  # lse is NULL
+    p.lse = 1 << 20
+    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 5, 2, None, 0, None) == 1
+    parts = L.bfla_partials()
+    assert so.bfla_merge_partials(P(p), P(parts), None) == 1  # n = 0
+    parts.n = 2
+    parts.o[0] = parts.lse[0] = 1 << 20
+    assert so.bfla_merge_partials(P(p), P(parts), None) == 1  # part 1 NULL
+    parts.o[1], parts.lse[1] = (1 << 20) + 4, 1 << 20
+    assert so.bfla_merge_partials(P(p), P(parts), None) == 3  # misaligned O

@@ -873,3 +873,46 @@ def test_ragged_tensor_core_stage1_large_blocks():
     not fit the staged layout) and d = 256 at b = 512 (same), bit-exact as above."""
     test_ragged_tensor_core_stage1(dict(B=1, Hq=4, Hkv=2, Nq=5000, Nkv=5000, d=128), b=1024)
     test_ragged_tensor_core_stage1(dict(B=1, Hq=4, Hkv=2, Nq=3100, Nkv=3100, d=256), b=512)
+
+
+@pytest.mark.parametrize("d,parts", [(128, 3), (256, 2), (128, 5)])
+def test_split_kv_partials_merge(d, parts):
+    """§8 f2 split-KV: the sparse prefill restricted to KV-tile ranges (bfla_sparse_prefill_kvrange) and
+    the LSE merge (bfla_merge_partials) reproduce the unsplit O within bf16 rounding and LSE to 1e-5
+    relative, and the oracle within the contract tolerance; rows with no kept tile in a range get
+    LSE = -inf there and still merge exactly."""
+    from paper_2605_12193_b200 import parallel
+
+    prob = workloads.structured(44, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=d, block=256)
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, rho=0.1, seed=7)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o_ref = torch.empty_like(q)
+    l_ref = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    P = bf.make_problem(q, k, v, o_ref, l_ref)
+    ws, m = bf.alloc_workspace(P, cfg), bf.alloc_mask(P, cfg, labels=True)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    ranges = parallel.split_kv_ranges(m.Tkv, parts)
+    o_parts, l_parts = [], []
+    for a, b_ in ranges:
+        o_k = torch.empty_like(q)
+        l_k = torch.empty_like(l_ref)
+        bf.bfla_sparse_prefill_kvrange(bf.make_problem(q, k, v, o_k, l_k), cfg, m, a, b_, ws)
+        o_parts.append(o_k)
+        l_parts.append(l_k)
+    torch.cuda.synchronize()
+    assert any(bool((x == -float("inf")).any()) for x in l_parts)  # some rows have nothing in a range
+    o = torch.empty_like(q)
+    l = torch.empty_like(l_ref)
+    bf.bfla_merge_partials(bf.make_problem(q, k, v, o, l), o_parts, l_parts)
+    torch.cuda.synchronize()
+    err = (o.float() - o_ref.float()).abs()
+    assert err.max().item() <= 1.6e-2 and err.mean().item() <= 1e-3, (err.max().item(), err.mean().item())
+    assert torch.allclose(l, l_ref, rtol=1e-5, atol=1e-5)
+    labels = m.tile_label.cpu().numpy()
+    rows = np.array([[p_, t] for p_ in range(8) for t in range(0, 4096, 37)], np.int32)
+    (o_or, lse_or), = oracle_attention(prob, labels, 64, rows_per_req=[rows])
+    og = o[0].float().cpu().numpy()[rows[:, 0], rows[:, 1]].astype(np.float64)
+    e2 = np.abs(og - o_or)
+    assert e2.max() <= 2e-2 and e2.mean() <= 2e-3, (e2.max(), e2.mean())

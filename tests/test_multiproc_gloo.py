@@ -243,3 +243,15 @@ def test_mirror_addresses_peer_chunks():
         got = parallel.mirror_addresses(bases, rank, rank * chunk)
         assert got == [bases[p] + rank * chunk for p in range(world) if p != rank]
         assert len(got) == world - 1
+
+
+def test_split_kv_ranges_cover():
+    """split_kv_ranges: contiguous, disjoint, covering [0, tkv), widths within one tile of each other."""
+    from paper_2605_12193_b200 import parallel
+
+    for tkv, parts in [(512, 3), (64, 8), (7, 4), (2048, 5)]:
+        rs = parallel.split_kv_ranges(tkv, parts)
+        assert rs[0][0] == 0 and rs[-1][1] == tkv and len(rs) == parts
+        assert all(a[1] == b[0] for a, b in zip(rs[:-1], rs[1:]))
+        w = [b - a for a, b in rs]
+        assert max(w) - min(w) <= 1
