@@ -230,13 +230,15 @@ bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla
                                          const bfla_mirrors* mirrors, void* ws, size_t ws_bytes, void* stream);
 
 /* Split-KV (a row too long for one GPU or one SM): the sparse prefill restricted to the kept
-   tiles j (mask tile index, T units) in [kv_tile_begin, kv_tile_end) of every row — Eq. 27 over that
-   subset of the row's kept tiles; a row with none writes O = 0 and LSE = -inf.  problem->lse is required
-   (the merge needs it).  Errors as bfla_sparse_prefill, plus BFLA_ERR_INVALID_ARGUMENT unless
-   0 <= kv_tile_begin <= kv_tile_end, or if problem->lse is NULL. */
+   tiles j (mask tile index, T units) in [kv_tile_begin, kv_tile_end) — Eq. 27 over that subset of each
+   row's kept tiles; a row with none writes O = 0 and LSE = -inf — over the LPT rows [row_begin, row_end)
+   (0, 0 = every row; bfla_sparse_prefill_rows semantics), so a scheduler can hand out (row slice, KV
+   range) pieces.  problem->lse is required (the merge needs it).  Errors as bfla_sparse_prefill_rows,
+   plus BFLA_ERR_INVALID_ARGUMENT unless 0 <= kv_tile_begin <= kv_tile_end, or if problem->lse is NULL. */
 bfla_status bfla_sparse_prefill_kvrange(const bfla_problem* problem, const bfla_config* config,
                                         const bfla_mask* mask, int64_t kv_tile_begin, int64_t kv_tile_end,
-                                        void* ws, size_t ws_bytes, void* stream);
+                                        int64_t row_begin, int64_t row_end, void* ws, size_t ws_bytes,
+                                        void* stream);
 /* Merge of KV-range partials: for every row, with M = max_k LSE_k and w_k = exp(LSE_k - M),
    O = sum_k w_k O_k / sum_k w_k and LSE = M + log(sum_k w_k) — the online softmax of Eq. 27 over the
    union of the ranges (exact up to the bf16 rounding of each O_k).  parts->o[k] / parts->lse[k]: device

@@ -256,13 +256,16 @@ def bfla_sparse_prefill_mirrored(problem: Problem, cfg: Config, mask: Mask, mirr
 
 
 def bfla_sparse_prefill_kvrange(problem: Problem, cfg: Config, mask: Mask, kv_begin: int, kv_end: int,
-                                ws: Optional[torch.Tensor] = None, stream=None) -> None:
-    """Split-KV partial: the sparse prefill over the kept tiles j in [kv_begin, kv_end) (mask tiles) only;
-    writes the range's normalised O and its LSE (problem must carry an LSE buffer)."""
+                                rows: tuple[int, int] = (0, 0), ws: Optional[torch.Tensor] = None,
+                                stream=None) -> None:
+    """Split-KV partial: the sparse prefill over the kept tiles j in [kv_begin, kv_end) (mask tiles) only,
+    for the LPT rows `rows` ((0, 0) = all); writes the range's normalised O and its LSE (problem must
+    carry an LSE buffer)."""
     m = mask.c()
     check(lib().bfla_sparse_prefill_kvrange(ctypes.byref(problem.c), ctypes.byref(cfg.c()), ctypes.byref(m),
-                                            int(kv_begin), int(kv_end), _ptr(ws), 0 if ws is None else ws.numel(),
-                                            _stream(stream)), "bfla_sparse_prefill_kvrange")
+                                            int(kv_begin), int(kv_end), int(rows[0]), int(rows[1]), _ptr(ws),
+                                            0 if ws is None else ws.numel(), _stream(stream)),
+          "bfla_sparse_prefill_kvrange")
 
 
 def bfla_merge_partials(problem: Problem, o_parts, lse_parts, stream=None) -> None:

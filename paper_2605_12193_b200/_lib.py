@@ -110,8 +110,8 @@ def lib():
         L.bfla_sparse_prefill_mirrored.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64,
                                                    P(bfla_mirrors), vp, ctypes.c_size_t, vp]
         L.bfla_sparse_prefill_mirrored.restype = ctypes.c_int
-        L.bfla_sparse_prefill_kvrange.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64, vp,
-                                                  ctypes.c_size_t, vp]
+        L.bfla_sparse_prefill_kvrange.argtypes = [P(bfla_problem), P(bfla_config), P(bfla_mask), i64, i64, i64, i64,
+                                                  vp, ctypes.c_size_t, vp]
         L.bfla_sparse_prefill_kvrange.restype = ctypes.c_int
         L.bfla_merge_partials.argtypes = [P(bfla_problem), P(bfla_partials), vp]
         L.bfla_merge_partials.restype = ctypes.c_int

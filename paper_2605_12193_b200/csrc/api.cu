@@ -596,8 +596,8 @@ bfla_status bfla_sparse_prefill_mirrored(const bfla_problem* problem, const bfla
 }
 
 bfla_status bfla_sparse_prefill_kvrange(const bfla_problem* problem, const bfla_config* config, const bfla_mask* mask,
-                                        int64_t kv_tile_begin, int64_t kv_tile_end, void* ws, size_t ws_bytes,
-                                        void* stream) {
+                                        int64_t kv_tile_begin, int64_t kv_tile_end, int64_t row_begin,
+                                        int64_t row_end, void* ws, size_t ws_bytes, void* stream) {
   NvtxRange nvtx_("bfla_sparse_prefill_kvrange");
   if (!config) return fail(BFLA_ERR_INVALID_ARGUMENT, "config is NULL");
   Geom g;
@@ -611,6 +611,17 @@ bfla_status bfla_sparse_prefill_kvrange(const bfla_problem* problem, const bfla_
   g.kv_range = 1;
   g.kv_lo = (int)std::min<int64_t>(kv_tile_begin, (int64_t)g.Tkv);
   g.kv_hi = (int)std::min<int64_t>(kv_tile_end, (int64_t)g.Tkv);
+  const int64_t rows = (int64_t)g.B * g.Hkv * g.Tq;
+  if (!(row_begin == 0 && row_end == 0)) {
+    if (row_begin < 0 || row_end < row_begin || row_end > rows)
+      return fail(BFLA_ERR_INVALID_ARGUMENT, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                  (long long)row_end, (long long)rows);
+    if (row_end == row_begin) return BFLA_OK;
+    if (row_begin != 0 || row_end != rows) {
+      g.row0 = (int)row_begin;
+      g.nrows = (int)(row_end - row_begin);
+    }
+  }
   const WsLayout L = ws_layout(g);
   int32_t* sched = (ws && ws_bytes >= L.total) ? reinterpret_cast<int32_t*>(static_cast<unsigned char*>(ws) + L.sched)
                                                 : nullptr;

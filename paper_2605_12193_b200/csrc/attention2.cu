@@ -830,9 +830,11 @@ int launch2_t(const Geom& g, const AttnMaps& maps, const int32_t* list, const in
     count_launch();
     return (int)cudaGetLastError();
   };
-  // pairs e with e mod 8 in {1, 5} (1 in 4) on the FMA pipe: measured best of 0, 1/8, 1/4, 3/8, 1/2
+  // exponential pairs with e mod 8 == 1 (1 in 8) on the FMA pipe.  Round 1 measured 1/4 best of 0, 1/8,
+  // 1/4, 3/8, 1/2; after the split PV issue (round 2, same box, 2 runs each): 0 0.920, 1/8 0.919, 1/4
+  // 0.925, 3/8 0.946 ms sparse 32K; 128K equal within 0.1 % (profiles/r2_s3a_poly_ab.jsonl)
 #ifndef BFLA_POLY_MASK
-#define BFLA_POLY_MASK 0x22
+#define BFLA_POLY_MASK 0x02
 #endif
   constexpr int PM = BFLA_POLY_MASK;
   using C = Cfg2<NQT, PAGED>;

@@ -163,9 +163,10 @@ def test_split_kv_validation(L):
     m = L.bfla_mask()
     m.tile_list = m.tile_count = 1 << 20
     p = _problem(L)
-    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 0, 4, None, 0, None) == 1  # lse is NULL
+    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 0, 4, 0, 0, None, 0, None) == 1  # lse is NULL
     p.lse = 1 << 20
-    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 5, 2, None, 0, None) == 1
+    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 5, 2, 0, 0, None, 0, None) == 1
+    assert so.bfla_sparse_prefill_kvrange(P(p), P(_cfg(L)), P(m), 0, 4, 3, 1, None, 0, None) == 1  # bad rows
     parts = L.bfla_partials()
     assert so.bfla_merge_partials(P(p), P(parts), None) == 1  # n = 0
     parts.n = 2

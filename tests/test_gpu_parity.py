@@ -898,7 +898,7 @@ def test_split_kv_partials_merge(d, parts):
     for a, b_ in ranges:
         o_k = torch.empty_like(q)
         l_k = torch.empty_like(l_ref)
-        bf.bfla_sparse_prefill_kvrange(bf.make_problem(q, k, v, o_k, l_k), cfg, m, a, b_, ws)
+        bf.bfla_sparse_prefill_kvrange(bf.make_problem(q, k, v, o_k, l_k), cfg, m, a, b_, ws=ws)
         o_parts.append(o_k)
         l_parts.append(l_k)
     torch.cuda.synchronize()
@@ -916,3 +916,42 @@ def test_split_kv_partials_merge(d, parts):
     og = o[0].float().cpu().numpy()[rows[:, 0], rows[:, 1]].astype(np.float64)
     e2 = np.abs(og - o_or)
     assert e2.max() <= 2e-2 and e2.mean() <= 2e-3, (e2.max(), e2.mean())
+
+
+def test_split_kv_on_a_row_slice():
+    """(row slice x KV range) pieces — what a scheduler hands out for rows too long for one rank: the
+    pieces of one LPT row slice split into 3 KV ranges merge to the unsplit O on those rows and leave
+    every other row untouched."""
+    from paper_2605_12193_b200 import parallel
+
+    prob = workloads.structured(45, B=1, Hq=8, Hkv=2, Nq=3072, Nkv=3072, d=128, block=256)
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, seed=8)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o_ref = torch.empty_like(q)
+    l_ref = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    P = bf.make_problem(q, k, v, o_ref, l_ref)
+    ws, m = bf.alloc_workspace(P, cfg), bf.alloc_mask(P, cfg)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    Tq = m.Tq
+    rows = (3, Tq + 5)  # tail of head group 0 (its longest rows) and the start of group 1
+    o_parts, l_parts = [], []
+    for a, b_ in parallel.split_kv_ranges(m.Tkv, 3):
+        o_k = torch.zeros_like(q)
+        l_k = torch.full_like(l_ref, -float("inf"))
+        bf.bfla_sparse_prefill_kvrange(bf.make_problem(q, k, v, o_k, l_k), cfg, m, a, b_, rows=rows, ws=ws)
+        o_parts.append(o_k)
+        l_parts.append(l_k)
+    o = torch.zeros_like(q)
+    l = torch.full_like(l_ref, -float("inf"))
+    bf.bfla_merge_partials(bf.make_problem(q, k, v, o, l), o_parts, l_parts)
+    torch.cuda.synchronize()
+    want = torch.zeros(q.shape[:3], dtype=torch.bool, device="cuda")
+    for rho in range(*rows):
+        h, i = rho // Tq, Tq - 1 - rho % Tq
+        want[:, h * 4:(h + 1) * 4, i * 64:(i + 1) * 64] = True
+    err = (o.float() - o_ref.float()).abs()[want]
+    assert err.max().item() <= 1.6e-2 and err.mean().item() <= 1e-3
+    assert torch.allclose(l[want], l_ref[want], rtol=1e-5, atol=1e-5)
+    assert not o[~want].any() and bool((l[~want] == -float("inf")).all())
