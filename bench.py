@@ -310,6 +310,26 @@ def make_head_output(args, B, Hq, N, d, world, rank, dev):
     return parallel.HeadShardedOutput(B, Hq, N, d, world, rank, dev)
 
 
+def make_full_output(args, shape, world, rank, dev):
+    """Balanced mode: a full-layer O in symmetric memory with the fused exchange (nvls / p2p as for
+    make_head_output), or None (the zero-fill + SUM all-reduce path)."""
+    from paper_2605_12193_b200 import parallel
+
+    if world == 1 or args.exchange == "nccl" or getattr(args, "force_nccl", False):
+        return None
+    for mode in (("nvls",) if args.exchange == "nvls" else ("p2p",) if args.exchange == "p2p" else ("nvls", "p2p")):
+        try:
+            out = parallel.PeerFullOutput(shape, world, rank, dev, multicast=mode == "nvls")
+            args.exchange_used = mode
+            return out
+        except Exception as e:  # noqa: BLE001
+            if args.exchange == mode:
+                raise
+            args.exchange_fallback = (getattr(args, "exchange_fallback", "") + f"; {mode}: {type(e).__name__}: {e}")[:300]
+    args.exchange_used = "nccl"
+    return None
+
+
 def exchange(hout):
     if hasattr(hout, "mirrors"):
         hout.finish()
@@ -362,7 +382,11 @@ def run_ours(args, w, rank, world, local_rank):
     ws = bf.alloc_workspace(P, cfg)
     m = bf.alloc_mask(P, cfg)
     if bal:
-        layer = parallel.BalancedLayer(q, k, v, o, cfg, rank, world)
+        peer = make_full_output(args, o.shape, world, rank, dev)
+        if peer is not None:
+            o = peer.o
+            P = bf.make_problem(q, k, v, o, head_offset=head_offset)
+        layer = parallel.BalancedLayer(q, k, v, o, cfg, rank, world, peer_out=peer)
         m = layer.ms  # stats of this rank's head group (Stage 1/2 certification)
     st = torch.cuda.current_stream()
 
@@ -392,6 +416,28 @@ def run_ours(args, w, rank, world, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if bal and layer.peer_out is not None:
+        # self-check of the balanced fused exchange: the O every rank assembled by the mirrored slice
+        # stores must equal the zero-fill + SUM all-reduce assembly of the same slices
+        r0_, r1_ = layer.bounds
+        ref = torch.zeros_like(o)
+        if r1_ > r0_:
+            Pr = bf.make_problem(q, k, v, ref)
+            bf.bfla_sparse_prefill_rows(Pr, cfg, layer.m, r0_, r1_, layer.ws)
+        dist.all_reduce(ref)
+        ok = torch.tensor([1 if torch.equal(ref, o) else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        args.exchange_verified = bool(ok.item())
+        if not args.exchange_verified:
+            args.exchange_fallback = f"{args.exchange_used}: assembled O differs from the all-reduce assembly"
+            args.exchange_used = "nccl"
+            args.force_nccl = True
+            o = torch.empty_like(o)
+            layer = parallel.BalancedLayer(q, k, v, o, cfg, rank, world)
+            m = layer.ms
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
     if heads and hasattr(hout, "mirrors"):
         # self-check of the fused exchange on this node: the layer every rank assembled through the
         # epilogue stores must equal the NCCL all-gather of the ranks' own chunks; otherwise fall back to
@@ -529,7 +575,14 @@ def run_ours(args, w, rank, world, local_rank):
         else:
             Pb = bf.make_problem(qd, kd, vd, od, head_offset=rank * Hkv)
         bufs.append((qd, kd, vd, od, Pb))
-    layers_e2e = [parallel.BalancedLayer(b_[0], b_[1], b_[2], b_[3], cfg, rank, world) for b_ in bufs] if bal else None
+    layers_e2e = None
+    if bal:
+        layers_e2e = []
+        for i_, b_ in enumerate(bufs):
+            pe = make_full_output(args, b_[3].shape, world, rank, dev)
+            od = pe.o if pe is not None else b_[3]
+            bufs[i_] = (b_[0], b_[1], b_[2], od, b_[4])
+            layers_e2e.append(parallel.BalancedLayer(b_[0], b_[1], b_[2], od, cfg, rank, world, peer_out=pe))
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     ne = max(2, args.steps)  # the timed e2e loop runs as many layers as the device-timed one (pipeline fill / drain amortised the same way)
     ev_in = [torch.cuda.Event() for _ in range(ne)]    # inputs of step i resident
@@ -796,11 +849,12 @@ def main():
         if r["s1_roof"] is not None:
             line["stage1_roofline"] = r["s1_roof"]
         line.update(r["extra"])
-        if args.shard == "heads" and world > 1:
+        if args.shard in ("heads", "balanced") and world > 1:
             line["config"]["exchange"] = {
                 "nvls": "fused: prefill epilogue multimem.st of O rows through the NVLS multicast address + device barrier",
                 "p2p": "fused: prefill epilogue TMA-stores O tiles into every peer's symmetric-memory buffer + device barrier",
-            }.get(getattr(args, "exchange_used", ""), "NCCL in-place all-gather after the prefill")
+            }.get(getattr(args, "exchange_used", ""), "NCCL in-place all-gather after the prefill" if args.shard == "heads"
+                  else "zero-fill + NCCL SUM all-reduce of O after the prefill slice")
             if getattr(args, "exchange_fallback", None):
                 line["config"]["exchange_fallback"] = args.exchange_fallback
             if hasattr(args, "exchange_verified"):

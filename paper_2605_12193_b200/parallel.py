@@ -134,6 +134,34 @@ def split_kv_ranges(tkv: int, parts: int) -> list[tuple[int, int]]:
     return [(edges[k], edges[k + 1]) for k in range(parts)]
 
 
+class PeerFullOutput:
+    """Full-layer O in symmetric memory for the cost-balanced mode (§8 f2): every rank's slice writes its
+    rows into its own buffer AND, through bfla_sparse_prefill_mirrored, into every peer's buffer at the
+    same offsets (P2P TMA stores, or one multimem.st through the NVLS multicast address) — replacing the
+    zero-fill + SUM all-reduce.  finish() is the device barrier after which every buffer holds the layer."""
+
+    def __init__(self, shape, world: int, rank: int, device, group=None, multicast: bool = False):
+        import torch.distributed._symmetric_memory as symm
+
+        if world - 1 > 7:
+            raise ValueError("at most 7 peers (BFLA_MAX_MIRRORS)")
+        self.o = symm.empty(tuple(shape), dtype=torch.bfloat16, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        self.hdl = symm.rendezvous(self.o, grp.group_name)
+        off = self.o.data_ptr() - int(self.hdl.buffer_ptrs[rank])
+        self.mirrors = mirror_addresses(self.hdl.buffer_ptrs, rank, off)
+        self.multicast_o = 0
+        if multicast:
+            mc = int(getattr(self.hdl, "multicast_ptr", 0) or 0)
+            if not mc:
+                raise RuntimeError("no NVLS multicast address for this symmetric buffer")
+            self.multicast_o = mc + off
+            self.mirrors = []
+
+    def finish(self):
+        self.hdl.barrier(channel=0)
+
+
 def request_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     """Request (batch) slice for request-level sharding: requests are fully independent."""
     per = -(-batch // world)
@@ -211,8 +239,12 @@ class BalancedLayer:
 
     q/k/v are the full layer (head-first, every rank holds them); o is the full-size output."""
 
-    def __init__(self, q, k, v, o, cfg, rank: int, world: int, row_overhead: int = 3, group=None):
+    def __init__(self, q, k, v, o, cfg, rank: int, world: int, row_overhead: int = 3, group=None, peer_out=None):
         from . import alloc_mask, alloc_workspace, make_problem
+
+        # peer_out (PeerFullOutput whose .o is `o`): step 4 stores every row into the peers' O as well,
+        # step 5 becomes a device barrier — no zero-fill, no all-reduce
+        self.peer_out = peer_out
 
         self.cfg, self.rank, self.world, self.ovh, self.group = cfg, rank, world, row_overhead, group
         self.B, self.Hkv = q.shape[0], k.shape[1]
@@ -233,7 +265,7 @@ class BalancedLayer:
     def run(self, marks=None, stream=None):
         """One layer; marks (optional) = 4 CUDA events recorded at the stage boundaries
         (start, masks done, lists gathered + sliced, prefill done)."""
-        from . import bfla_block_mask, bfla_expand_rescue, bfla_sparse_prefill_rows
+        from . import bfla_block_mask, bfla_expand_rescue, bfla_sparse_prefill_mirrored, bfla_sparse_prefill_rows
 
         st = torch.cuda.current_stream() if stream is None else stream
         rec = (lambda k: marks[k].record(st)) if marks is not None else (lambda k: None)
@@ -252,6 +284,13 @@ class BalancedLayer:
             r0, r1 = balanced_slice(self.counts_host.view(self.B, self.Hkv, -1), self.world, self.rank, self.ovh)
             self.bounds = (r0, r1)
             rec(2)
+            if self.peer_out is not None:  # fused exchange: the slice's rows land in every rank's O
+                if r1 > r0:  # (an empty slice enqueues nothing; rows (0, 0) would mean every row)
+                    bfla_sparse_prefill_mirrored(self.P, self.cfg, self.m, self.peer_out.mirrors, rows=(r0, r1),
+                                                 ws=self.ws, stream=st, multicast_o=self.peer_out.multicast_o)
+                rec(3)
+                self.peer_out.finish()
+                return
             self.o.zero_()
             bfla_sparse_prefill_rows(self.P, self.cfg, self.m, r0, r1, self.ws, st)
             rec(3)

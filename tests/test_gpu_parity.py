@@ -591,6 +591,16 @@ def test_balanced_layer_single_rank_nccl():
         torch.cuda.synchronize()
         assert layer.bounds == (0, 2 * 2 * 33)
         assert torch.equal(o, o_ref)
+        # the fused exchange (symmetric-memory O, mirrored slice stores + device barrier): no peers at world 1
+        try:
+            peer = parallel.PeerFullOutput(q.shape, 1, 0, q.device)
+        except Exception as e:  # noqa: BLE001
+            pytest.skip(f"torch symmetric memory unavailable: {e}")
+        peer.o.fill_(3.0)
+        layer2 = parallel.BalancedLayer(q, k, v, peer.o, cfg, 0, 1, peer_out=peer)
+        layer2.run()
+        torch.cuda.synchronize()
+        assert torch.equal(peer.o, o_ref)
     finally:
         dist.destroy_process_group()
 
