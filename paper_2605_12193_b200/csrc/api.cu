@@ -262,8 +262,8 @@ static WsLayout ws_layout(const Geom& g, bool dense = false) {
   o += al((size_t)g.B * g.Hq * g.Lq * 4);
   L.units = o;  // recompute units (flagged row, KV block) of every flagged row's band, int32
   o += al((size_t)g.B * g.Hq * g.Lq * g.Lkv * 4);
-  L.nflag = o;
-  o += al(16);
+  L.nflag = o;  // flagged-row and recompute-unit counters, then the split-K tile counters (one memset)
+  o += al(16 + tc_tick_bytes(g));
   L.sched = o;  // attention item counter (dynamic scheduling)
   o += al(16);
   L.kgather = o;
@@ -287,7 +287,7 @@ static bfla_status cuda_check(const char* what) {
 // gamma_n = n u / (1 - n u) <= (C + g) u here (the classical recursive-summation bound; the tests
 // pin it on adversarial inputs).  Tensor-core side: n/16 K=16 MMA steps into an fp32 accumulator,
 // bounded by 2 (n/16) u even if every step truncated; + 2 u per split-K partial added in fp32
-// (k_s1_tc_reduce).  Cauchy-Schwarz: sum|x_k y_k| <= ||x|| ||y||.  `slack` >= 1 (bfla_config
+// (the last split of a tile adds them in k_s1_tc_scores).  Cauchy-Schwarz: sum|x_k y_k| <= ||x|| ||y||.  `slack` >= 1 (bfla_config
 // certify_slack) only widens tau: more rows are recomputed, the mask cannot change.
 static float certify_tau(const Geom& g, float slack) {
   const double n = (double)g.g * g.D, u = std::ldexp(1.0, -24);
@@ -345,7 +345,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     {
       const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv_real, (uint64_t)g.B};
       const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
-      const uint32_t box[4] = {64, (uint32_t)kTcTileN / 2, 1, 1};  // two boxes per stage (one on diagonal tiles)
+      const uint32_t box[4] = {64, (uint32_t)kTcBBox, 1, 1};  // 128-row boxes (64-row boxes measured 1.5x slower)
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
     CUtensorMap rq, rk;  // token-row maps (64 x 64 SW128 boxes) for the TMA-staged recompute
@@ -373,13 +373,14 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       launch_block_norms(gk, P->q, kc, qn, kn, st, q_norms_separate);
     }
     float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
-    const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart);
+    cudaMemsetAsync(nflag, 0, 16 + tc_tick_bytes(g), st);  // flagged rows, recompute units, split-K tickets
+    const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart,
+                                        reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(nflag) + 16));
     const bool ragged = g.lens || (g.Nq % g.g) || (g.Nkv % g.g);
     if (!tc_err && ragged && launch_ragged_fixup(gk, P->q, kc, S, st)) {
       if (ss) cudaStreamWaitEvent(st, ss->join, 0);
       return fail(BFLA_ERR_CUDA, "ragged fixup launch failed");
     }
-    cudaMemsetAsync(nflag, 0, 2 * sizeof(int32_t), st);  // flagged rows, recompute units
     if (ss) cudaStreamWaitEvent(st, ss->join, 0);  // joined even on failure: never leave a fork open
     if (tc_err) return fail(BFLA_ERR_CUDA, "tc scores launch failed (%d)", tc_err);
     const int sms = num_sms_current();

@@ -24,12 +24,15 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
                    int32_t* ulist = nullptr);
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
 constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
+constexpr int kTcBBox = 128;   // key-group rows per TMA box of a score B stage
+constexpr int kTcCluster = 2;  // score CTAs per cluster (query heads sharing each K stage by multicast)
 size_t tc_scores_smem();
 // qn (optional): the scores kernel also writes the query-group norm bounds (Gram diagonal)
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st, float* part = nullptr);
+                     cudaStream_t st, float* part = nullptr, int* tick = nullptr);
 int tc_splits(const Geom& g);
 size_t tc_part_bytes(const Geom& g);
+size_t tc_tick_bytes(const Geom& g);
 // canonical rewrite of the block scores of partial groups (ragged n mod g != 0, varlen requests)
 int launch_ragged_fixup(const Geom& g, const void* q, const void* k, float* S, cudaStream_t st);
 // with_q = false: key-group norms only (the scores kernel wrote the query norms)

@@ -25,9 +25,17 @@ constexpr int TM = 128;   // query groups per tile (MMA M)
 constexpr int TN = kTcTileN;  // key groups per tile (MMA N = 256)
 constexpr int TK = 64;    // K elements per stage (one 128-byte swizzle row)
 constexpr int ST = 4;     // pipeline stages (48 KB each)
+// Query norms: summed by the idle epilogue warps from the A stages (default), or from a Gram A A^T on
+// the tensor pipe (BFLA_S1_GRAM, the round-2 design; A/B in DESIGN.md §7.0)
+#ifdef BFLA_S1_GRAM
+constexpr bool kNormWarps = false;
+#else
+constexpr bool kNormWarps = true;
+#endif
+constexpr int kBBox = kTcBBox;  // B rows per TMA box (at csz > 2 some cluster CTAs fetch none)
 constexpr int ABYTES = TM * TK * 2;
 constexpr int BBYTES = TN * TK * 2;
-constexpr int SMEM = ST * (ABYTES + BBYTES) + 2 * ST * 8 + 8 + 16 + 1024;
+constexpr int SMEM = ST * (ABYTES + BBYTES) + 2 * ST * 8 + 8 + 16 + 1024;  // + barriers, TMEM slot, ticket
 
 // ---- group norms: one CTA per (request, head, block) of Q (first) or K.  All eight warps stream:
 // warp w takes group w % G and the (w / G)-th of 8 / G contiguous token slices of it (G <= 8), each lane
@@ -104,21 +112,24 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
   }
 }
 
-// ---- tcgen05 scores: one CTA per (request, query head, M tile of 128 query groups, N tile of 128 key
-// groups); causally dead tiles exit.  Warp 0: TMA producer; warp 1: MMA issuer; warp 2: TMEM alloc;
-// warps 4-7: epilogue (thread = query group row): max over the G key groups of each KV block in
+// ---- tcgen05 scores: one CTA per (request, query head, M tile of 128 query groups, N tile of 256 key
+// groups, K split); causally dead tiles exit.  Warp 0: TMA producer; warp 1: MMA issuer; warp 2: TMEM
+// alloc; warps 4-7: epilogue (thread = query group row): max over the G key groups of each KV block in
 // registers, max over the G query groups of each query block by shuffles (Eq. 10).
 //
-// Query-group norms for the certification come out of the same kernel: the CTAs of the
-// first N tile (nt = 0, every query group) also accumulate A A^T (the query tile against itself,
-// M128 x N128, into TMEM columns 256-383) from the A stages already in shared memory — no extra bytes
-// from L2 — and read its diagonal ||x_u||^2 (fp32 tensor-core sum of exact bf16 squares: relative
-// error <= 2(n/16)u, far inside the 2^-10 slack).  Only the K norms remain for k_s1_block_norms.
+// Query-group norms for the certification come out of the same kernel: in the CTAs of
+// the first N tile (nt = 0, every query group) the idle epilogue warps read each A stage as it lands
+// (thread = its query-group row, 64 bf16 per stage, no extra bytes from L2) and accumulate the sum of
+// squares in fp32 (per stage a 64-long FMA chain, then one add: relative error <= gamma_192, far inside
+// the 2^-10 slack); they release the stage on its `empty` barrier next to the MMA commit.  Only the K
+// norms remain for k_s1_block_norms.
 //
-// Split-K (splits > 1, few tiles: short prompts, and the 1.3-wave grid at 32K): CTA (tile, split) runs
-// k-steps [k0, k1) and writes its raw fp32 partial accumulators, column-major [col][row], to `part`
-// (and the Gram diagonal to `qpart`); k_s1_tc_reduce adds the splits in ascending order and runs the
-// same max-pool epilogue.  The certification bound counts the extra additions (api.cu certify_tau).
+// Split-K (splits > 1, few tiles: short prompts and the 1.3-wave grid at 32K): the CTAs of a tile
+// take a ticket when their accumulators are ready; all but the last write their raw fp32 partials,
+// column-major [col][row], to `part` (query-norm partials to `qpart`) and count themselves done; the
+// last waits for them (they hold tickets, so they are resident) and adds the splits in ascending order
+// — the same sum whichever CTA finishes last — then runs the max-pool epilogue and resets the tile's
+// counters.  The certification bound counts the extra additions (api.cu certify_tau).
 __device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& R, int mt, int nt, int* nlive) {
   const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
   long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
@@ -128,46 +139,61 @@ __device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& R, int mt
   return true;
 }
 
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, Geom g,
                                                          float* __restrict__ S, int n_mt, int n_nt,
                                                          float* __restrict__ qn, int splits,
-                                                         float* __restrict__ part, float* __restrict__ qpart) {
+                                                         float* __restrict__ part, float* __restrict__ qpart,
+                                                         int* __restrict__ tick, int csz_arg) {
+#ifdef BFLA_S1_NOCLUSTER
+  constexpr int csz = 1;  // A/B: the cluster-free code generation
+  (void)csz_arg;
+#else
+  const int csz = csz_arg;
+#endif
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ABYTES + BBYTES));
   uint64_t* empty = full + ST;
   uint64_t* done = empty + ST;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  int* ticket = reinterpret_cast<int*>(tslot + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int t = blockIdx.x / splits;
-  const int split = blockIdx.x % splits;
-  const long long tile = t;
+  // grid order: (head group of csz heads of one KV group, mt, nt, split, cluster rank); the csz CTAs of
+  // a cluster are the same tile of csz query heads that share the KV head, so they share every B stage
+  const int crank = csz > 1 ? (int)cluster_ctarank() : 0;
+  int t = blockIdx.x / csz;
+  const int split = t % splits;
+  t /= splits;
   const int nt = t % n_nt;
   t /= n_nt;
   const int mt = t % n_mt;
-  const int rp = t / n_mt;  // r * Hq + p
+  const int rp = (t / n_mt) * csz + crank;  // r * Hq + p
+  const long long tile = ((long long)rp * n_mt + mt) * n_nt + nt;
   const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
   const Req R = req_of(g, r);  // this request's logical dims (varlen); g.* is the buffer layout
   // key-group columns with any causal block for this M tile: 256, or 128 when the tile's second half
   // lies entirely past the causal frontier (diagonal tiles); causally dead tiles exit (Eq. 11-13)
   int nlive = TN;
   if (!tc_tile_live(g, R, mt, nt, &nlive)) return;
+  const bool qduty = qn != nullptr && nt == 0;  // uniform over the CTA
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, csz + (qduty && kNormWarps ? 4 : 0));  // every cluster CTA's MMA commit (+ norm warps)
     }
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  const bool qduty = qn != nullptr && nt == 0;  // uniform over the CTA
   if (warp == 2) {
-    if (qduty) tmem_alloc<2 * TN>(tslot);
+    if (qduty && !kNormWarps) tmem_alloc<2 * TN>(tslot);  // + the Gram A A^T (columns 256-383)
     else tmem_alloc<TN>(tslot);
   }
   tc_fence_before();
   __syncthreads();
+  if (csz > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const int nk = g.g * g.D / TK;
@@ -176,15 +202,20 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     for (int kk = k0; kk < k1; ++kk) {
       const int s = (kk - k0) % ST;
       mbar_wait(empty + s, (((kk - k0) / ST) & 1) ^ 1);
-      mbar_arrive_expect_tx(full + s, ABYTES + (nlive == TN ? BBYTES : BBYTES / 2));
+      mbar_arrive_expect_tx(full + s, ABYTES + nlive * TK * 2);  // own A + the whole live B
       unsigned char* a = smem + s * (ABYTES + BBYTES);
       tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
-      tma_load_4d(a + ABYTES, &tmB, full + s, kk * TK, nt * TN, h / g.kvdiv, r);  // 128-row boxes
-      if (nlive == TN) tma_load_4d(a + ABYTES + BBYTES / 2, &tmB, full + s, kk * TK, nt * TN + TN / 2, h / g.kvdiv, r);
+      // B in 64-row boxes; with a cluster each CTA fetches every csz-th box once and multicasts it
+      for (int q = crank; q < nlive / kBBox; q += csz) {
+        if (csz > 1)
+          tma_load_4d_mc(a + ABYTES + q * kBBox * 128, &tmB, full + s, kk * TK, nt * TN + q * kBBox, h / g.kvdiv, r,
+                         (uint16_t)((1u << csz) - 1u));
+        else
+          tma_load_4d(a + ABYTES + q * kBBox * 128, &tmB, full + s, kk * TK, nt * TN + q * kBBox, h / g.kvdiv, r);
+      }
     }
   } else if (warp == 1) {  // converged warp, one elected lane issues (see umma_f16_ss_warp)
     const uint32_t idesc = nlive == TN ? idesc_bf16(TM, TN, 0, 0) : idesc_bf16(TM, TN / 2, 0, 0);
-    constexpr uint32_t idesc_g = idesc_bf16(TM, TM, 0, 0);  // Gram A A^T
     const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
     for (int kk = k0; kk < k1; ++kk) {
       const int s = (kk - k0) % ST;
@@ -194,88 +225,157 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 #pragma unroll
       for (int k16 = 0; k16 < TK / 16; ++k16)
         umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk > k0 || k16) ? 1u : 0u);
-      if (qduty) {
+      if (qduty && !kNormWarps) {
 #pragma unroll
         for (int k16 = 0; k16 < TK / 16; ++k16)
-          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_g,
+          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_bf16(TM, TM, 0, 0),
                            (kk > k0 || k16) ? 1u : 0u);
       }
-      umma_commit_warp(empty + s);
+      if (csz > 1) umma_commit_mc_warp(empty + s, (uint16_t)((1u << csz) - 1u));  // B slots are shared
+      else umma_commit_warp(empty + s);
     }
     umma_commit_warp(done);
   } else if (warp >= 4) {
     const int lg = warp & 3;
     const int row = lg * 32 + lane;  // query group within the tile
+    float sq = 0.f;                  // ||x_row||^2 over this split's k-range (qduty)
+    if (qduty && kNormWarps) {
+      // the row's 128 bytes of each A stage (SWIZZLE_128B permutes its eight 16-byte chunks within the
+      // row; a sum of squares does not care).  Chunk (c + lane) & 7: the eight rows of a quarter warp
+      // hit eight distinct chunk positions, so every LDS.128 wavefront covers all 32 banks once.
+      for (int kk = k0; kk < k1; ++kk) {
+        const int s = (kk - k0) % ST;
+        mbar_wait(full + s, ((kk - k0) / ST) & 1);
+        const uint32_t arow = smem_u32(smem + s * (ABYTES + BBYTES) + row * 128);
+        float a8[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t w4[4];
+          ld_shared_v4(arow + (((c + lane) & 7) << 4), w4);
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const float lo = __uint_as_float(w4[f] << 16), hi = __uint_as_float(w4[f] & 0xffff0000u);
+            a8[f] = __fmaf_rn(hi, hi, __fmaf_rn(lo, lo, a8[f]));
+          }
+        }
+        const float part_sq = __fadd_rn(__fadd_rn(a8[0], a8[1]), __fadd_rn(a8[2], a8[3]));
+        // release the stage to the next TMA fill (async proxy) only after this warp's shared-memory
+        // reads are performed: proxy fence, then the arrive (a generic load still in flight when the
+        // arrive landed let the next fill race it — the bug of an earlier two-heads variant)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        sq = __fadd_rn(sq, part_sq);
+      }
+    }
     mbar_wait(done, 0);
     tc_fence_after();
-    if (splits > 1) {  // raw partials; k_s1_tc_reduce finishes the tile
-      if (qduty) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
-        tmem_wait_ld();
-        float sq = 0.f;
+    if (qduty && !kNormWarps) {  // ||x_row||^2 = (A A^T)[row][row]: this warp's lanes x columns [32 lg, 32 lg + 32)
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
+      tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (e == lane) sq = v[e];
-        qpart[(((long long)rp * n_mt + mt) * splits + split) * TM + row] = sq;
+      for (int e = 0; e < 32; ++e)
+        if (e == lane) sq = v[e];
+    }
+    bool last = true;
+    if (splits > 1) {
+      // tick == nullptr: every split publishes its partials and k_s1_tc_reduce finishes the tile
+      if (threadIdx.x == 128) *ticket = tick ? atomicAdd(tick + 2 * tile, 1) : 0;
+      epi_bar();
+      last = tick && *ticket == splits - 1;
+      if (!last) {  // publish the raw partials, count this split done
+        if (qduty) qpart[(((long long)rp * n_mt + mt) * splits + split) * TM + row] = sq;
+        float* pp = part + (tile * splits + split) * (long long)(TN * TM);
+        for (int c0 = 0; c0 < nlive; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) __stcg(pp + (c0 + e) * TM + row, v[e]);  // lanes = consecutive rows
+        }
+        if (tick) {
+          __threadfence();
+          epi_bar();
+          if (threadIdx.x == 128) atomicAdd(tick + 2 * tile + 1, 1);
+        }
+      } else {  // the others hold tickets: they are resident and finish their stores
+        if (threadIdx.x == 128) {
+          while (atomicAdd(tick + 2 * tile + 1, 0) < splits - 1) {
+          }
+          __threadfence();
+        }
+        epi_bar();
+        if (qduty) {
+          float a = 0.f;
+          for (int sp = 0; sp < splits; ++sp)
+            a = __fadd_rn(a, sp == split ? sq : __ldcg(qpart + (((long long)rp * n_mt + mt) * splits + sp) * TM + row));
+          sq = a;
+        }
       }
-      float* pp = part + (tile * splits + split) * (long long)(TN * TM);
+    }
+    if (last) {
+      const int grow = mt * TM + row;  // global query group of head p
+      const int ib = grow / g.G, u = grow % g.G;
+      if (qduty) {
+        // full groups only: a partial group's row holds padding (zero-filled or another request's
+        // bytes); its scores come from k_s1_ragged_fixup in the canonical order (exact, no bound needed)
+        const bool ufull = (long long)(grow + 1) * g.g <= R.Nq;
+        float mx = ufull ? sqrtf(fmaxf(sq, 0.f)) : 0.f;
+        for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
+      }
+      // padding-only groups never take the max (R3); partial groups (ragged N, varlen) are left to the
+      // canonical fixup, which rewrites every block score they take part in
+      const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;
+      long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
+      if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+      float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
+      const float* pp = part + tile * splits * (long long)(TN * TM) + row;
       for (int c0 = 0; c0 < nlive; c0 += 32) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
         tmem_wait_ld();
+        if (splits > 1) {  // ascending split order: the same sum whichever split finished last
+          float a[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) pp[(c0 + e) * TM + row] = v[e];  // lanes = consecutive rows
-      }
-    } else {
-    const int grow = mt * TM + row;           // global query group of head p
-    const int ib = grow / g.G, u = grow % g.G;
-    if (qduty) {
-      // ||x_row||^2 = (A A^T)[row][row]: this warp's 32 lanes x columns [32 lg, 32 lg + 32)
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
-      tmem_wait_ld();
-      float sq = 0.f;
+          for (int e = 0; e < 32; ++e) a[e] = split == 0 ? v[e] : __ldcg(pp + (c0 + e) * TM);
+          for (int sp = 1; sp < splits; ++sp) {
+            const float* ps = pp + (long long)sp * TN * TM + c0 * TM;
+            float b[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (e == lane) sq = v[e];
-      // full groups only: a partial group's row holds padding (zero-filled or another request's
-      // bytes); its scores come from k_s1_ragged_fixup in the canonical order (exact, no bound needed)
-      const bool ufull = (long long)(grow + 1) * g.g <= R.Nq;
-      float mx = ufull ? sqrtf(fmaxf(sq, 0.f)) : 0.f;
-      for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
-    }
-    // padding-only groups never take the max (R3); partial groups (ragged N, varlen) are left to the
-    // canonical fixup, which rewrites every block score they take part in
-    const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;
-    long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
-    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
-    float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
-    for (int c0 = 0; c0 < nlive; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
-      tmem_wait_ld();
-      for (int jb0 = 0; jb0 < 32; jb0 += g.G) {
-        const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
-        float mx = -INFINITY;
-        for (int vv = 0; vv < g.G; ++vv)
-          if ((long long)(gcol + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);  // full key groups
-        if (!uvalid) mx = -INFINITY;
-        for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const int jb = gcol / g.G;
-        if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
+            for (int e = 0; e < 32; ++e) b[e] = sp == split ? v[e] : __ldcg(ps + e * TM);  // 32 loads in flight
+#pragma unroll
+            for (int e = 0; e < 32; ++e) a[e] = __fadd_rn(a[e], b[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = a[e];
+        }
+        for (int jb0 = 0; jb0 < 32; jb0 += g.G) {
+          const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
+          float mx = -INFINITY;
+          for (int vv = 0; vv < g.G; ++vv)
+            if ((long long)(gcol + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);  // full key groups
+          if (!uvalid) mx = -INFINITY;
+          for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          const int jb = gcol / g.G;
+          if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
+        }
       }
-    }
+      if (splits > 1 && threadIdx.x == 128) {  // every split has counted itself: reset for the next call
+        tick[2 * tile] = 0;
+        tick[2 * tile + 1] = 0;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    if (qduty) tmem_dealloc<2 * TN>(tmem);
+    if (qduty && !kNormWarps) tmem_dealloc<2 * TN>(tmem);
     else tmem_dealloc<TN>(tmem);
   }
+  if (csz > 1) cluster_sync_all();  // no CTA leaves while a peer's multicast or commit may target it
 }
 
 // Split-K finish: four CTAs (128 threads, thread = query-group row) per tile, one per 64-column
@@ -985,27 +1085,78 @@ int tc_splits(const Geom& g) {
   return s < 1 ? 1 : s;
 }
 
+// Split-K scratch: raw partials [tile][split][TN][TM] and query-norm partials [rp][mt][split][TM];
+// `tick` holds two int counters per tile (ticket, splits done), zero on entry (the caller's memset;
+// the last split of each tile also resets its pair).
+static long long tc_tiles(const Geom& g, int* n_mt_out = nullptr, int* n_nt_out = nullptr) {
+  const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
+  const int n_mt = (ngq + TM - 1) / TM, n_nt = (ngk + TN - 1) / TN;
+  if (n_mt_out) *n_mt_out = n_mt;
+  if (n_nt_out) *n_nt_out = n_nt;
+  return (long long)g.B * g.Hq * n_mt * n_nt;
+}
+
 size_t tc_part_bytes(const Geom& g) {
   const int s = tc_splits(g);
   if (s == 1) return 0;
-  const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
-  const long long n_mt = (ngq + TM - 1) / TM, tiles = (long long)g.B * g.Hq * n_mt * ((ngk + TN - 1) / TN);
+  int n_mt;
+  const long long tiles = tc_tiles(g, &n_mt);
   return (size_t)(tiles * s * TN * TM + (long long)g.B * g.Hq * n_mt * s * TM) * 4;
 }
 
+size_t tc_tick_bytes(const Geom& g) { return tc_splits(g) > 1 ? (size_t)tc_tiles(g) * 2 * sizeof(int) : 0; }
+
+// Cluster size for the score kernel: the csz query heads of one KV group that share every K tile run as
+// one thread-block cluster and fetch each B stage once (TMA multicast), cutting the L2->SM traffic that
+// bounds this kernel.  csz divides m; 1 = no cluster.
+static int tc_cluster(const Geom& g) {
+  static const int forced = experiment_knob("BFLA_S1_CLUSTER", 0);  // A/B builds only
+  int c = forced > 0 ? forced : kTcCluster;
+  while (c > 1 && (g.m % c)) c >>= 1;
+  return c < 1 ? 1 : c;
+}
+
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st, float* part) {
-  const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
-  const int n_mt = (ngq + TM - 1) / TM, n_nt = (ngk + TN - 1) / TN;
-  const long long ctas = (long long)g.B * g.Hq * n_mt * n_nt;
+                     cudaStream_t st, float* part, int* tick) {
+  int n_mt, n_nt;
+  const long long ctas = tc_tiles(g, &n_mt, &n_nt);
   const int splits = part ? tc_splits(g) : 1;
   if (ctas <= 0 || ctas * splits > 0x7fffffff) return -1;
   cudaError_t e = cudaFuncSetAttribute(k_s1_tc_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (e != cudaSuccess) return (int)e;
   float* qpart = part ? part + ctas * splits * (long long)(TN * TM) : nullptr;
-  k_s1_tc_scores<<<(int)(ctas * splits), 256, SMEM, st>>>(tmA, tmB, g, S, n_mt, n_nt, qn, splits, part, qpart);
+  // split-K finish: in the score kernel (the last split of a tile adds the others' partials) for grids
+  // of at most about one wave, else by k_s1_tc_reduce over the whole grid
+  static const int fused_knob = experiment_knob("BFLA_S1_FUSED_SPLIT", -1);  // A/B builds only
+  const bool fused = splits > 1 && (fused_knob >= 0 ? fused_knob == 1 : ctas * splits <= 2 * 148);
+  if (fused && !tick) return -1;
+  int csz = tc_cluster(g);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3((unsigned)(ctas * splits));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  if (csz > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)csz;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k_s1_tc_scores, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      csz = 1;
+      cfg.attrs = nullptr;
+      cfg.numAttrs = 0;
+    }
+  }
+  e = cudaLaunchKernelEx(&cfg, k_s1_tc_scores, tmA, tmB, g, S, n_mt, n_nt, qn, splits, part, qpart,
+                         fused ? tick : nullptr, csz);
   count_launch();
-  if (splits > 1) {
+  if (e != cudaSuccess) return (int)e;
+  if (splits > 1 && !fused) {
     k_s1_tc_reduce<<<(int)(ctas * (TN / kRedCols)), 128, 0, st>>>(g, S, n_mt, n_nt, qn, splits, part, qpart);
     count_launch();
   }
