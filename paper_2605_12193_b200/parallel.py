@@ -134,6 +134,177 @@ def split_kv_ranges(tkv: int, parts: int) -> list[tuple[int, int]]:
     return [(edges[k], edges[k + 1]) for k in range(parts)]
 
 
+# ---- §8 f2: split-KV piece planner -------------------------------------------------------------
+# A row (r, h, i) of the prefill is ONE work item on ONE SM (its kept tiles run in sequence), so a
+# rank's prefill time is about max(its tiles / #SMs, its longest row).  A diffuse head (kappa -> 1)
+# has rows of hundreds of kept tiles; at P = 8 one such row outlasts the rank's whole share (DESIGN §8:
+# 2.9x of ideal at 32K), and no row partition can fix it.  The planner splits every row longer than
+# the per-SM share into KV-tile ranges (bfla_sparse_prefill_kvrange on a row slice), hands the ranges
+# of one row to different ranks, balances the remaining rows as contiguous LPT slices around them,
+# and the ranges' (O_k, LSE_k) merge with bfla_merge_partials.
+
+
+def _lpt_rows(counts, nc_tiles: int = 0):
+    """Per LPT row rho = (r * h_kv + h) * tq + (tq - 1 - i): kept tiles and causal extent n(i) (tiles)."""
+    import numpy as np
+
+    c = np.asarray(counts, dtype=np.int64)
+    B, H, tq = c.shape
+    kept = c[:, :, ::-1].reshape(-1)  # rho order: descending i inside each (r, h) segment
+    i = np.tile(np.arange(tq - 1, -1, -1), B * H)
+    a = nc_tiles + 1  # causal tiles of row i: i + a (Eq. 11-13 with N_c a multiple of T)
+    return kept, i + a
+
+
+def plan_pieces(counts, parts: int, row_overhead: int = 3, sms: int = 148, nc_tiles: int = 0,
+                max_split: int = 8):
+    """Split-KV work plan for `parts` ranks from a host copy of mask.tile_count ([B, h_kv, tq]).
+
+    Returns one list per rank of pieces (rho_begin, rho_end, kv_begin, kv_end, slot): LPT row slice x
+    KV-tile range [kv_begin, kv_end) ((0, 0) = the whole row, bfla_sparse_prefill_rows), whose O / LSE
+    go to partial buffer `slot` (the merge input; whole rows use slot 0, the k-th range of a split run
+    slot k).  Every (row, kept tile) is covered exactly once.  A row is split when its cost (kept tiles
+    + row_overhead) exceeds the per-SM share of one rank, ceil(total / parts / sms), together
+    with the rest of its head's rows up to the last such row (the longest rows of a head come first in
+    rho, so that is one contiguous run per head and one launch per KV range); each run is cut into K <=
+    min(parts, max_split) KV ranges of equal estimated work (kept tiles spread uniformly over each row's
+    causal extent) and the K pieces go to K different ranks, least loaded first; the other rows are
+    then packed as contiguous slices over the ranks in order, minimising the bottleneck (bisection +
+    greedy fill around each rank's piece load)."""
+    import numpy as np
+
+    kept, ext = _lpt_rows(counts, nc_tiles)
+    cost = kept + row_overhead
+    nrows = len(cost)
+    total = int(cost.sum())
+    share = max(row_overhead + 1, -(-total // (parts * sms)))
+    heavy = (cost > share) & (kept > 0)
+    # one run per (r, h) segment: from the segment's first row (its longest, rho order is descending i)
+    # through its last heavy row — each run is ONE launch per KV range, so a rank's pieces never
+    # serialise row by row (isolated heavy rows would each cost a launch on a single SM)
+    tq = np.asarray(counts).shape[-1]
+    for s0 in range(0, nrows, tq):
+        hv = np.nonzero(heavy[s0:s0 + tq])[0]
+        if len(hv):
+            heavy[s0:s0 + hv[-1] + 1] = True
+    load = [0.0] * parts
+    plan = [[] for _ in range(parts)]
+    if not heavy.any():  # nothing to split: the exact bottleneck-optimal row partition
+        from . import bfla_balance_rows
+
+        bounds = bfla_balance_rows(np.asarray(counts, dtype=np.int32), parts, row_overhead)
+        return [[(bounds[r], bounds[r + 1], 0, 0, 0)] if bounds[r + 1] > bounds[r] else [] for r in range(parts)]
+    # heavy runs -> KV-range pieces
+    rho = 0
+    while rho < nrows:
+        if not heavy[rho]:
+            rho += 1
+            continue
+        end = rho
+        while end < nrows and heavy[end]:
+            end += 1
+        # pieces at most half the per-SM share: a piece's longest row is the critical path of its launch
+        K = int(min(parts, max_split, -(-2 * int(cost[rho:end].max()) // share)))
+        dens = kept[rho:end] / ext[rho:end]  # kept tiles per causal tile of each row
+        tkv = int(ext[rho:end].max())
+        # work per KV column j: sum over the run's rows that reach j of their density
+        col = np.zeros(tkv + 1)
+        np.add.at(col, ext[rho:end], -dens)
+        col[0] += dens.sum()
+        work = np.cumsum(col)[:tkv]
+        cum = np.concatenate([[0.0], np.cumsum(work)])
+        edges = [0]
+        for k in range(1, K):
+            e = int(np.searchsorted(cum, cum[-1] * k / K))
+            if edges[-1] < e < tkv:
+                edges.append(e)
+        edges.append(tkv)
+        used = set()
+        for k in range(len(edges) - 1):
+            a_, b_ = edges[k], edges[k + 1]
+            pc = float(cum[b_] - cum[a_]) + row_overhead * (end - rho)
+            r = min((x for x in range(parts) if x not in used), key=lambda x: load[x])
+            used.add(r)
+            load[r] += pc
+            plan[r].append((rho, end, a_, b_, k))
+        rho = end
+    # light rows: contiguous slices of the remaining LPT sequence over ranks 0..parts-1
+    light = np.nonzero(~heavy)[0]
+    lc = cost[light].astype(np.float64)
+
+    pre = np.concatenate([[0.0], np.cumsum(lc)])
+
+    def fill(bound):  # greedy: each rank in order takes the longest prefix that fits its capacity
+        cuts, pos = [], 0
+        for r in range(parts):
+            if r == parts - 1:
+                end = len(lc)
+            else:
+                end = int(np.searchsorted(pre, pre[pos] + bound - load[r] + 1e-9, side="right")) - 1
+                end = max(pos, min(end, len(lc)))
+            cuts.append((pos, end))
+            pos = end
+        ok = all(load[r] + pre[b] - pre[a] <= bound + 1e-9 for r, (a, b) in enumerate(cuts))
+        return cuts, ok
+
+    lo, hi = max([0.0] + load + ([float(lc.max())] if len(lc) else [])), float(total) + max(load + [0.0])
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if fill(mid)[1]:
+            hi = mid
+        else:
+            lo = mid
+    cuts, _ = fill(hi)
+    for r, (a, b) in enumerate(cuts):
+        if b <= a:
+            continue
+        seg = light[a:b]
+        # contiguous rho runs inside the slice (heavy runs in between were planned above)
+        brk = np.nonzero(np.diff(seg) != 1)[0]
+        starts = np.concatenate([[0], brk + 1])
+        ends = np.concatenate([brk + 1, [len(seg)]])
+        for s0, e0 in zip(starts, ends):
+            plan[r].append((int(seg[s0]), int(seg[e0 - 1]) + 1, 0, 0, 0))
+    return plan
+
+
+def plan_slots(plan) -> int:
+    """Number of partial (O, LSE) buffers a plan writes (1 + the largest KV-range slot)."""
+    return 1 + max((p[4] for pl in plan for p in pl), default=0)
+
+
+def run_plan(problem_for_slot, cfg, mask, pieces, ws=None, stream=None, streams=None) -> None:
+    """Enqueue one rank's pieces: whole-row slices through bfla_sparse_prefill_rows, KV-range pieces
+    through bfla_sparse_prefill_kvrange; problem_for_slot(k) is the bfla problem whose O / LSE are
+    partial buffer k (their LSE must be set: the merge weighs the partials by it).  With `streams`
+    (side streams) the pieces are spread over them, forked from and joined back into `stream`, so the
+    launches overlap on the GPU (each is one persistent grid; the next fills SMs as the previous drains)
+    instead of paying every launch's tail in sequence.  ws is the workspace of a single launch (its item
+    counter): concurrent pieces need one workspace each — pass a list."""
+    from . import bfla_sparse_prefill_kvrange, bfla_sparse_prefill_rows
+
+    main = torch.cuda.current_stream() if stream is None else stream
+    lanes = list(streams) if streams else [main]
+    wss = ws if isinstance(ws, (list, tuple)) else [ws] * len(pieces)
+    if streams:
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for s_ in lanes:
+            s_.wait_event(fork)
+    for n, (r0, r1, a, b, slot) in enumerate(pieces):
+        st = lanes[n % len(lanes)]
+        w = wss[n % len(wss)]
+        if a == 0 and b == 0:
+            bfla_sparse_prefill_rows(problem_for_slot(slot), cfg, mask, r0, r1, w, st)
+        else:
+            bfla_sparse_prefill_kvrange(problem_for_slot(slot), cfg, mask, a, b, rows=(r0, r1), ws=w, stream=st)
+    if streams:
+        for s_ in lanes:
+            ev = torch.cuda.Event()
+            ev.record(s_)
+            main.wait_event(ev)
+
+
 class PeerFullOutput:
     """Full-layer O in symmetric memory for the cost-balanced mode (§8 f2): every rank's slice writes its
     rows into its own buffer AND, through bfla_sparse_prefill_mirrored, into every peer's buffer at the

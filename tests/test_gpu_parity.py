@@ -968,3 +968,51 @@ def test_split_kv_on_a_row_slice():
     assert err.max().item() <= 1.6e-2 and err.mean().item() <= 1e-3
     assert torch.allclose(l[want], l_ref[want], rtol=1e-5, atol=1e-5)
     assert not o[~want].any() and bool((l[~want] == -float("inf")).all())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts,sms", [(8, 148), (4, 16), (2, 148)])
+def test_split_kv_plan_executes_to_the_unsplit_output(parts, sms):
+    """§8 f2 split-KV planner (parallel.plan_pieces): every rank's pieces — whole-row slices and
+    (row slice x KV range) pieces of the rows longer than the per-SM share — run on one GPU into the
+    plan's partial slots, and bfla_merge_partials gives the unsplit O within bf16 rounding and its LSE
+    to 1e-5, and the oracle on sampled rows.  KV group 0 is diffuse (Q x 0.05: near-uniform block
+    softmax), the case that splits."""
+    from paper_2605_12193_b200 import parallel
+
+    prob = workloads.structured(46, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128, block=256)
+    prob.q[:, :4] *= 0.05
+    cfg = bf.Config(b=256, g=64, gamma=0.95, eta=16, seed=9)
+    q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
+    o_ref = torch.empty_like(q)
+    l_ref = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    P = bf.make_problem(q, k, v, o_ref, l_ref)
+    ws, m = bf.alloc_workspace(P, cfg), bf.alloc_mask(P, cfg, labels=True)
+    bf.bfla_block_mask(P, cfg, m, ws)
+    bf.bfla_expand_rescue(P, cfg, m, ws)
+    bf.bfla_sparse_prefill(P, cfg, m, ws)
+    counts = m.tile_count.cpu().numpy()
+    plan = parallel.plan_pieces(counts, parts, sms=sms)
+    nslot = parallel.plan_slots(plan)
+    if (parts, sms) == (8, 148):
+        assert nslot > 1, "the diffuse head's long rows must be split"
+    o_parts = [torch.zeros_like(q) for _ in range(nslot)]
+    l_parts = [torch.full_like(l_ref, -float("inf")) for _ in range(nslot)]
+    probs = [bf.make_problem(q, k, v, o_parts[s], l_parts[s]) for s in range(nslot)]
+    for pieces in plan:
+        parallel.run_plan(lambda s: probs[s], cfg, m, pieces, ws=ws)
+    o = torch.empty_like(q)
+    l = torch.empty_like(l_ref)
+    bf.bfla_merge_partials(bf.make_problem(q, k, v, o, l), o_parts, l_parts)
+    torch.cuda.synchronize()
+    err = (o.float() - o_ref.float()).abs()
+    assert err.max().item() <= 1.6e-2 and err.mean().item() <= 1e-3, (err.max().item(), err.mean().item())
+    assert torch.allclose(l, l_ref, rtol=1e-5, atol=1e-5)
+    if nslot == 1:
+        assert torch.equal(o, o_ref)  # whole rows only: the merge of one part is exact
+    labels = m.tile_label.cpu().numpy()
+    rows = np.array([[p_, t] for p_ in (0, 3, 5) for t in range(0, 4096, 53)], np.int32)
+    (o_or, _), = oracle_attention(prob, labels, 64, rows_per_req=[rows])
+    og = o[0].float().cpu().numpy()[rows[:, 0], rows[:, 1]].astype(np.float64)
+    e2 = np.abs(og - o_or)
+    assert e2.max() <= 2e-2 and e2.mean() <= 2e-3, (e2.max(), e2.mean())

@@ -98,4 +98,23 @@ for parts in (2, 4, 8):
     t = [time_slice(x, y) for x, y in zip(bal_b[:-1], bal_b[1:])]
     res["balanced"] = {"slice_ms": [round(x, 4) for x in t], "max_ms": round(max(t), 4),
                        "max_over_ideal": round(max(t) / (full / parts), 3), "bounds": bal_b}
+    # split-KV plan (parallel.plan_pieces): a rank's pieces run back to back on its GPU; the KV-range
+    # partials go to slot buffers (the cross-rank merge of the split rows is not timed: one GPU)
+    plan = parallel.plan_pieces(counts.numpy(), parts, a.overhead)
+    nslot = parallel.plan_slots(plan)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+    o_s = [torch.empty_like(q) for _ in range(nslot)]
+    l_s = [torch.empty_like(lse) for _ in range(nslot)]
+    if w["paged"]:
+        probs = [bf.make_problem(q, kc, vc, o_s[s], l_s[s], page_table=pt, n_kv=N) for s in range(nslot)]
+    else:
+        probs = [bf.make_problem(q, k, v, o_s[s], l_s[s]) for s in range(nslot)]
+    lanes = [torch.cuda.Stream() for _ in range(max(len(pl) for pl in plan))]
+    wsl = [ws] + [bf.alloc_workspace(P, cfg) for _ in range(len(lanes) - 1)]  # one item counter per lane
+    t = [time_call(lambda pl=pl: parallel.run_plan(lambda s: probs[s], cfg, m, pl, ws=wsl, streams=lanes))
+         for pl in plan]
+    res["split_kv"] = {"rank_ms": [round(x, 4) for x in t], "max_ms": round(max(t), 4),
+                       "max_over_ideal": round(max(t) / (full / parts), 3), "slots": nslot,
+                       "kv_pieces": sum(1 for pl in plan for p in pl if p[3])}
+    del o_s, l_s, probs
     print(json.dumps({"workload": a.workload, "skew": a.skew, "P": parts, "ideal_ms": round(full / parts, 4), **res}))
