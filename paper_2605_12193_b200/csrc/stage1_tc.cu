@@ -382,7 +382,10 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 // group; sums the splits in ascending order, then the epilogue of k_s1_tc_scores (Gram diagonal ->
 // query norms; G x G max).  Loads are column-major partials: a warp reads 128 contiguous bytes, and
 // the G x splits loads of a block column are independent (in flight together).
-constexpr int kRedCols = 64;
+#ifndef BFLA_RED_COLS
+#define BFLA_RED_COLS 16  // A/B (profiles/r3_s1_reduce_cols.txt): 64 -> 16 cols: 32K 0.198 -> 0.194, 16K 0.169 -> 0.132 ms
+#endif
+constexpr int kRedCols = BFLA_RED_COLS;  // key-group columns per reduce CTA
 __global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict__ S, int n_mt, int n_nt,
                                                       float* __restrict__ qn, int splits,
                                                       const float* __restrict__ part,
