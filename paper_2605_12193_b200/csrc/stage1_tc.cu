@@ -1147,9 +1147,18 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k_s1_tc_scores, &cfg) != cudaSuccess || nclusters < 1) {
+    // can a cluster of csz one-CTA-per-SM blocks be resident at all (queried once per device and size)
+    static thread_local int ok_dev = -1, ok_csz = 0, ok_val = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (ok_dev != dev || ok_csz != csz) {
+      int nclusters = 0;
+      ok_val = cudaOccupancyMaxActiveClusters(&nclusters, k_s1_tc_scores, &cfg) == cudaSuccess && nclusters >= 1;
       cudaGetLastError();
+      ok_dev = dev;
+      ok_csz = csz;
+    }
+    if (!ok_val) {
       csz = 1;
       cfg.attrs = nullptr;
       cfg.numAttrs = 0;
