@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) k_s1_block_norms(Geom g, const __nv_bfloa
 // last waits for them (they hold tickets, so they are resident) and adds the splits in ascending order
 // — the same sum whichever CTA finishes last — then runs the max-pool epilogue and resets the tile's
 // counters.  The certification bound counts the extra additions (api.cu certify_tau).
-__device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& R, int mt, int nt, int* nlive) {
+__host__ __device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& R, int mt, int nt, int* nlive) {
   const int BQ = TM / g.G, BK = TN / g.G;  // blocks per tile
   long long e_last = (long long)R.Nc + (long long)((mt + 1) * BQ) * g.b - 1;
   if (e_last > R.Nkv - 1) e_last = R.Nkv - 1;
@@ -1074,15 +1074,28 @@ void launch_paged_gather(const Geom& g, const void* kcache, const int32_t* pt, v
 
 size_t tc_scores_smem() { return SMEM; }
 
-// Split-K factor: enough CTAs for about two waves of 148 SMs when the tile grid is small, at most 8
-// and at least 16 k-steps per split; BFLA_TC_SPLITS overrides (A/B).  Deterministic in the geometry,
-// so bfla_workspace_size can reserve the partials.
+// Split-K factor from the live (causal) tile count: just under one wave of 148 SMs for small grids, 2
+// between one and two waves, else 1; at most 8 and at least 16 k-steps per split; BFLA_TC_SPLITS
+// overrides (A/B).  Deterministic in the geometry, so bfla_workspace_size can reserve the partials.
 int tc_splits(const Geom& g) {
   const int ngq = (g.Nq + g.g - 1) / g.g, ngk = (g.Nkv + g.g - 1) / g.g;
-  const long long tiles = (long long)g.B * g.Hq * ((ngq + TM - 1) / TM) * ((ngk + TN - 1) / TN);
+  const int n_mt = (ngq + TM - 1) / TM, n_nt = (ngk + TN - 1) / TN;
   const int nk = g.g * g.D / TK;
   static const int forced = experiment_knob("BFLA_TC_SPLITS", 0);  // A/B builds only
-  int s = forced > 0 ? forced : (tiles >= 2 * 148 ? 1 : (int)((2 * 148 + tiles - 1) / tiles));
+  int s = forced;
+  if (s <= 0) {
+    // live (causal) tiles of one (request, head) — buffer dims stand in for varlen requests
+    const Req R = make_req(g.Nq, g.Nkv, g.b, g.T);
+    long long live = 0;
+    int nl;
+    for (int mt = 0; mt < n_mt; ++mt)
+      for (int nt = 0; nt < n_nt; ++nt) live += tc_tile_live(g, R, mt, nt, &nl) ? 1 : 0;
+    live *= (long long)g.B * g.Hq;
+    // measured (profiles/r3_s1_splits.txt): a grid just under one wave beats more, shorter splits
+    // (8K: 32 live tiles x 4 splits 0.085 ms vs x 8 0.100); between one and two waves of tiles, two
+    // splits even out the diagonal half tiles (32K: 192 live tiles, 2 splits 0.194 vs 1 0.214)
+    s = live >= 2 * 148 ? 1 : live >= 148 ? 2 : (int)(148 / (live > 0 ? live : 1));
+  }
   if (s > 8) s = 8;
   while (s > 1 && nk / s < 16) --s;
   return s < 1 ? 1 : s;
