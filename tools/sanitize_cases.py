@@ -15,7 +15,7 @@ import workloads  # noqa: E402
 SLACK = 50.0  # bfla_config.certify_slack: widen tau so rows are flagged and the recompute kernels run
 
 
-def run(prob, cfg, paged=0, slices=0, mirrors=0, seqlens=None):
+def run(prob, cfg, paged=0, slices=0, mirrors=0, seqlens=None, stage1_only=False):
     q, k, v = prob.q.cuda(), prob.k.cuda(), prob.v.cuda()
     o = torch.zeros_like(q)
     lse = torch.zeros(q.shape[:3], dtype=torch.float32, device="cuda")
@@ -30,6 +30,9 @@ def run(prob, cfg, paged=0, slices=0, mirrors=0, seqlens=None):
         ws = bf.alloc_workspace(P, cfg)
         m = bf.alloc_mask(P, cfg, labels=True)
         bf.bfla_block_mask(P, cfg, m, ws)
+        if stage1_only:
+            torch.cuda.synchronize()
+            return o
         bf.bfla_expand_rescue(P, cfg, m, ws)
         if slices:
             bounds = bf.bfla_balance_rows(m.tile_count.cpu(), slices)
@@ -85,6 +88,15 @@ def main():
         ("mirrored d=128 (TMA epilogue)", g1, bf.Config(b=256, g=64), dict(mirrors=2)),
         ("mirrored d=256 (thread stores)", workloads.gaussian(13, B=1, Hq=4, Hkv=2, Nq=1024, Nkv=1024, d=256,
                                                               sigma=0.8), bf.Config(b=256, g=64), dict(mirrors=2)),
+        # round 3: score-kernel clusters (multicast B stages, m = 4 -> CTA pairs; m = 1 -> no cluster),
+        # split-K finished in the kernel (small grid) and by the reduce kernel (64 tiles x 5 splits)
+        ("s1 cluster + in-kernel split finish", workloads.gaussian(14, B=1, Hq=8, Hkv=2, Nq=4096, Nkv=4096, d=128,
+                                                                  sigma=0.8), bf.Config(b=256, g=64), dict(stage1_only=True)),
+        ("s1 no cluster (m = 1)", workloads.gaussian(15, B=1, Hq=2, Hkv=2, Nq=4096, Nkv=4096, d=128, sigma=0.8),
+         bf.Config(b=256, g=64), dict(stage1_only=True)),
+        ("s1 cluster + reduce-kernel split finish", workloads.gaussian(16, B=1, Hq=32, Hkv=8, Nq=16384, Nkv=16384,
+                                                                      d=128, sigma=0.8), bf.Config(b=256, g=64),
+         dict(stage1_only=True)),
     ]:
         o = run(prob, cfg, **kw)
         print(f"{name}: ok, |O| max {o.float().abs().max().item():.3f}", flush=True)
