@@ -360,22 +360,26 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     }
     if (stats) cudaMemsetAsync(stats, 0, sizeof(bfla_stats), st);
     if (g.paged) launch_paged_gather(g, P->k, P->page_table, ws + L.kgather, st);
-    // query-group norms come from the scores kernel (Gram diagonal, no extra HBM bytes); key-group
-    // norms (HBM-bound, K only) run on this thread's side stream concurrently, joined before the selection
+    // query-group norms come from the scores kernel (epilogue warps, no extra HBM bytes); key-group
+    // norms (HBM-bound, K only) run on this thread's side stream concurrently, joined before the
+    // selection.  The fork is recorded before the scores kernel but the norms are launched after it, so
+    // the score CTAs (one per SM, all of its shared memory) are dispatched first and the norm CTAs fill
+    // the remaining thread slots — launched first, the norm CTAs took every slot and the two kernels
+    // ran back to back
     static const bool q_norms_separate = experiment_knob("BFLA_QNORM_KERNEL", 0) == 1;  // A/B builds only
     SideStream* ss = side_stream();
+    if (ss) cudaEventRecord(ss->fork, st);
+    float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
+    cudaMemsetAsync(nflag, 0, 16 + tc_tick_bytes(g), st);  // flagged rows, recompute units, split-K tickets
+    const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart,
+                                        reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(nflag) + 16));
     if (ss) {
-      cudaEventRecord(ss->fork, st);
       cudaStreamWaitEvent(ss->s, ss->fork, 0);
       launch_block_norms(gk, P->q, kc, qn, kn, ss->s, q_norms_separate);
       cudaEventRecord(ss->join, ss->s);
     } else {
       launch_block_norms(gk, P->q, kc, qn, kn, st, q_norms_separate);
     }
-    float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
-    cudaMemsetAsync(nflag, 0, 16 + tc_tick_bytes(g), st);  // flagged rows, recompute units, split-K tickets
-    const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart,
-                                        reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(nflag) + 16));
     const bool ragged = g.lens || (g.Nq % g.g) || (g.Nkv % g.g);
     if (!tc_err && ragged && launch_ragged_fixup(gk, P->q, kc, S, st)) {
       if (ss) cudaStreamWaitEvent(st, ss->join, 0);
