@@ -348,6 +348,13 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
       const uint32_t box[4] = {64, (uint32_t)kTcBBox, 1, 1};  // 128-row boxes (64-row boxes measured 1.5x slower)
       if ((s = encode_4d(&tmB, kc, dims, str, box)) != BFLA_OK) return s;
     }
+    CUtensorMap tmB64;  // 64-row boxes of the same K view: B halves of the CTA-pair kernel's half tiles
+    {
+      const uint64_t dims[4] = {(uint64_t)g.g * g.D, (uint64_t)(g.Nkv / g.g), (uint64_t)g.Hkv_real, (uint64_t)g.B};
+      const uint64_t str[3] = {(uint64_t)g.g * g.D * 2, (uint64_t)gk.kvs1 * 2, (uint64_t)gk.kvs0 * 2};
+      const uint32_t box[4] = {64, 64, 1, 1};
+      if ((s = encode_4d(&tmB64, kc, dims, str, box)) != BFLA_OK) return s;
+    }
     CUtensorMap rq, rk;  // token-row maps (64 x 64 SW128 boxes) for the TMA-staged recompute
     bool rmaps;
     {
@@ -372,7 +379,7 @@ static bfla_status run_block_mask(const Geom& g, const bfla_config* cfg, bfla_ma
     float* tcpart = tc_part_bytes(g) ? reinterpret_cast<float*>(ws + L.tcpart) : nullptr;  // split-K partials
     cudaMemsetAsync(nflag, 0, 16 + tc_tick_bytes(g), st);  // flagged rows, recompute units, split-K tickets
     const int tc_err = launch_tc_scores(gk, tmA, tmB, S, q_norms_separate ? nullptr : qn, st, tcpart,
-                                        reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(nflag) + 16));
+                                        reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(nflag) + 16), &tmB64);
     if (ss) {
       cudaStreamWaitEvent(ss->s, ss->fork, 0);
       launch_block_norms(gk, P->q, kc, qn, kn, ss->s, q_norms_separate);

@@ -25,11 +25,13 @@ void launch_select(const Geom& g, const float* S, float c_alpha, int select, flo
 // Fast Stage-1 scores (tcgen05) + certification support (stage1_tc.cu)
 constexpr int kTcTileN = 256;  // key groups per score tile (MMA N)
 constexpr int kTcBBox = 128;   // key-group rows per TMA box of a score B stage
-constexpr int kTcCluster = 2;  // score CTAs per cluster (query heads sharing each K stage by multicast)
+constexpr int kTcCluster = 2;
+constexpr int kTcPair = 1;     // CTA-pair (cta_group::2) score kernel for clusters of two  // score CTAs per cluster (query heads sharing each K stage by multicast)
 size_t tc_scores_smem();
 // qn (optional): the scores kernel also writes the query-group norm bounds (Gram diagonal)
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st, float* part = nullptr, int* tick = nullptr);
+                     cudaStream_t st, float* part = nullptr, int* tick = nullptr,
+                     const CUtensorMap* tmB64 = nullptr);  // 64-row B boxes (CTA-pair kernel, half tiles)
 int tc_splits(const Geom& g);
 size_t tc_part_bytes(const Geom& g);
 size_t tc_tick_bytes(const Geom& g);

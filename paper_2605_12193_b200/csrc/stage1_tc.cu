@@ -141,6 +141,105 @@ __host__ __device__ __forceinline__ bool tc_tile_live(const Geom& g, const Req& 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// Epilogue of a score tile (epilogue warps, thread = query-group row of the tile): split-K bookkeeping
+// (ticket / partials), query-group norm bounds (qduty) and the G x G max-pool into S.
+__device__ __forceinline__ void tc_score_epilogue(const Geom& g, const Req& R, float* __restrict__ S,
+                                                  float* __restrict__ qn, int splits, float* __restrict__ part,
+                                                  float* __restrict__ qpart, int* __restrict__ tick, int* ticket,
+                                                  long long tile, int rp, int p, int r, int mt, int nt, int n_mt,
+                                                  int split, int nlive, uint32_t tmem, int lg, int lane, int row,
+                                                  float sq, bool qduty) {
+  bool last = true;
+  if (splits > 1) {
+    // tick == nullptr: every split publishes its partials and k_s1_tc_reduce finishes the tile
+    if (threadIdx.x == 128) *ticket = tick ? atomicAdd(tick + 2 * tile, 1) : 0;
+    epi_bar();
+    last = tick && *ticket == splits - 1;
+    if (!last) {  // publish the raw partials, count this split done
+      if (qduty) qpart[(((long long)rp * n_mt + mt) * splits + split) * TM + row] = sq;
+      float* pp = part + (tile * splits + split) * (long long)(TN * TM);
+      for (int c0 = 0; c0 < nlive; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) __stcg(pp + (c0 + e) * TM + row, v[e]);  // lanes = consecutive rows
+      }
+      if (tick) {
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) atomicAdd(tick + 2 * tile + 1, 1);
+      }
+    } else {  // the others hold tickets: they are resident and finish their stores
+      if (threadIdx.x == 128) {
+        while (atomicAdd(tick + 2 * tile + 1, 0) < splits - 1) {
+        }
+        __threadfence();
+      }
+      epi_bar();
+      if (qduty) {
+        float a = 0.f;
+        for (int sp = 0; sp < splits; ++sp)
+          a = __fadd_rn(a, sp == split ? sq : __ldcg(qpart + (((long long)rp * n_mt + mt) * splits + sp) * TM + row));
+        sq = a;
+      }
+    }
+  }
+  if (last) {
+    const int grow = mt * TM + row;  // global query group of head p
+    const int ib = grow / g.G, u = grow % g.G;
+    if (qduty) {
+      // full groups only: a partial group's row holds padding (zero-filled or another request's
+      // bytes); its scores come from k_s1_ragged_fixup in the canonical order (exact, no bound needed)
+      const bool ufull = (long long)(grow + 1) * g.g <= R.Nq;
+      float mx = ufull ? sqrtf(fmaxf(sq, 0.f)) : 0.f;
+      for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
+    }
+    // padding-only groups never take the max (R3); partial groups (ragged N, varlen) are left to the
+    // canonical fixup, which rewrites every block score they take part in
+    const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;
+    long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
+    if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
+    float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
+    const float* pp = part + tile * splits * (long long)(TN * TM) + row;
+    for (int c0 = 0; c0 < nlive; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
+      tmem_wait_ld();
+      if (splits > 1) {  // ascending split order: the same sum whichever split finished last
+        float a[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) a[e] = split == 0 ? v[e] : __ldcg(pp + (c0 + e) * TM);
+        for (int sp = 1; sp < splits; ++sp) {
+          const float* ps = pp + (long long)sp * TN * TM + c0 * TM;
+          float b[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) b[e] = sp == split ? v[e] : __ldcg(ps + e * TM);  // 32 loads in flight
+#pragma unroll
+          for (int e = 0; e < 32; ++e) a[e] = __fadd_rn(a[e], b[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = a[e];
+      }
+      for (int jb0 = 0; jb0 < 32; jb0 += g.G) {
+        const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
+        float mx = -INFINITY;
+        for (int vv = 0; vv < g.G; ++vv)
+          if ((long long)(gcol + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);  // full key groups
+        if (!uvalid) mx = -INFINITY;
+        for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const int jb = gcol / g.G;
+        if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
+      }
+    }
+    if (splits > 1 && threadIdx.x == 128) {  // every split has counted itself: reset for the next call
+      tick[2 * tile] = 0;
+      tick[2 * tile + 1] = 0;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, Geom g,
                                                          float* __restrict__ S, int n_mt, int n_nt,
@@ -278,95 +377,8 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
       for (int e = 0; e < 32; ++e)
         if (e == lane) sq = v[e];
     }
-    bool last = true;
-    if (splits > 1) {
-      // tick == nullptr: every split publishes its partials and k_s1_tc_reduce finishes the tile
-      if (threadIdx.x == 128) *ticket = tick ? atomicAdd(tick + 2 * tile, 1) : 0;
-      epi_bar();
-      last = tick && *ticket == splits - 1;
-      if (!last) {  // publish the raw partials, count this split done
-        if (qduty) qpart[(((long long)rp * n_mt + mt) * splits + split) * TM + row] = sq;
-        float* pp = part + (tile * splits + split) * (long long)(TN * TM);
-        for (int c0 = 0; c0 < nlive; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) __stcg(pp + (c0 + e) * TM + row, v[e]);  // lanes = consecutive rows
-        }
-        if (tick) {
-          __threadfence();
-          epi_bar();
-          if (threadIdx.x == 128) atomicAdd(tick + 2 * tile + 1, 1);
-        }
-      } else {  // the others hold tickets: they are resident and finish their stores
-        if (threadIdx.x == 128) {
-          while (atomicAdd(tick + 2 * tile + 1, 0) < splits - 1) {
-          }
-          __threadfence();
-        }
-        epi_bar();
-        if (qduty) {
-          float a = 0.f;
-          for (int sp = 0; sp < splits; ++sp)
-            a = __fadd_rn(a, sp == split ? sq : __ldcg(qpart + (((long long)rp * n_mt + mt) * splits + sp) * TM + row));
-          sq = a;
-        }
-      }
-    }
-    if (last) {
-      const int grow = mt * TM + row;  // global query group of head p
-      const int ib = grow / g.G, u = grow % g.G;
-      if (qduty) {
-        // full groups only: a partial group's row holds padding (zero-filled or another request's
-        // bytes); its scores come from k_s1_ragged_fixup in the canonical order (exact, no bound needed)
-        const bool ufull = (long long)(grow + 1) * g.g <= R.Nq;
-        float mx = ufull ? sqrtf(fmaxf(sq, 0.f)) : 0.f;
-        for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (u == 0 && ib < R.Lq) qn[((long long)r * g.Hq + p) * g.Lq + ib] = mx * (1.0f + 0x1p-10f) + 1e-30f;
-      }
-      // padding-only groups never take the max (R3); partial groups (ragged N, varlen) are left to the
-      // canonical fixup, which rewrites every block score they take part in
-      const bool uvalid = (long long)(grow + 1) * g.g <= R.Nq;
-      long long e_i = (long long)R.Nc + (long long)(ib + 1) * g.b - 1;
-      if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
-      float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
-      const float* pp = part + tile * splits * (long long)(TN * TM) + row;
-      for (int c0 = 0; c0 < nlive; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + c0, v);
-        tmem_wait_ld();
-        if (splits > 1) {  // ascending split order: the same sum whichever split finished last
-          float a[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) a[e] = split == 0 ? v[e] : __ldcg(pp + (c0 + e) * TM);
-          for (int sp = 1; sp < splits; ++sp) {
-            const float* ps = pp + (long long)sp * TN * TM + c0 * TM;
-            float b[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) b[e] = sp == split ? v[e] : __ldcg(ps + e * TM);  // 32 loads in flight
-#pragma unroll
-            for (int e = 0; e < 32; ++e) a[e] = __fadd_rn(a[e], b[e]);
-          }
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = a[e];
-        }
-        for (int jb0 = 0; jb0 < 32; jb0 += g.G) {
-          const int gcol = nt * TN + c0 + jb0;  // first key group of this KV block
-          float mx = -INFINITY;
-          for (int vv = 0; vv < g.G; ++vv)
-            if ((long long)(gcol + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, v[jb0 + vv]);  // full key groups
-          if (!uvalid) mx = -INFINITY;
-          for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          const int jb = gcol / g.G;
-          if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
-        }
-      }
-      if (splits > 1 && threadIdx.x == 128) {  // every split has counted itself: reset for the next call
-        tick[2 * tile] = 0;
-        tick[2 * tile + 1] = 0;
-      }
-    }
+    tc_score_epilogue(g, R, S, qn, splits, part, qpart, tick, ticket, tile, rp, p, r, mt, nt, n_mt, split, nlive,
+                      tmem, lg, lane, row, sq, qduty);
   }
   tc_fence_before();
   __syncthreads();
@@ -376,6 +388,142 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     else tmem_dealloc<TN>(tmem);
   }
   if (csz > 1) cluster_sync_all();  // no CTA leaves while a peer's multicast or commit may target it
+}
+
+// ---- CTA-pair variant (cta_group::2): the two query heads of a cluster form ONE M = 256 MMA.  Each CTA
+// stages its own 128 A rows and HALF of the B tile (N/2 key groups), so a stage is 32 KB instead of 48 and
+// six stages fit (1.5x the bytes in flight per k-step of latency); the leader CTA issues the pair MMAs,
+// whose D rows 0-127 land in its TMEM and 128-255 in the peer's; both CTAs' TMA loads signal the
+// leader's `full` barrier (the peer's own A rows signal the peer's barrier, so its norm warps can read
+// them, and a forwarding warp then arrives on the leader's), the leader's commits release `empty` (and
+// `done`) in both CTAs.  Epilogue,
+// split-K and the query norms (epilogue warps on each CTA's own A rows) are the single-CTA kernel's.
+constexpr int PST = 6;                  // pair stages
+constexpr int PBB = (TN / 2) * TK * 2;  // B half per CTA and stage (16 KB)
+constexpr int PSTAGE = ABYTES + PBB;    // 32 KB
+constexpr int PSMEM = PST * PSTAGE + 2 * PST * 8 + 8 + 16 + 1024;
+
+__global__ void __launch_bounds__(256, 1) k_s1_tc_scores_pair(const __grid_constant__ CUtensorMap tmA,
+                                                              const __grid_constant__ CUtensorMap tmB,
+                                                              const __grid_constant__ CUtensorMap tmB64, Geom g,
+                                                              float* __restrict__ S, int n_mt, int n_nt,
+                                                              float* __restrict__ qn, int splits,
+                                                              float* __restrict__ part, float* __restrict__ qpart,
+                                                              int* __restrict__ tick) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + PST * PSTAGE);
+  uint64_t* empty = full + PST;
+  uint64_t* done = empty + PST;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  int* ticket = reinterpret_cast<int*>(tslot + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int crank = (int)cluster_ctarank();
+  const bool leader = crank == 0;
+  int t = blockIdx.x / 2;
+  const int split = t % splits;
+  t /= splits;
+  const int nt = t % n_nt;
+  t /= n_nt;
+  const int mt = t % n_mt;
+  const int rp = (t / n_mt) * 2 + crank;  // r * Hq + p
+  const long long tile = ((long long)rp * n_mt + mt) * n_nt + nt;
+  const int p = rp % g.Hq, r = rp / g.Hq, h = p / g.m;
+  const Req R = req_of(g, r);
+  int nlive = TN;
+  if (!tc_tile_live(g, R, mt, nt, &nlive)) return;  // uniform over the pair (same mt, nt, request)
+  const bool qduty = qn != nullptr && nt == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PST; ++s) {
+      mbar_init(full + s, leader ? 2 : 1);  // leader: own producer + the peer's forward; peer: own producer
+      mbar_init(empty + s, 1 + (qduty ? 4 : 0));  // the leader's pair commit (+ this CTA's norm warps)
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<TN>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers and TMEM exist before any load or MMA targets them
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int nk = g.g * g.D / TK;
+  const int k0 = (int)((long long)nk * split / splits), k1 = (int)((long long)nk * (split + 1) / splits);
+  const int hb = nlive / 2;  // B rows per CTA
+  if (warp == 0 && lane == 0) {
+    for (int kk = k0; kk < k1; ++kk) {
+      const int s = (kk - k0) % PST;
+      mbar_wait(empty + s, (((kk - k0) / PST) & 1) ^ 1);
+      // leader: own A + both B halves; peer: its own A (its B half counts at the leader)
+      mbar_arrive_expect_tx(full + s, leader ? ABYTES + 2 * hb * TK * 2 : ABYTES);
+      unsigned char* a = smem + s * PSTAGE;
+      tma_load_4d(a, &tmA, full + s, kk * TK, mt * TM, p, r);
+      if (hb == TN / 2)
+        tma_load_4d_pair(a + ABYTES, &tmB, full + s, kk * TK, nt * TN + crank * (TN / 2), h / g.kvdiv, r);
+      else
+        tma_load_4d_pair(a + ABYTES, &tmB64, full + s, kk * TK, nt * TN + crank * (TN / 4), h / g.kvdiv, r);
+    }
+  } else if (warp == 1 && leader) {
+    const uint32_t idesc = idesc_bf16(2 * TM, nlive, 0, 0);
+    const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
+    for (int kk = k0; kk < k1; ++kk) {
+      const int s = (kk - k0) % PST;
+      mbar_wait(full + s, ((kk - k0) / PST) & 1);
+      tc_fence_after();
+      const uint64_t a = d0 + (uint64_t)((s * PSTAGE) >> 4), b = a + (uint64_t)(ABYTES >> 4);
+#pragma unroll
+      for (int k16 = 0; k16 < TK / 16; ++k16)
+        umma_f16_ss_pair_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc,
+                              (kk > k0 || k16) ? 1u : 0u);
+      umma_commit_pair_warp(empty + s, (uint16_t)3u);
+    }
+    umma_commit_pair_warp(done, (uint16_t)3u);
+  } else if (warp == 3 && !leader) {  // forward "the peer's A rows have landed" to the leader's barrier
+    for (int kk = k0; kk < k1; ++kk) {
+      const int s = (kk - k0) % PST;
+      mbar_wait(full + s, ((kk - k0) / PST) & 1);
+      if (lane == 0) mbar_arrive_remote(full + s, 0);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int lg = warp & 3;
+    const int row = lg * 32 + lane;
+    float sq = 0.f;
+    if (qduty) {
+      for (int kk = k0; kk < k1; ++kk) {
+        const int s = (kk - k0) % PST;
+        mbar_wait(full + s, ((kk - k0) / PST) & 1);
+        const uint32_t arow = smem_u32(smem + s * PSTAGE + row * 128);
+        float a8[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t w4[4];
+          ld_shared_v4(arow + (((c + lane) & 7) << 4), w4);
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const float lo = __uint_as_float(w4[f] << 16), hi = __uint_as_float(w4[f] & 0xffff0000u);
+            a8[f] = __fmaf_rn(hi, hi, __fmaf_rn(lo, lo, a8[f]));
+          }
+        }
+        const float part_sq = __fadd_rn(__fadd_rn(a8[0], a8[1]), __fadd_rn(a8[2], a8[3]));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        sq = __fadd_rn(sq, part_sq);
+      }
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    tc_score_epilogue(g, R, S, qn, splits, part, qpart, tick, ticket, tile, rp, p, r, mt, nt, n_mt, split, nlive,
+                      tmem, lg, lane, row, sq, qduty);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's epilogue has read its TMEM; no load or commit still targets either CTA
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<TN>(tmem);
+  }
 }
 
 // Split-K finish: four CTAs (128 threads, thread = query-group row) per tile, one per 64-column
@@ -1133,7 +1281,7 @@ static int tc_cluster(const Geom& g) {
 }
 
 int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& tmB, float* S, float* qn,
-                     cudaStream_t st, float* part, int* tick) {
+                     cudaStream_t st, float* part, int* tick, const CUtensorMap* tmB64) {
   int n_mt, n_nt;
   const long long ctas = tc_tiles(g, &n_mt, &n_nt);
   const int splits = part ? tc_splits(g) : 1;
@@ -1177,8 +1325,18 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
       cfg.numAttrs = 0;
     }
   }
-  e = cudaLaunchKernelEx(&cfg, k_s1_tc_scores, tmA, tmB, g, S, n_mt, n_nt, qn, splits, part, qpart,
-                         fused ? tick : nullptr, csz);
+  // CTA-pair MMA variant (cta_group::2) for clusters of two (A/B: BFLA_S1_PAIR)
+  static const bool pair_knob = experiment_knob("BFLA_S1_PAIR", kTcPair) == 1;
+  if (csz == 2 && pair_knob && tmB64 && kNormWarps) {
+    e = cudaFuncSetAttribute(k_s1_tc_scores_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM);
+    if (e != cudaSuccess) return (int)e;
+    cfg.dynamicSmemBytes = PSMEM;
+    e = cudaLaunchKernelEx(&cfg, k_s1_tc_scores_pair, tmA, tmB, *tmB64, g, S, n_mt, n_nt, qn, splits, part, qpart,
+                           fused ? tick : nullptr);
+  } else {
+    e = cudaLaunchKernelEx(&cfg, k_s1_tc_scores, tmA, tmB, g, S, n_mt, n_nt, qn, splits, part, qpart,
+                           fused ? tick : nullptr, csz);
+  }
   count_launch();
   if (e != cudaSuccess) return (int)e;
   if (splits > 1 && !fused) {
