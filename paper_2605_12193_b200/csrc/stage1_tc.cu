@@ -398,7 +398,10 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 // them, and a forwarding warp then arrives on the leader's), the leader's commits release `empty` (and
 // `done`) in both CTAs.  Epilogue,
 // split-K and the query norms (epilogue warps on each CTA's own A rows) are the single-CTA kernel's.
-constexpr int PST = 6;                  // pair stages
+#ifndef BFLA_S1_PST
+#define BFLA_S1_PST 6
+#endif
+constexpr int PST = BFLA_S1_PST;        // pair stages
 constexpr int PBB = (TN / 2) * TK * 2;  // B half per CTA and stage (16 KB)
 constexpr int PSTAGE = ABYTES + PBB;    // 32 KB
 constexpr int PSMEM = PST * PSTAGE + 2 * PST * 8 + 8 + 16 + 1024;
