@@ -536,6 +536,9 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores_pair(const __grid_const
 #ifndef BFLA_RED_COLS
 #define BFLA_RED_COLS 16  // A/B (profiles/r3_s1_reduce_cols.txt): 64 -> 16 cols: 32K 0.198 -> 0.194, 16K 0.169 -> 0.132 ms
 #endif
+#if BFLA_RED_COLS % 16
+#error "BFLA_RED_COLS must be a multiple of 16 (the G <= 16 max pyramid)"
+#endif
 constexpr int kRedCols = BFLA_RED_COLS;  // key-group columns per reduce CTA
 __global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict__ S, int n_mt, int n_nt,
                                                       float* __restrict__ qn, int splits,
@@ -567,29 +570,40 @@ __global__ void __launch_bounds__(128) k_s1_tc_reduce(Geom g, float* __restrict_
   if (e_i > R.Nkv - 1) e_i = R.Nkv - 1;
   float* srow = S + (((long long)r * g.Hq + p) * g.Lq + ib) * g.Lkv;
   const float* pp = part + tile * splits * (long long)(TN * TM) + row;
-  const int c_end = min(nlive, (cg + 1) * kRedCols);
-  for (int jb0 = cg * kRedCols; jb0 < c_end; jb0 += g.G) {
-    const int gcol = nt * TN + jb0;
-    float mx = -INFINITY;
-    for (int v0 = 0; v0 < g.G; v0 += 8) {  // G <= 16: one or two chunks of 8 key groups
-      float a[8];
+  const int c0 = cg * kRedCols;
+  if (c0 >= nlive) return;
+  // all kRedCols columns of every split in flight at once (fully unrolled, static register indexing)
+  float a[kRedCols];
 #pragma unroll
-      for (int vv = 0; vv < 8; ++vv) a[vv] = v0 + vv < g.G ? __ldg(pp + (long long)(jb0 + v0 + vv) * TM) : 0.f;
-      for (int sp = 1; sp < splits; ++sp) {
-        float b[8];
+  for (int c = 0; c < kRedCols; ++c) a[c] = __ldg(pp + (long long)(c0 + c) * TM);
+  for (int sp = 1; sp < splits; ++sp) {  // ascending split order
+    float b[kRedCols];
 #pragma unroll
-        for (int vv = 0; vv < 8; ++vv)
-          b[vv] = v0 + vv < g.G ? __ldg(pp + ((long long)sp * TN + jb0 + v0 + vv) * TM) : 0.f;
+    for (int c = 0; c < kRedCols; ++c) b[c] = __ldg(pp + ((long long)sp * TN + c0 + c) * TM);
 #pragma unroll
-        for (int vv = 0; vv < 8; ++vv) a[vv] += b[vv];
-      }
+    for (int c = 0; c < kRedCols; ++c) a[c] += b[c];
+  }
 #pragma unroll
-      for (int vv = 0; vv < 8; ++vv)
-        if (v0 + vv < g.G && (long long)(gcol + v0 + vv + 1) * g.g <= R.Nkv) mx = fmaxf(mx, a[vv]);
-    }
+  for (int c = 0; c < kRedCols; ++c)  // full, live key groups only
+    if (c0 + c >= nlive || (long long)(nt * TN + c0 + c + 1) * g.g > R.Nkv) a[c] = -INFINITY;
+  // max over each block's G key groups: a pyramid of pairwise maxima, read at the level of G
+  float m2[kRedCols / 2], m4[kRedCols / 4], m8[kRedCols / 8], m16[kRedCols / 16];
+#pragma unroll
+  for (int c = 0; c < kRedCols / 2; ++c) m2[c] = fmaxf(a[2 * c], a[2 * c + 1]);
+#pragma unroll
+  for (int c = 0; c < kRedCols / 4; ++c) m4[c] = fmaxf(m2[2 * c], m2[2 * c + 1]);
+#pragma unroll
+  for (int c = 0; c < kRedCols / 8; ++c) m8[c] = fmaxf(m4[2 * c], m4[2 * c + 1]);
+#pragma unroll
+  for (int c = 0; c < kRedCols / 16; ++c) m16[c] = fmaxf(m8[2 * c], m8[2 * c + 1]);
+#pragma unroll
+  for (int k = 0; k < kRedCols; ++k) {
+    if (k >= kRedCols / g.G) break;  // G uniform over the grid
+    float mx = g.G == 1 ? a[k] : g.G == 2 ? m2[k % (kRedCols / 2)] : g.G == 4 ? m4[k % (kRedCols / 4)]
+             : g.G == 8 ? m8[k % (kRedCols / 8)] : m16[k % (kRedCols / 16)];
     if (!uvalid) mx = -INFINITY;
     for (int o = 1; o < g.G; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int jb = gcol / g.G;
+    const int jb = (nt * TN + c0) / g.G + k;
     if (u == 0 && ib < R.Lq && jb < R.Lkv && (long long)jb * g.b <= e_i) srow[jb] = mx;
   }
 }
