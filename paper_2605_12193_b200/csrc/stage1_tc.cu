@@ -25,13 +25,6 @@ constexpr int TM = 128;   // query groups per tile (MMA M)
 constexpr int TN = kTcTileN;  // key groups per tile (MMA N = 256)
 constexpr int TK = 64;    // K elements per stage (one 128-byte swizzle row)
 constexpr int ST = 4;     // pipeline stages (48 KB each)
-// Query norms: summed by the idle epilogue warps from the A stages (default), or from a Gram A A^T on
-// the tensor pipe (BFLA_S1_GRAM, the round-2 design; A/B in DESIGN.md §7.0)
-#ifdef BFLA_S1_GRAM
-constexpr bool kNormWarps = false;
-#else
-constexpr bool kNormWarps = true;
-#endif
 constexpr int kBBox = kTcBBox;  // B rows per TMA box (at csz > 2 some cluster CTAs fetch none)
 constexpr int ABYTES = TM * TK * 2;
 constexpr int BBYTES = TN * TK * 2;
@@ -245,13 +238,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
                                                          float* __restrict__ S, int n_mt, int n_nt,
                                                          float* __restrict__ qn, int splits,
                                                          float* __restrict__ part, float* __restrict__ qpart,
-                                                         int* __restrict__ tick, int csz_arg) {
-#ifdef BFLA_S1_NOCLUSTER
-  constexpr int csz = 1;  // A/B: the cluster-free code generation
-  (void)csz_arg;
-#else
-  const int csz = csz_arg;
-#endif
+                                                         int* __restrict__ tick, int csz) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * (ABYTES + BBYTES));
@@ -281,15 +268,12 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, csz + (qduty && kNormWarps ? 4 : 0));  // every cluster CTA's MMA commit (+ norm warps)
+      mbar_init(empty + s, csz + (qduty ? 4 : 0));  // every cluster CTA's MMA commit (+ norm warps)
     }
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 2) {
-    if (qduty && !kNormWarps) tmem_alloc<2 * TN>(tslot);  // + the Gram A A^T (columns 256-383)
-    else tmem_alloc<TN>(tslot);
-  }
+  if (warp == 2) tmem_alloc<TN>(tslot);
   tc_fence_before();
   __syncthreads();
   if (csz > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
@@ -324,12 +308,6 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
 #pragma unroll
       for (int k16 = 0; k16 < TK / 16; ++k16)
         umma_f16_ss_warp(tmem, a + (uint64_t)(k16 * 2), b + (uint64_t)(k16 * 2), idesc, (kk > k0 || k16) ? 1u : 0u);
-      if (qduty && !kNormWarps) {
-#pragma unroll
-        for (int k16 = 0; k16 < TK / 16; ++k16)
-          umma_f16_ss_warp(tmem + TN, a + (uint64_t)(k16 * 2), a + (uint64_t)(k16 * 2), idesc_bf16(TM, TM, 0, 0),
-                           (kk > k0 || k16) ? 1u : 0u);
-      }
       if (csz > 1) umma_commit_mc_warp(empty + s, (uint16_t)((1u << csz) - 1u));  // B slots are shared
       else umma_commit_warp(empty + s);
     }
@@ -338,7 +316,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     const int lg = warp & 3;
     const int row = lg * 32 + lane;  // query group within the tile
     float sq = 0.f;                  // ||x_row||^2 over this split's k-range (qduty)
-    if (qduty && kNormWarps) {
+    if (qduty) {
       // the row's 128 bytes of each A stage (SWIZZLE_128B permutes its eight 16-byte chunks within the
       // row; a sum of squares does not care).  Chunk (c + lane) & 7: the eight rows of a quarter warp
       // hit eight distinct chunk positions, so every LDS.128 wavefront covers all 32 banks once.
@@ -369,14 +347,6 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
     }
     mbar_wait(done, 0);
     tc_fence_after();
-    if (qduty && !kNormWarps) {  // ||x_row||^2 = (A A^T)[row][row]: this warp's lanes x columns [32 lg, 32 lg + 32)
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + TN + lg * 32, v);
-      tmem_wait_ld();
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (e == lane) sq = v[e];
-    }
     tc_score_epilogue(g, R, S, qn, splits, part, qpart, tick, ticket, tile, rp, p, r, mt, nt, n_mt, split, nlive,
                       tmem, lg, lane, row, sq, qduty);
   }
@@ -384,8 +354,7 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores(const __grid_constant__
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    if (qduty && !kNormWarps) tmem_dealloc<2 * TN>(tmem);
-    else tmem_dealloc<TN>(tmem);
+    tmem_dealloc<TN>(tmem);
   }
   if (csz > 1) cluster_sync_all();  // no CTA leaves while a peer's multicast or commit may target it
 }
@@ -529,10 +498,10 @@ __global__ void __launch_bounds__(256, 1) k_s1_tc_scores_pair(const __grid_const
   }
 }
 
-// Split-K finish: four CTAs (128 threads, thread = query-group row) per tile, one per 64-column
-// group; sums the splits in ascending order, then the epilogue of k_s1_tc_scores (Gram diagonal ->
-// query norms; G x G max).  Loads are column-major partials: a warp reads 128 contiguous bytes, and
-// the G x splits loads of a block column are independent (in flight together).
+// Split-K finish: TN / kRedCols CTAs (128 threads, thread = query-group row) per tile, one per
+// kRedCols-column group; sums the splits in ascending order, then the epilogue of k_s1_tc_scores
+// (query-norm partials -> query norms; G x G max).  Loads are column-major partials: a warp reads 128
+// contiguous bytes, and every load of the CTA's columns and splits is in flight together.
 #ifndef BFLA_RED_COLS
 #define BFLA_RED_COLS 16  // A/B (profiles/r3_s1_reduce_cols.txt): 64 -> 16 cols: 32K 0.198 -> 0.194, 16K 0.169 -> 0.132 ms
 #endif
@@ -1344,7 +1313,7 @@ int launch_tc_scores(const Geom& g, const CUtensorMap& tmA, const CUtensorMap& t
   }
   // CTA-pair MMA variant (cta_group::2) for clusters of two (A/B: BFLA_S1_PAIR)
   static const bool pair_knob = experiment_knob("BFLA_S1_PAIR", kTcPair) == 1;
-  if (csz == 2 && pair_knob && tmB64 && kNormWarps) {
+  if (csz == 2 && pair_knob && tmB64) {
     e = cudaFuncSetAttribute(k_s1_tc_scores_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM);
     if (e != cudaSuccess) return (int)e;
     cfg.dynamicSmemBytes = PSMEM;
