@@ -25,13 +25,13 @@ __device__ __forceinline__ float exp2_canon(float t) {
   return __fmul_rn(p, __int_as_float((n + 127) << 23));
 }
 
+// 64-bit warp max with two redux.sync reductions: the largest high word, then the largest low word
+// among the lanes holding it (the same value as a shuffle tree, in 2 instead of 10 shuffles)
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
-  }
-  return v;
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? (uint32_t)v : 0u);
+  return ((unsigned long long)mh << 32) | ml;
 }
 
 // Selection of one head row (r, p, i) by one warp (Eq. 13-18):
