@@ -85,11 +85,11 @@ def _diffuse_counts(seed, B=1, H=8, tq=256, dense_heads=1):
 
 
 @pytest.mark.parametrize("parts", [1, 2, 4, 8, 16])
-@pytest.mark.parametrize("dense_heads", [0, 1, 3])
-def test_plan_pieces_covers_every_tile_once(parts, dense_heads):
+@pytest.mark.parametrize("dense_heads,B", [(0, 1), (1, 1), (3, 1), (1, 2)])
+def test_plan_pieces_covers_every_tile_once(parts, dense_heads, B):
     from paper_2605_12193_b200 import parallel
 
-    counts = _diffuse_counts(parts + dense_heads, dense_heads=dense_heads)
+    counts = _diffuse_counts(parts + dense_heads, B=B, dense_heads=dense_heads)
     plan = parallel.plan_pieces(counts, parts)
     kept, ext = parallel._lpt_rows(counts)
     assert len(plan) == parts
